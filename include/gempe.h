@@ -1,0 +1,208 @@
+/* gempe.h -- C ABI of the B200-native GEMPE hot path (libgempe_b200.so).
+ *
+ * Drop-in boundary for ONE path of the reference library "entropy-embed"
+ * (/root/reference/proj; file:line citations below are relative to it): one Jacobi round of
+ * EmbeddingEngine::run_single_iteration (src/engine.cpp:278-325) -- edge terms, hash-verified
+ * sampled non-edge terms, per-vertex reduction of (y, z) and the update x = y / z -- plus the
+ * one-time preparation that defines its inputs (relabel, initial coordinates, edge hash set).
+ *
+ * The reference has no FFI layer; its boundary is the C++ surface of
+ * include/entropy_embed/engine.hpp:112-171.  Every entry point below names the reference
+ * interface it replaces.  Plain pointers and sizes only; all host pointers are caller-owned and
+ * copied.  One context per GPU and per host thread; contexts are not re-entrant (same contract
+ * as the reference engine).
+ *
+ * Return codes mirror the CLI's exit codes (tools/embed_main.cpp:214-230):
+ *   0 ok, 1 config_error, 2 data_error (incl. near_complete_graph_error), 3 divergence_error,
+ *   4 CUDA runtime failure (no reference analogue; there is NO CPU fallback).
+ */
+#ifndef GEMPE_H_
+#define GEMPE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GEMPE_OK 0
+#define GEMPE_ERR_CONFIG 1
+#define GEMPE_ERR_DATA 2
+#define GEMPE_ERR_DIVERGENCE 3
+#define GEMPE_ERR_CUDA 4
+
+#define GEMPE_HIST_BINS 512 /* include/entropy_embed/histogram.hpp:15-16: 512 bins over [0,12) */
+
+/* negative-sampling scheme */
+#define GEMPE_NEG_PER_EDGE_2 0   /* reference: 2 draws per edge (src/engine.cpp:227-249) */
+#define GEMPE_NEG_PER_VERTEX_K 1 /* BASELINE.json: k draws per vertex, stream key (seed,iter,v,draw) */
+/* math policy for e^{-x^2}/erfc(x) */
+#define GEMPE_MATH_TABLES 0 /* FastMath piecewise tables (include/entropy_embed/piecewise.hpp:72-79) */
+#define GEMPE_MATH_EXACT 1  /* ExactMath (include/entropy_embed/sigmoid.hpp:61-65) */
+/* sample-stream generator */
+#define GEMPE_RNG_REFERENCE 0 /* expand_seed32 + LCG replay (include/entropy_embed/rng.hpp:31-34,82-86) */
+#define GEMPE_RNG_PHILOX 1    /* Philox4x32-10 keyed (seed,iter), counter (slot,try); not a parity mode */
+/* initial-coordinate rule */
+#define GEMPE_INIT_REFERENCE 0 /* init_embedding: U[0,1) SplitMix stream (src/engine.cpp:116-124) */
+#define GEMPE_INIT_UNIFORM_PM1 1 /* U(-1,1)  (BASELINE.json configs 1-2) */
+#define GEMPE_INIT_NORMAL 2      /* N(0, std^2) (BASELINE.json configs 3-5, std = 0.01) */
+
+typedef struct gempe_ctx gempe_ctx;
+
+typedef struct gempe_options {
+  uint32_t dim;           /* embedding dimension d >= 1 (EmbeddingEngine ctor, src/engine.cpp:152) */
+  int32_t hash_bits;      /* 0 = auto (next pow2 >= 64 m, cap 2^31), else [1,31] (src/hash_set.cpp:13-24) */
+  uint64_t seed;          /* run seed */
+  int32_t neg_mode;       /* GEMPE_NEG_* */
+  uint32_t negatives;     /* k for PER_VERTEX_K (ignored for PER_EDGE_2) */
+  int32_t math;           /* GEMPE_MATH_* */
+  int32_t rng;            /* GEMPE_RNG_* */
+  int32_t relabel;        /* 1 = apply random_relabel(mix_seed(seed,0xA11BE11)) as the reference ctor does
+                             (src/engine.cpp:161-163); 0 = ids are used as work ids */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t rank, world;    /* vertex sharding, one process per GPU; world = 1 for a single GPU */
+  int32_t comm_chunks;    /* all-gather pipeline depth (>= 1; forced to 1 when world == 1) */
+  uint32_t chunk_entries; /* hub split: max adjacency entries per work item (0 = default) */
+  int32_t deterministic;  /* 1 = sort incoming-sample buckets so the fp32 sums are run-to-run identical */
+} gempe_options;
+
+/* Fills *opt with defaults (dim must still be set). */
+void gempe_default_options(gempe_options* opt);
+
+/* Replaces EmbeddingEngine::EmbeddingEngine (src/engine.cpp:143-180): copies the graph (ORIGINAL ids),
+ * relabels, builds the edge hash set, the both-direction CSR and the work-item table on `device`, and
+ * initialises coordinates with the reference rule.  n <= 1 or m == 0 yields a degenerate context
+ * (gempe_is_degenerate) on which gempe_iterate returns GEMPE_ERR_CONFIG, as the reference does. */
+int gempe_create(gempe_ctx** out, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                 const gempe_options* opt);
+void gempe_destroy(gempe_ctx* ctx);
+/* Message of the last failure on this context (ctx == NULL: last failure of gempe_create on this thread). */
+const char* gempe_last_error(const gempe_ctx* ctx);
+
+int gempe_is_degenerate(const gempe_ctx* ctx);              /* EmbeddingEngine::degenerate() */
+int gempe_hash_bits(const gempe_ctx* ctx);                  /* EdgeHashSet::bits() */
+uint64_t gempe_sample_slots(const gempe_ctx* ctx);          /* S: 2m (PER_EDGE_2) or n*k */
+uint64_t gempe_pair_terms(const gempe_ctx* ctx);            /* m + S: pair-terms per iteration */
+uint64_t gempe_algorithmic_bytes(const gempe_ctx* ctx);     /* B_alg of SURVEY.md 8(d) with p = 1 */
+
+/* EmbeddingEngine::work_graph() and the original->work permutation (src/engine.cpp:182-194).
+ * Any pointer may be NULL. */
+int gempe_get_work_graph(const gempe_ctx* ctx, uint32_t* src, uint32_t* dst, uint32_t* to_work);
+
+/* Coordinates in WORK indexing, n*dim row-major fp32 (EmbeddingEngine::work_coords()).  The reference has
+ * no setter; set_coords exists for teacher-forced parity runs and custom initial layouts. */
+int gempe_set_coords(gempe_ctx* ctx, const float* x_work);
+int gempe_get_coords(gempe_ctx* ctx, float* x_work);
+int gempe_init_coords(gempe_ctx* ctx, int rule, uint64_t seed, double std);
+
+/* Re-relabel (EmbeddingEngine::apply_relabel, src/engine.cpp:182-194): permutes the work graph and the
+ * coordinates with random_relabel(relabel_seed) and rebuilds hash set, CSR and work items. */
+int gempe_relabel(gempe_ctx* ctx, uint64_t relabel_seed);
+
+/* One Jacobi round = accumulate_worker + reduce_and_update (src/engine.cpp:196-276) for the stream index
+ * `iter_index` (the reference's iter_), with the (mu, sigma) of SigmoidParams.  Blocks until the round is
+ * complete; fills the 2 x 512 distance tallies (DistanceHistogram::record, histogram.hpp:24-29; either may
+ * be NULL).  Returns GEMPE_ERR_DIVERGENCE on a non-finite coordinate (src/engine.cpp:273-275, the state is
+ * then undefined) and GEMPE_ERR_DATA when a sample stream hit the 10^4 retry cap (src/sampler.cpp:18-21). */
+int gempe_iterate(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index,
+                  uint64_t* hist_edge, uint64_t* hist_nonedge);
+
+/* Same round, enqueue-only: no host synchronisation.  gempe_sync waits, checks the status word and
+ * returns the tallies of the LAST round. */
+int gempe_iterate_async(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index);
+int gempe_sync(gempe_ctx* ctx, uint64_t* hist_edge, uint64_t* hist_nonedge);
+
+/* IterationCapture (include/entropy_embed/engine.hpp:92-96): consolidated y (n*dim) and z (n) of the last
+ * round, in double.  Capture must be switched on before the round. */
+int gempe_set_capture(gempe_ctx* ctx, int on);
+int gempe_get_yz(gempe_ctx* ctx, double* y, double* z);
+
+/* Bit-exact test hooks.
+ * gempe_probe  == EdgeHashSet::maybe_edge (include/entropy_embed/hash_set.hpp:28-30) on WORK ids.
+ * gempe_sample == the accepted partners of sample_non_edges (src/sampler.cpp:7-31) for every stream of
+ *   round `iter_index`: PER_EDGE_2 slot 2*e+draw (anchor src[e] / dst[e]); PER_VERTEX_K slot v*k+draw.
+ *   total_draws (may be NULL) receives the number of LCG draws, rejected ones included. */
+int gempe_probe(gempe_ctx* ctx, const uint32_t* i, const uint32_t* j, uint64_t count, uint8_t* out);
+int gempe_sample(gempe_ctx* ctx, uint64_t iter_index, uint32_t* partners, uint64_t* total_draws);
+
+/* ---- plumbing for one-process-per-GPU drivers (streams, NCCL all-gather of updated shards) ---------- */
+int gempe_set_stream(gempe_ctx* ctx, void* cuda_stream);           /* cudaStream_t; NULL = context's own */
+void* gempe_device_coords(gempe_ctx* ctx, int which);              /* 0 = X_t (read), 1 = X_{t+1} (written) */
+uint32_t gempe_row_stride(const gempe_ctx* ctx);                   /* floats per row in device layout */
+uint32_t gempe_padded_rows(const gempe_ctx* ctx);                  /* world*comm_chunks*block rows */
+uint32_t gempe_block_rows(const gempe_ctx* ctx);                   /* rows per (chunk, rank) ownership block */
+int gempe_begin_round(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index); /* sampling passes */
+int gempe_gather_chunk(gempe_ctx* ctx, int chunk);                 /* gradient+update for one comm chunk */
+int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t / X_{t+1} */
+/* Device time in ms of the last `rounds` enqueued through gempe_iterate_async since the previous call
+ * (CUDA events on the context's stream), split as {total, sampling passes, gather+update}. */
+int gempe_elapsed_ms(gempe_ctx* ctx, float out3[3]);
+uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels launched so far */
+
+/* ---- host-side numerics of the path (no GPU needed) ------------------------------------------------ */
+/* FastMath::build tables (src/piecewise.cpp:182-195). which: 0 erf, 1 exp_neg, 2 ratio.
+ * out67 = knots[17] a[16] b[16] c[16] lo hi.  Returns odd_mirror (0/1) or a negative error. */
+int gempe_host_fastmath_table(int which, double* out67);
+/* optimize_sigma_detail / histogram_objective(_dsigma) (src/slope.cpp:27-51, 75-125). */
+double gempe_host_optimize_sigma(const uint64_t* hist_edge, const uint64_t* hist_nonedge,
+                                 double nonedge_weight, double mu, int* bisection_steps);
+double gempe_host_histogram_objective(const uint64_t* hist_edge, const uint64_t* hist_nonedge,
+                                      double nonedge_weight, double mu, double sigma);
+double gempe_host_histogram_objective_dsigma(const uint64_t* hist_edge, const uint64_t* hist_nonedge,
+                                             double nonedge_weight, double mu, double sigma);
+/* random_relabel (src/graph.cpp:182-194): forward[original] = relabeled. */
+int gempe_host_random_relabel(uint32_t n, uint64_t seed, uint32_t* forward);
+uint64_t gempe_host_mix_seed(uint64_t seed, uint64_t component);   /* include/entropy_embed/rng.hpp:26-28 */
+
+/* ---- run-level facade: EmbeddingEngine / embed() (include/entropy_embed/engine.hpp:112-171) ------- */
+typedef struct gempe_engine gempe_engine;
+
+typedef struct gempe_iteration_config { /* IterationConfig, engine.hpp:29-38 */
+  int32_t max_iters;          /* 100 */
+  uint32_t lane_width;        /* accepted for source compatibility; sample streams do not depend on it */
+  uint32_t workers;           /* accepted for source compatibility; unused on the GPU */
+  double convergence_tol;     /* 1e-4 */
+  int32_t convergence_window; /* 5 */
+  int32_t relabel_period;     /* 0 */
+  int32_t fast_math;          /* 1 = tables */
+  int32_t hash_bits;          /* 0 = auto */
+  /* extensions (zero = reference behaviour) */
+  int32_t neg_mode;
+  uint32_t negatives;
+  int32_t device;
+} gempe_iteration_config;
+
+typedef struct gempe_embed_result { /* EmbedResult, engine.hpp:98-107 */
+  float* embedding;           /* n*dim, ORIGINAL indexing; caller-provided */
+  double* pe_trace;           /* caller-provided, capacity pe_trace_cap */
+  int32_t pe_trace_cap;
+  int32_t pe_trace_len;
+  double final_sigma;
+  int32_t converged;
+  int32_t degenerate;
+  int32_t iterations;
+  uint32_t* relabel_forward;  /* n, may be NULL */
+  uint64_t* last_hist_edge;   /* 512, may be NULL */
+  uint64_t* last_hist_nonedge;
+  double last_nonedge_weight;
+} gempe_embed_result;
+
+void gempe_default_iteration_config(gempe_iteration_config* cfg);
+int gempe_engine_create(gempe_engine** out, uint32_t n, uint64_t m, const uint32_t* src,
+                        const uint32_t* dst, uint32_t dim, const gempe_iteration_config* cfg,
+                        uint64_t seed);
+void gempe_engine_destroy(gempe_engine* e);
+const char* gempe_engine_last_error(const gempe_engine* e);
+gempe_ctx* gempe_engine_context(gempe_engine* e);                   /* borrowed */
+int gempe_engine_degenerate(const gempe_engine* e);
+int gempe_engine_iteration(const gempe_engine* e);                  /* EmbeddingEngine::iteration() */
+double gempe_engine_sigma(const gempe_engine* e);                   /* params().sigma */
+/* EmbeddingEngine::run_single_iteration (src/engine.cpp:278-325). */
+int gempe_engine_run_single_iteration(gempe_engine* e, double* pe_estimate, double* sigma);
+/* EmbeddingEngine::run (src/engine.cpp:339-382). */
+int gempe_engine_run(gempe_engine* e, gempe_embed_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEMPE_H_ */

@@ -1,0 +1,645 @@
+// C-ABI of the device path (include/gempe.h): context construction (relabel, CSR, work items, hash set),
+// the per-round launch sequence and the test hooks.  Citations are relative to /root/reference/proj.
+#include "context.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+
+namespace gempe {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const divergence_error*>(&e)) return GEMPE_ERR_DIVERGENCE;
+  if (dynamic_cast<const config_error*>(&e)) return GEMPE_ERR_CONFIG;
+  if (dynamic_cast<const data_error*>(&e)) return GEMPE_ERR_DATA;
+  if (dynamic_cast<const cuda_error*>(&e)) return GEMPE_ERR_CUDA;
+  return GEMPE_ERR_DATA;
+}
+
+}  // namespace
+void set_create_error(const std::string& msg) { g_create_error = msg; }
+namespace {
+
+template <typename Fn>
+int guarded(gempe_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    return GEMPE_OK;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->error = e.what();
+    else g_create_error = e.what();
+    return code_of(e);
+  }
+}
+
+std::uint32_t row_stride_for(std::uint32_t dim) { return dim <= 2 ? dim : (dim + 3u) & ~3u; }
+
+std::uint32_t lanes_per_row(std::uint32_t ld) {
+  std::uint32_t lpr = 1;
+  while (lpr < 32 && lpr * 4 < ld) lpr <<= 1;
+  return lpr;
+}
+
+void pack_tables(DeviceTables& out) {
+  const FastMathTables& t = FastMathTables::get();
+  auto pack = [](const QuadTable& q, double* dst) {
+    for (int i = 0; i <= kSegments; ++i) dst[i] = q.knots[i];
+    for (int i = 0; i < kSegments; ++i) {
+      dst[17 + i] = q.a[i];
+      dst[33 + i] = q.b[i];
+      dst[49 + i] = q.c[i];
+    }
+  };
+  pack(t.erf, out.erf);
+  pack(t.ratio, out.ratio);
+}
+
+void set_round_math(gempe_ctx* c, double mu, double sigma) {
+  if (!(sigma > 0.0) || !std::isfinite(sigma) || !std::isfinite(mu)) throw config_error("sigma must be positive and finite");
+  const double pi = 3.14159265358979323846264338327950288, ln2 = 0.693147180559945309417232121458176568;
+  const double c1 = 2.0 / (pi * ln2);
+  const double c2 = 1.0 / (2.50662827463100050241576528481 * ln2);
+  RoundMath& m = c->math;
+  m.mu = mu;
+  m.inv_sqrt2_sigma = 1.0 / (1.41421356237309504880168872420969808 * sigma);
+  m.A = c1 / (sigma * sigma);
+  m.B = c2 / (sigma * sigma * sigma);
+  m.C = c2 / sigma;
+  m.exact = c->opt.math == GEMPE_MATH_EXACT;
+}
+
+// Builds every graph-derived device structure from the current host work graph.
+void build_structures(gempe_ctx* c) {
+  const std::uint32_t n = c->n;
+  const std::uint64_t m = c->m;
+  const auto& src = c->work_src;
+  const auto& dst = c->work_dst;
+
+  // both-direction CSR in edge order; eid_role = 2*e + role keys the PER_EDGE_2 sample streams
+  std::vector<std::uint32_t> rowptr(static_cast<std::size_t>(n) + 1, 0);
+  for (std::uint64_t e = 0; e < m; ++e) {
+    ++rowptr[src[e] + 1];
+    ++rowptr[dst[e] + 1];
+  }
+  for (std::uint32_t v = 0; v < n; ++v) rowptr[v + 1] += rowptr[v];
+  std::vector<std::uint32_t> nbr(2 * m), cursor(rowptr.begin(), rowptr.end() - 1);
+  const bool per_edge = c->opt.neg_mode == GEMPE_NEG_PER_EDGE_2;
+  std::vector<std::uint32_t> eid_role, csr_src;
+  if (per_edge) {
+    eid_role.resize(2 * m);
+    csr_src.resize(2 * m);
+  }
+  for (std::uint64_t e = 0; e < m; ++e) {
+    const std::uint32_t p0 = cursor[src[e]]++, p1 = cursor[dst[e]]++;
+    nbr[p0] = dst[e];
+    nbr[p1] = src[e];
+    if (per_edge) {
+      eid_role[p0] = static_cast<std::uint32_t>(2 * e);
+      eid_role[p1] = static_cast<std::uint32_t>(2 * e + 1);
+      csr_src[p0] = src[e];
+      csr_src[p1] = dst[e];
+    }
+  }
+
+  // work items: one per owned vertex, hubs split every chunk_entries adjacency positions
+  std::vector<uint4> items;
+  std::vector<std::uint32_t> hub_first, hub_items;
+  std::uint32_t parts = 0;
+  c->chunk_item_off.assign(c->comm_chunks + 1, 0);
+  const std::uint32_t world = static_cast<std::uint32_t>(c->opt.world), rank = static_cast<std::uint32_t>(c->opt.rank);
+  for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
+    c->chunk_item_off[chunk] = static_cast<std::uint32_t>(items.size());
+    const std::uint64_t block = static_cast<std::uint64_t>(chunk) * world + rank;
+    const std::uint64_t lo = std::min<std::uint64_t>(n, block * c->block_rows);
+    const std::uint64_t hi = std::min<std::uint64_t>(n, (block + 1) * c->block_rows);
+    for (std::uint32_t v = static_cast<std::uint32_t>(lo); v < hi; ++v) {
+      const std::uint32_t deg = rowptr[v + 1] - rowptr[v];
+      const std::uint32_t pieces = std::max(1u, (deg + c->chunk_entries - 1) / c->chunk_entries);
+      if (pieces == 1) {
+        items.push_back(make_uint4(v, rowptr[v], kNoHub, 0));
+      } else {
+        const std::uint32_t hub = static_cast<std::uint32_t>(hub_first.size());
+        hub_first.push_back(parts);
+        hub_items.push_back(pieces);
+        for (std::uint32_t p = 0; p < pieces; ++p) {
+          items.push_back(make_uint4(v, rowptr[v] + p * c->chunk_entries, hub, p));
+        }
+        parts += pieces;
+      }
+    }
+  }
+  c->chunk_item_off[c->comm_chunks] = static_cast<std::uint32_t>(items.size());
+
+  c->rowptr.upload(rowptr);
+  c->nbr.upload(nbr);
+  c->eid_role.upload(eid_role);
+  c->csr_src.upload(csr_src);
+  c->items.upload(items);
+  c->hub_first.upload(hub_first);
+  c->hub_items.upload(hub_items);
+  c->hub_arrived.allocate(hub_first.size(), true);
+  c->part_y.allocate(static_cast<std::size_t>(parts) * c->ld);
+  c->part_z.allocate(parts);
+
+  c->slots = per_edge ? 2 * m : static_cast<std::uint64_t>(n) * c->opt.negatives;
+  c->neg_own.allocate(c->slots);
+  c->in_rank.allocate(c->slots);
+  c->in_anchor.allocate(c->slots);
+  c->in_cnt.allocate(n);
+  c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
+  c->scan_scratch.allocate((n + 4095) / 4096 + 2);
+
+  // edge hash set, bit-packed (hash_set.cpp:9-34)
+  c->hash_bits = auto_hash_bits(m, c->opt.hash_bits);
+  const std::uint64_t cells = 1ull << c->hash_bits;
+  c->hash_words.allocate(std::max<std::uint64_t>(1, cells / 32), true);
+  {
+    DeviceBuffer<std::uint32_t> d_src, d_dst;
+    d_src.upload(src);
+    d_dst.upload(dst);
+    c->launches += launch_hash_build(d_src.get(), d_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
+                                     c->hash_words.get(), c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "hash build");
+  }
+  if (c->capture) {
+    c->cap_y.allocate(static_cast<std::size_t>(n) * c->dim, true);
+    c->cap_z.allocate(n, true);
+  }
+}
+
+SampleArgs sample_args(gempe_ctx* c, std::uint64_t iter) {
+  SampleArgs a{};
+  a.n = c->n;
+  a.slots = c->slots;
+  a.neg_mode = c->opt.neg_mode;
+  a.k = c->opt.negatives;
+  a.rng = c->opt.rng;
+  a.stream_base = c->opt.rng == GEMPE_RNG_REFERENCE ? mix_seed(c->opt.seed, iter) : c->opt.seed;
+  a.iter = iter;
+  a.csr_src = c->csr_src.get();
+  a.eid_role = c->eid_role.get();
+  a.hash_words = c->hash_words.get();
+  a.hash_mask = static_cast<std::uint32_t>((1ull << c->hash_bits) - 1);
+  a.neg_own = c->neg_own.get();
+  a.in_cnt = c->in_cnt.get();
+  a.in_rank = c->in_rank.get();
+  a.status = c->status.get();
+  a.own = Ownership{c->block_rows, static_cast<std::uint32_t>(c->opt.world), static_cast<std::uint32_t>(c->opt.rank)};
+  return a;
+}
+
+void require_live(gempe_ctx* c) {
+  if (c->degenerate) throw config_error("cannot iterate a degenerate graph");  // engine.cpp:279
+}
+
+void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
+  cuda_check(cudaMemsetAsync(c->status.get(), 0, 8 * sizeof(std::uint32_t), c->stream), "memset status");
+  cuda_check(cudaMemsetAsync(c->hist.get(), 0, 2 * kBins * sizeof(unsigned long long), c->stream), "memset hist");
+  cuda_check(cudaMemsetAsync(c->in_cnt.get(), 0, c->n * sizeof(std::uint32_t), c->stream), "memset in_cnt");
+  const SampleArgs a = sample_args(c, iter);
+  c->launches += launch_sample(a, c->stream);
+  c->launches += launch_scan(c->in_cnt.get(), c->in_off.get(), c->n, c->scan_scratch.get(), c->stream);
+  c->launches += launch_scatter(a, c->in_off.get(), c->in_anchor.get(), c->stream);
+  if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
+  cuda_check(cudaGetLastError(), "sampling passes");
+}
+
+void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
+  GatherArgs g{};
+  g.x_cur = c->x[c->cur].get();
+  g.x_next = c->x[c->cur ^ 1].get();
+  g.n = c->n;
+  g.dim = c->dim;
+  g.ld = c->ld;
+  g.rowptr = c->rowptr.get();
+  g.nbr = c->nbr.get();
+  g.neg_own = c->neg_own.get();
+  g.in_off = c->in_off.get();
+  g.in_anchor = c->in_anchor.get();
+  g.items = c->items.get();
+  g.hub_first = c->hub_first.get();
+  g.hub_items = c->hub_items.get();
+  g.hub_arrived = c->hub_arrived.get();
+  g.part_y = c->part_y.get();
+  g.part_z = c->part_z.get();
+  g.hist = c->hist.get();
+  g.status = c->status.get();
+  g.cap_y = c->capture ? c->cap_y.get() : nullptr;
+  g.cap_z = c->capture ? c->cap_z.get() : nullptr;
+  g.chunk_entries = c->chunk_entries;
+  g.k = c->opt.negatives;
+  g.neg_mode = c->opt.neg_mode;
+  g.math = c->math;
+  g.tab = c->tables;
+  c->launches += launch_gather(g, item_lo, item_hi, c->stream);
+  cuda_check(cudaGetLastError(), "gather launch");
+}
+
+cudaEvent_t next_event(gempe_ctx* c) {
+  if (c->events_used == c->events.size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    c->events.push_back(e);
+  }
+  return c->events[c->events_used++];
+}
+
+void fetch_status(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
+  cuda_check(cudaMemcpyAsync(c->pinned, c->status.get(), 8 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream),
+             "status D2H");
+  cuda_check(cudaMemcpyAsync(c->pinned + 4, c->hist.get(), 2 * kBins * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c->stream), "hist D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "round");
+  std::uint32_t st[8];
+  std::memcpy(st, c->pinned, sizeof st);
+  c->last_draws = static_cast<std::uint64_t>(st[kStatDrawsLo]) | (static_cast<std::uint64_t>(st[kStatDrawsHi]) << 32);
+  if (hist_edge) std::memcpy(hist_edge, c->pinned + 4, kBins * sizeof(std::uint64_t));
+  if (hist_nonedge) std::memcpy(hist_nonedge, c->pinned + 4 + kBins, kBins * sizeof(std::uint64_t));
+  if (st[kStatRetryCap]) {
+    throw near_complete_graph_error("no non-edge partner found after 10^4 draws; graph is near-complete");
+  }
+  if (st[kStatNonFinite]) {
+    throw divergence_error("non-finite coordinate after update", static_cast<int>(c->round_iter) + 1);
+  }
+}
+
+void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const std::uint32_t* dst,
+              const gempe_options& o) {
+  if (o.dim < 1) throw config_error("dimension must be >= 1");
+  if (row_stride_for(o.dim) > 1024) throw config_error("dimension above 1024 is not supported by the device layout");
+  if (o.neg_mode != GEMPE_NEG_PER_EDGE_2 && o.neg_mode != GEMPE_NEG_PER_VERTEX_K) throw config_error("unknown neg_mode");
+  if (o.math != GEMPE_MATH_TABLES && o.math != GEMPE_MATH_EXACT) throw config_error("unknown math policy");
+  if (o.rng != GEMPE_RNG_REFERENCE && o.rng != GEMPE_RNG_PHILOX) throw config_error("unknown rng mode");
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw config_error("bad rank/world");
+  if (o.comm_chunks < 1) throw config_error("comm_chunks must be >= 1");
+  if (m > 0 && (!src || !dst)) throw data_error("null edge arrays");
+  if (2 * m >= 0xffffffffull) throw config_error("edge count exceeds the 32-bit adjacency index");
+  const std::uint64_t slots = o.neg_mode == GEMPE_NEG_PER_EDGE_2 ? 2 * m : static_cast<std::uint64_t>(n) * o.negatives;
+  if (slots >= 0xffffffffull) throw config_error("sample count exceeds the 32-bit bucket index");
+  for (std::uint64_t e = 0; e < m; ++e) {
+    if (src[e] >= n || dst[e] >= n) throw data_error("edge endpoint out of range");
+    if (src[e] == dst[e]) throw data_error("self-loop in edge list (graphs must be canonical)");
+  }
+}
+
+}  // namespace
+}  // namespace gempe
+
+using namespace gempe;
+
+gempe_ctx::~gempe_ctx() {
+  for (cudaEvent_t e : events) cudaEventDestroy(e);
+  if (pinned) cudaFreeHost(pinned);
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+extern "C" {
+
+void gempe_default_options(gempe_options* o) {
+  std::memset(o, 0, sizeof *o);
+  o->dim = 2;
+  o->seed = 1;
+  o->neg_mode = GEMPE_NEG_PER_EDGE_2;
+  o->negatives = 0;
+  o->math = GEMPE_MATH_TABLES;
+  o->rng = GEMPE_RNG_REFERENCE;
+  o->relabel = 1;
+  o->world = 1;
+  o->comm_chunks = 1;
+}
+
+int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                 const std::uint32_t* dst, const gempe_options* opt) {
+  if (!out || !opt) {
+    g_create_error = "null argument";
+    return GEMPE_ERR_CONFIG;
+  }
+  *out = nullptr;
+  gempe_ctx* c = nullptr;
+  const int rc = guarded(nullptr, [&] {
+    validate(n, m, src, dst, *opt);
+    int device_count = 0;
+    const cudaError_t probe = cudaGetDeviceCount(&device_count);
+    if (probe != cudaSuccess || device_count == 0) {
+      throw cuda_error("no CUDA device available: the GEMPE path has no CPU fallback");
+    }
+    cuda_check(cudaSetDevice(opt->device), "cudaSetDevice");
+    c = new gempe_ctx;
+    c->opt = *opt;
+    c->n = n;
+    c->m = m;
+    c->dim = opt->dim;
+    c->ld = row_stride_for(opt->dim);
+    c->degenerate = n <= 1 || m == 0;  // engine.cpp:159
+    if (c->opt.world == 1) c->opt.comm_chunks = 1;
+    c->comm_chunks = static_cast<std::uint32_t>(c->opt.comm_chunks);
+    const std::uint64_t blocks = static_cast<std::uint64_t>(c->opt.world) * c->comm_chunks;
+    c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);
+    c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
+    c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : std::max(128u, 4096u / lanes_per_row(c->ld));
+    cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own_stream;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned), (4 + 2 * kBins) * sizeof(unsigned long long),
+                             cudaHostAllocDefault), "cudaHostAlloc");
+    pack_tables(c->tables);
+    c->status.allocate(8, true);
+    c->hist.allocate(2 * kBins, true);
+    for (auto& buf : c->x) buf.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
+
+    c->work_src.assign(src, src + m);
+    c->work_dst.assign(dst, dst + m);
+    c->to_work.resize(n);
+    for (std::uint32_t v = 0; v < n; ++v) c->to_work[v] = v;
+    if (!c->degenerate) {
+      if (opt->relabel) {  // engine.cpp:161-163 -> graph.cpp:182-206
+        const auto fwd = random_relabel_forward(n, mix_seed(opt->seed, 0xA11BE11));
+        for (auto& v : c->work_src) v = fwd[v];
+        for (auto& v : c->work_dst) v = fwd[v];
+        c->to_work = fwd;
+      }
+      build_structures(c);
+    }
+    c->launches += launch_init_coords(c->x[0].get(), n, c->dim, c->ld, GEMPE_INIT_REFERENCE, opt->seed, 0.0, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "init coords");
+  });
+  if (rc != GEMPE_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return GEMPE_OK;
+}
+
+void gempe_destroy(gempe_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->opt.device);
+  delete c;
+}
+
+const char* gempe_last_error(const gempe_ctx* c) { return c ? c->error.c_str() : g_create_error.c_str(); }
+int gempe_is_degenerate(const gempe_ctx* c) { return c->degenerate; }
+int gempe_hash_bits(const gempe_ctx* c) { return c->hash_bits; }
+std::uint64_t gempe_sample_slots(const gempe_ctx* c) { return c->slots; }
+std::uint64_t gempe_pair_terms(const gempe_ctx* c) { return c->m + c->slots; }
+
+std::uint64_t gempe_algorithmic_bytes(const gempe_ctx* c) {
+  // (2m + 2S) R + 2 n R + 8 m + 8 n + 4 S + S p, with R = 4 d and p = 1
+  const std::uint64_t R = 4ull * c->dim, S = c->slots;
+  return (2 * c->m + 2 * S) * R + 2ull * c->n * R + 8 * c->m + 8ull * c->n + 4 * S + S;
+}
+
+int gempe_get_work_graph(const gempe_ctx* c, std::uint32_t* src, std::uint32_t* dst, std::uint32_t* to_work) {
+  if (src) std::copy(c->work_src.begin(), c->work_src.end(), src);
+  if (dst) std::copy(c->work_dst.begin(), c->work_dst.end(), dst);
+  if (to_work) std::copy(c->to_work.begin(), c->to_work.end(), to_work);
+  return GEMPE_OK;
+}
+
+int gempe_set_coords(gempe_ctx* c, const float* x_work) {
+  return guarded(c, [&] {
+    if (!x_work) throw config_error("null coordinates");
+    if (c->n == 0) return;
+    cuda_check(cudaMemcpy2DAsync(c->x[c->cur].get(), c->ld * sizeof(float), x_work, c->dim * sizeof(float),
+                                 c->dim * sizeof(float), c->n, cudaMemcpyHostToDevice, c->stream), "set_coords");
+    cuda_check(cudaStreamSynchronize(c->stream), "set_coords");
+  });
+}
+
+int gempe_get_coords(gempe_ctx* c, float* x_work) {
+  return guarded(c, [&] {
+    if (!x_work) throw config_error("null coordinates");
+    if (c->n == 0) return;
+    cuda_check(cudaMemcpy2DAsync(x_work, c->dim * sizeof(float), c->x[c->cur].get(), c->ld * sizeof(float),
+                                 c->dim * sizeof(float), c->n, cudaMemcpyDeviceToHost, c->stream), "get_coords");
+    cuda_check(cudaStreamSynchronize(c->stream), "get_coords");
+  });
+}
+
+int gempe_init_coords(gempe_ctx* c, int rule, std::uint64_t seed, double stddev) {
+  return guarded(c, [&] {
+    if (rule < 0 || rule > 2) throw config_error("unknown init rule");
+    c->launches += launch_init_coords(c->x[c->cur].get(), c->n, c->dim, c->ld, rule, seed, stddev, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "init coords");
+  });
+}
+
+int gempe_relabel(gempe_ctx* c, std::uint64_t relabel_seed) {
+  return guarded(c, [&] {
+    require_live(c);
+    const auto fwd = random_relabel_forward(c->n, relabel_seed);
+    std::vector<float> before(static_cast<std::size_t>(c->n) * c->dim), after(before.size());
+    if (gempe_get_coords(c, before.data()) != GEMPE_OK) throw cuda_error(c->error);
+    for (std::uint32_t v = 0; v < c->n; ++v) {  // engine.cpp:186-190
+      std::memcpy(after.data() + static_cast<std::size_t>(fwd[v]) * c->dim,
+                  before.data() + static_cast<std::size_t>(v) * c->dim, sizeof(float) * c->dim);
+    }
+    for (auto& v : c->work_src) v = fwd[v];
+    for (auto& v : c->work_dst) v = fwd[v];
+    for (auto& v : c->to_work) v = fwd[v];
+    build_structures(c);
+    if (gempe_set_coords(c, after.data()) != GEMPE_OK) throw cuda_error(c->error);
+  });
+}
+
+int gempe_set_capture(gempe_ctx* c, int on) {
+  return guarded(c, [&] {
+    c->capture = on != 0;
+    if (c->capture && c->cap_y.size() == 0 && !c->degenerate) {
+      c->cap_y.allocate(static_cast<std::size_t>(c->n) * c->dim, true);
+      c->cap_z.allocate(c->n, true);
+    }
+  });
+}
+
+int gempe_get_yz(gempe_ctx* c, double* y, double* z) {
+  return guarded(c, [&] {
+    if (!c->capture || c->cap_y.size() == 0) throw config_error("capture is off");
+    cuda_check(cudaStreamSynchronize(c->stream), "get_yz");
+    if (y) cuda_check(cudaMemcpy(y, c->cap_y.get(), c->cap_y.size() * sizeof(double), cudaMemcpyDeviceToHost), "y D2H");
+    if (z) cuda_check(cudaMemcpy(z, c->cap_z.get(), c->cap_z.size() * sizeof(double), cudaMemcpyDeviceToHost), "z D2H");
+  });
+}
+
+int gempe_begin_round(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_index) {
+  return guarded(c, [&] {
+    require_live(c);
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    set_round_math(c, mu, sigma);
+    c->round_iter = iter_index;
+    sampling_passes(c, iter_index);
+  });
+}
+
+int gempe_gather_chunk(gempe_ctx* c, int chunk) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (chunk < 0 || chunk >= static_cast<int>(c->comm_chunks)) throw config_error("chunk out of range");
+    gather_items(c, c->chunk_item_off[chunk], c->chunk_item_off[chunk + 1]);
+  });
+}
+
+int gempe_end_round(gempe_ctx* c) {
+  c->cur ^= 1;
+  return GEMPE_OK;
+}
+
+int gempe_iterate_async(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_index) {
+  return guarded(c, [&] {
+    require_live(c);
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    set_round_math(c, mu, sigma);
+    c->round_iter = iter_index;
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    sampling_passes(c, iter_index);
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    c->cur ^= 1;
+  });
+}
+
+int gempe_sync(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
+  return guarded(c, [&] { fetch_status(c, hist_edge, hist_nonedge); });
+}
+
+int gempe_iterate(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_index, std::uint64_t* hist_edge,
+                  std::uint64_t* hist_nonedge) {
+  const int rc = gempe_iterate_async(c, mu, sigma, iter_index);
+  if (rc != GEMPE_OK) return rc;
+  return gempe_sync(c, hist_edge, hist_nonedge);
+}
+
+int gempe_elapsed_ms(gempe_ctx* c, float out3[3]) {
+  return guarded(c, [&] {
+    out3[0] = out3[1] = out3[2] = 0.0f;
+    if (c->events_used < 3) return;
+    cuda_check(cudaEventSynchronize(c->events[c->events_used - 1]), "event sync");
+    for (std::size_t r = 0; r + 2 < c->events_used; r += 3) {
+      float sample_ms = 0.0f, gather_ms = 0.0f;
+      cuda_check(cudaEventElapsedTime(&sample_ms, c->events[r], c->events[r + 1]), "elapsed");
+      cuda_check(cudaEventElapsedTime(&gather_ms, c->events[r + 1], c->events[r + 2]), "elapsed");
+      out3[1] += sample_ms;
+      out3[2] += gather_ms;
+    }
+    cuda_check(cudaEventElapsedTime(&out3[0], c->events[0], c->events[c->events_used - 1]), "elapsed");
+    c->events_used = 0;
+  });
+}
+
+std::uint64_t gempe_kernel_launches(const gempe_ctx* c) { return c->launches; }
+
+int gempe_probe(gempe_ctx* c, const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (count == 0) return;
+    DeviceBuffer<std::uint32_t> di, dj;
+    DeviceBuffer<std::uint8_t> dout;
+    di.upload(std::vector<std::uint32_t>(i, i + count));
+    dj.upload(std::vector<std::uint32_t>(j, j + count));
+    dout.allocate(count);
+    c->launches += launch_probe(c->hash_words.get(), static_cast<std::uint32_t>((1ull << c->hash_bits) - 1), c->n,
+                                di.get(), dj.get(), count, dout.get(), c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "probe");
+    cuda_check(cudaMemcpy(out, dout.get(), count, cudaMemcpyDeviceToHost), "probe D2H");
+  });
+}
+
+int gempe_sample(gempe_ctx* c, std::uint64_t iter_index, std::uint32_t* partners, std::uint64_t* total_draws) {
+  return guarded(c, [&] {
+    require_live(c);
+    c->round_iter = iter_index;
+    sampling_passes(c, iter_index);
+    const std::uint32_t* result = c->neg_own.get();
+    DeviceBuffer<std::uint32_t> ordered;
+    if (c->opt.neg_mode == GEMPE_NEG_PER_EDGE_2) {
+      ordered.allocate(c->slots);
+      c->launches += launch_unpermute_partners(c->neg_own.get(), c->eid_role.get(), c->slots, ordered.get(), c->stream);
+      result = ordered.get();
+    }
+    cuda_check(cudaMemcpyAsync(c->pinned, c->status.get(), 8 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream),
+               "status D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sample");
+    if (partners && c->slots) {
+      cuda_check(cudaMemcpy(partners, result, c->slots * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "partners D2H");
+    }
+    std::uint32_t st[8];
+    std::memcpy(st, c->pinned, sizeof st);
+    if (total_draws) *total_draws = static_cast<std::uint64_t>(st[kStatDrawsLo]) | (static_cast<std::uint64_t>(st[kStatDrawsHi]) << 32);
+    if (st[kStatRetryCap]) throw near_complete_graph_error("no non-edge partner found after 10^4 draws; graph is near-complete");
+  });
+}
+
+int gempe_set_stream(gempe_ctx* c, void* cuda_stream) {
+  c->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->own_stream;
+  return GEMPE_OK;
+}
+void* gempe_device_coords(gempe_ctx* c, int which) { return c->x[which ? c->cur ^ 1 : c->cur].get(); }
+std::uint32_t gempe_row_stride(const gempe_ctx* c) { return c->ld; }
+std::uint32_t gempe_padded_rows(const gempe_ctx* c) { return c->n_pad; }
+std::uint32_t gempe_block_rows(const gempe_ctx* c) { return c->block_rows; }
+
+// ---- host numerics --------------------------------------------------------------------------------
+
+int gempe_host_fastmath_table(int which, double* out67) {
+  try {
+    const FastMathTables& t = FastMathTables::get();
+    const QuadTable& q = which == 0 ? t.erf : (which == 1 ? t.exp_neg : t.ratio);
+    double* p = out67;
+    for (double v : q.knots) *p++ = v;
+    for (double v : q.a) *p++ = v;
+    for (double v : q.b) *p++ = v;
+    for (double v : q.c) *p++ = v;
+    *p++ = q.lo;
+    *p++ = q.hi;
+    return q.odd_mirror ? 1 : 0;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return -1;
+  }
+}
+
+static Tallies make_tallies(const std::uint64_t* he, const std::uint64_t* hn, double w) {
+  Tallies t;
+  std::copy(he, he + kHistBins, t.edge.begin());
+  std::copy(hn, hn + kHistBins, t.nonedge.begin());
+  t.nonedge_weight = w;
+  return t;
+}
+
+double gempe_host_optimize_sigma(const std::uint64_t* he, const std::uint64_t* hn, double w, double mu, int* steps) {
+  try {
+    const SigmaSearch s = optimize_sigma(make_tallies(he, hn, w), mu);
+    if (steps) *steps = s.bisection_steps;
+    return s.sigma;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return std::numeric_limits<double>::quiet_NaN();
+  }
+}
+double gempe_host_histogram_objective(const std::uint64_t* he, const std::uint64_t* hn, double w, double mu, double sigma) {
+  return histogram_objective(make_tallies(he, hn, w), mu, sigma);
+}
+double gempe_host_histogram_objective_dsigma(const std::uint64_t* he, const std::uint64_t* hn, double w, double mu,
+                                             double sigma) {
+  return histogram_objective_dsigma(make_tallies(he, hn, w), mu, sigma);
+}
+int gempe_host_random_relabel(std::uint32_t n, std::uint64_t seed, std::uint32_t* forward) {
+  const auto f = random_relabel_forward(n, seed);
+  std::copy(f.begin(), f.end(), forward);
+  return GEMPE_OK;
+}
+std::uint64_t gempe_host_mix_seed(std::uint64_t seed, std::uint64_t component) { return mix_seed(seed, component); }
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// gempe_ctx: device-resident state of one GEMPE engine shard (one GPU).  See DESIGN.md for the layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gempe.h"
+#include "hostmath.hpp"
+#include "kernels.hpp"
+
+namespace gempe {
+
+void cuda_check(cudaError_t e, const char* what);
+void set_create_error(const std::string& msg);  // read back through gempe_last_error(NULL)
+
+// Owning device allocation (cudaMalloc/cudaFree), zero-filled on request.
+template <typename T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() { release(); }
+  void allocate(std::size_t count, bool zero = false) {
+    release();
+    count_ = count;
+    if (count == 0) return;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ptr_), count * sizeof(T)), "cudaMalloc");
+    if (zero) cuda_check(cudaMemset(ptr_, 0, count * sizeof(T)), "cudaMemset");
+  }
+  void upload(const std::vector<T>& host) {
+    allocate(host.size());
+    if (!host.empty()) {
+      cuda_check(cudaMemcpy(ptr_, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    }
+  }
+  void release() {
+    if (ptr_) cudaFree(ptr_);
+    ptr_ = nullptr;
+    count_ = 0;
+  }
+  T* get() const { return ptr_; }
+  std::size_t size() const { return count_; }
+  void swap(DeviceBuffer& o) {
+    std::swap(ptr_, o.ptr_);
+    std::swap(count_, o.count_);
+  }
+
+ private:
+  T* ptr_ = nullptr;
+  std::size_t count_ = 0;
+};
+
+}  // namespace gempe
+
+struct gempe_ctx {
+  gempe_options opt{};
+  std::uint32_t n = 0, dim = 0, ld = 0;
+  std::uint64_t m = 0;
+  bool degenerate = false;
+  int hash_bits = 0;
+  std::uint64_t slots = 0;          // S
+  std::uint32_t block_rows = 0, n_pad = 0, comm_chunks = 1;
+  std::uint32_t chunk_entries = 0;
+  std::string error;
+
+  // host copies kept for the work-graph accessors and re-relabelling
+  std::vector<std::uint32_t> work_src, work_dst, to_work;
+
+  // device state
+  gempe::DeviceBuffer<float> x[2];
+  int cur = 0;
+  gempe::DeviceBuffer<std::uint32_t> rowptr, nbr, eid_role, csr_src;
+  gempe::DeviceBuffer<std::uint32_t> hash_words;
+  gempe::DeviceBuffer<std::uint32_t> neg_own, in_cnt, in_off, in_rank, in_anchor, scan_scratch;
+  gempe::DeviceBuffer<uint4> items;
+  std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
+  gempe::DeviceBuffer<std::uint32_t> hub_first, hub_items, hub_arrived;
+  gempe::DeviceBuffer<double> part_y, part_z;
+  gempe::DeviceBuffer<unsigned long long> hist;
+  gempe::DeviceBuffer<std::uint32_t> status;
+  gempe::DeviceBuffer<double> cap_y, cap_z;
+  bool capture = false;
+
+  // pinned host mirror of {status[8] as u64-aligned words, hist[1024]}
+  unsigned long long* pinned = nullptr;
+
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  gempe::RoundMath math{};
+  gempe::DeviceTables tables{};
+  std::uint64_t round_iter = 0;
+  std::uint64_t launches = 0;
+  std::uint64_t last_draws = 0;
+
+  // timing: event triples {start, after sampling passes, end} per async round since the last query
+  std::vector<cudaEvent_t> events;
+  std::size_t events_used = 0;
+
+  ~gempe_ctx();
+};

@@ -1,0 +1,230 @@
+// Run-level facade over the device context: the host half of EmbeddingEngine
+// (/root/reference/proj/src/engine.cpp:278-388) -- sigma search on the round's tallies, PE trace, best-PE
+// snapshot, convergence window, periodic re-relabel, map-back to original ids.  The Jacobi round itself
+// is gempe_iterate (context.cpp); nothing here touches coordinates on the host except the final export.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+
+#include "context.hpp"
+
+using namespace gempe;
+
+struct gempe_engine {
+  gempe_ctx* ctx = nullptr;
+  gempe_iteration_config cfg{};
+  std::uint64_t seed = 0;
+  std::uint32_t n = 0, dim = 0;
+  std::uint64_t m = 0;
+  double mu = kDefaultMu, sigma = 1.0;  // SigmoidParams defaults (sigmoid.hpp:18-21)
+  int iter = 0;
+  std::vector<double> pe_trace;
+  Tallies last_hist;
+  bool have_hist = false;
+  double best_pe = std::numeric_limits<double>::infinity();
+  DeviceBuffer<float> best_x;               // device snapshot, WORK indexing of the moment it was taken
+  std::vector<std::uint32_t> best_to_work;
+  std::string error;
+
+  ~gempe_engine() { gempe_destroy(ctx); }
+};
+
+namespace {
+
+template <typename Fn>
+int guarded(gempe_engine* e, Fn&& fn) {
+  try {
+    fn();
+    return GEMPE_OK;
+  } catch (const divergence_error& ex) {
+    e->error = ex.what();
+    return GEMPE_ERR_DIVERGENCE;
+  } catch (const config_error& ex) {
+    e->error = ex.what();
+    return GEMPE_ERR_CONFIG;
+  } catch (const cuda_error& ex) {
+    e->error = ex.what();
+    return GEMPE_ERR_CUDA;
+  } catch (const std::exception& ex) {
+    e->error = ex.what();
+    return GEMPE_ERR_DATA;
+  }
+}
+
+void rethrow(gempe_ctx* c, int rc) {
+  if (rc == GEMPE_OK) return;
+  const std::string msg = gempe_last_error(c);
+  switch (rc) {
+    case GEMPE_ERR_CONFIG: throw config_error(msg);
+    case GEMPE_ERR_DIVERGENCE: throw divergence_error(msg, 0);
+    case GEMPE_ERR_CUDA: throw cuda_error(msg);
+    default: throw data_error(msg);
+  }
+}
+
+// original-indexed export of a work-indexed device layout (engine.cpp:327-337)
+void map_back(gempe_engine* e, const float* x_dev, const std::vector<std::uint32_t>& to_work, float* out) {
+  gempe_ctx* c = e->ctx;
+  std::vector<float> work(static_cast<std::size_t>(e->n) * e->dim);
+  if (e->n) {
+    cuda_check(cudaStreamSynchronize(c->stream), "map_back");
+    cuda_check(cudaMemcpy2D(work.data(), e->dim * sizeof(float), x_dev, c->ld * sizeof(float), e->dim * sizeof(float),
+                            e->n, cudaMemcpyDeviceToHost), "map_back D2H");
+  }
+  for (std::uint32_t v = 0; v < e->n; ++v) {
+    std::memcpy(out + static_cast<std::size_t>(v) * e->dim, work.data() + static_cast<std::size_t>(to_work[v]) * e->dim,
+                sizeof(float) * e->dim);
+  }
+}
+
+void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {
+  gempe_ctx* c = e->ctx;
+  if (c->degenerate) throw config_error("cannot iterate a degenerate graph");
+  if (e->cfg.relabel_period > 0 && e->iter > 0 && e->iter % e->cfg.relabel_period == 0) {  // engine.cpp:281-283
+    rethrow(c, gempe_relabel(c, mix_seed(mix_seed(e->seed, 0xA11BE11), static_cast<std::uint64_t>(e->iter))));
+  }
+  Tallies t;
+  rethrow(c, gempe_iterate(c, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(), t.nonedge.data()));
+
+  const std::uint64_t samples = t.nonedge_total();
+  const std::uint64_t pairs = static_cast<std::uint64_t>(e->n) * (e->n > 0 ? e->n - 1 : 0) / 2;
+  t.nonedge_weight = samples > 0 ? static_cast<double>(pairs - e->m) / static_cast<double>(samples) : 1.0;
+  // growth-capped sigma update (engine.cpp:302-307)
+  e->sigma = std::min(optimize_sigma(t, e->mu).sigma, e->sigma * 1.5);
+  const double pe = histogram_objective(t, e->mu, e->sigma) / static_cast<double>(pairs);
+  e->pe_trace.push_back(pe);
+  e->last_hist = t;
+  e->have_hist = true;
+  ++e->iter;
+  if (pe < e->best_pe) {  // engine.cpp:316-319, kept on the device
+    e->best_pe = pe;
+    const std::size_t count = static_cast<std::size_t>(c->n_pad) * c->ld;
+    if (e->best_x.size() != count) e->best_x.allocate(count);
+    cuda_check(cudaMemcpyAsync(e->best_x.get(), c->x[c->cur].get(), count * sizeof(float), cudaMemcpyDeviceToDevice,
+                               c->stream), "best snapshot");
+    e->best_to_work = c->to_work;
+  }
+  if (pe_out) *pe_out = pe;
+  if (sigma_out) *sigma_out = e->sigma;
+}
+
+}  // namespace
+
+extern "C" {
+
+void gempe_default_iteration_config(gempe_iteration_config* cfg) {
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->max_iters = 100;
+  cfg->lane_width = 16;
+  cfg->workers = 0;
+  cfg->convergence_tol = 1e-4;
+  cfg->convergence_window = 5;
+  cfg->relabel_period = 0;
+  cfg->fast_math = 1;
+  cfg->hash_bits = 0;
+  cfg->neg_mode = GEMPE_NEG_PER_EDGE_2;
+  cfg->negatives = 0;
+  cfg->device = 0;
+}
+
+int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                        const std::uint32_t* dst, std::uint32_t dim, const gempe_iteration_config* cfg,
+                        std::uint64_t seed) {
+  if (!out || !cfg) return GEMPE_ERR_CONFIG;
+  *out = nullptr;
+  auto e = std::make_unique<gempe_engine>();
+  e->cfg = *cfg;
+  e->seed = seed;
+  e->n = n;
+  e->m = m;
+  e->dim = dim;
+  // config validation of the reference ctor (engine.cpp:152-154); hash_bits is validated by gempe_create
+  const char* bad = dim < 1 ? "dimension must be >= 1"
+                            : (cfg->lane_width < 1 ? "lane width must be >= 1"
+                                                   : (cfg->max_iters < 1 ? "max_iters must be >= 1" : nullptr));
+  gempe_options opt;
+  gempe_default_options(&opt);
+  opt.dim = dim;
+  opt.hash_bits = cfg->hash_bits;
+  opt.seed = seed;
+  opt.neg_mode = cfg->neg_mode;
+  opt.negatives = cfg->negatives;
+  opt.math = cfg->fast_math ? GEMPE_MATH_TABLES : GEMPE_MATH_EXACT;
+  opt.device = cfg->device;
+  int rc = GEMPE_ERR_CONFIG;
+  if (!bad) rc = gempe_create(&e->ctx, n, m, src, dst, &opt);
+  if (bad) set_create_error(bad);
+  if (bad || rc != GEMPE_OK) return rc;  // message: gempe_last_error(NULL)
+  *out = e.release();
+  return GEMPE_OK;
+}
+
+void gempe_engine_destroy(gempe_engine* e) { delete e; }
+const char* gempe_engine_last_error(const gempe_engine* e) { return e ? e->error.c_str() : ""; }
+gempe_ctx* gempe_engine_context(gempe_engine* e) { return e->ctx; }
+int gempe_engine_degenerate(const gempe_engine* e) { return e->ctx ? e->ctx->degenerate : 0; }
+int gempe_engine_iteration(const gempe_engine* e) { return e->iter; }
+double gempe_engine_sigma(const gempe_engine* e) { return e->sigma; }
+
+int gempe_engine_run_single_iteration(gempe_engine* e, double* pe_estimate, double* sigma) {
+  return guarded(e, [&] {
+    if (!e->ctx) throw config_error("engine was not constructed: " + e->error);
+    single_iteration(e, pe_estimate, sigma);
+  });
+}
+
+int gempe_engine_run(gempe_engine* e, gempe_embed_result* r) {
+  return guarded(e, [&] {
+    if (!e->ctx) throw config_error("engine was not constructed: " + e->error);
+    if (!r || !r->embedding) throw config_error("result needs an embedding buffer");
+    gempe_ctx* c = e->ctx;
+    r->converged = 0;
+    r->degenerate = c->degenerate;
+    r->pe_trace_len = 0;
+    r->iterations = 0;
+    r->final_sigma = e->sigma;
+    r->last_nonedge_weight = 1.0;
+    if (c->degenerate) {  // engine.cpp:341-347: initial layout, identity relabel
+      map_back(e, c->x[c->cur].get(), c->to_work, r->embedding);
+      if (r->relabel_forward) std::copy(c->to_work.begin(), c->to_work.end(), r->relabel_forward);
+      return;
+    }
+    // converged when the last `window` rounds brought no new PE minimum beating the earlier best by tol
+    // (engine.cpp:353-367)
+    const int window = e->cfg.convergence_window;
+    while (e->iter < e->cfg.max_iters) {
+      single_iteration(e, nullptr, nullptr);
+      const int k = static_cast<int>(e->pe_trace.size());
+      if (k > window) {
+        const double best_before = *std::min_element(e->pe_trace.begin(), e->pe_trace.begin() + (k - window));
+        const double best_recent = *std::min_element(e->pe_trace.begin() + (k - window), e->pe_trace.end());
+        if (best_before - best_recent < e->cfg.convergence_tol * std::fabs(best_before)) {
+          r->converged = 1;
+          break;
+        }
+      }
+    }
+    if (!r->converged && e->best_x.size()) {
+      map_back(e, e->best_x.get(), e->best_to_work, r->embedding);
+    } else {
+      map_back(e, c->x[c->cur].get(), c->to_work, r->embedding);
+    }
+    r->pe_trace_len = static_cast<std::int32_t>(e->pe_trace.size());
+    if (r->pe_trace) {
+      const int copy = std::min<int>(r->pe_trace_cap, r->pe_trace_len);
+      std::copy(e->pe_trace.begin(), e->pe_trace.begin() + copy, r->pe_trace);
+    }
+    r->final_sigma = e->sigma;
+    r->iterations = e->iter;
+    if (r->relabel_forward) std::copy(c->to_work.begin(), c->to_work.end(), r->relabel_forward);
+    if (e->have_hist) {
+      if (r->last_hist_edge) std::copy(e->last_hist.edge.begin(), e->last_hist.edge.end(), r->last_hist_edge);
+      if (r->last_hist_nonedge) std::copy(e->last_hist.nonedge.begin(), e->last_hist.nonedge.end(), r->last_hist_nonedge);
+      r->last_nonedge_weight = e->last_hist.nonedge_weight;
+    }
+  });
+}
+
+}  // extern "C"

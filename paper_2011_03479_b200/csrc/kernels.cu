@@ -1,0 +1,679 @@
+// sm_100a kernels of the GEMPE round.  No tensor cores: the round is an HBM-bound sparse row gather plus
+// a per-vertex reduction.  Citations are relative to /root/reference/proj.
+//
+//   hash_build / probe        bit-packed direct-mapped edge filter  (hash_set.cpp:9-34, hash_set.hpp:28-30)
+//   sample                    one thread per sample stream          (sampler.cpp:7-31, engine.cpp:227-237)
+//   scan / scatter / sort     bucket the accepted samples by PARTNER so the partner-side term of
+//                             add_pair (engine.cpp:68-72) becomes a gather instead of an atomic scatter
+//   gather                    per work item (vertex or hub slice): pair_distance + parabola_impl + add_pair
+//                             for every row it touches, warp-shuffle reduction, fused x = y/z update
+//                             (engine.cpp:45-73, 253-276, sigmoid.hpp:88-101, histogram.hpp:24-29)
+#include "kernels.hpp"
+
+#include <cuda_runtime.h>
+
+#include "device_fns.cuh"
+
+namespace gempe {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ bool is_local(const Ownership& o, std::uint32_t v) {
+  return o.world == 1 || (v / o.block_rows) % o.world == o.rank;
+}
+
+__device__ __forceinline__ bool hash_test(const std::uint32_t* __restrict__ words, std::uint32_t mask,
+                                          std::uint32_t n, std::uint32_t i, std::uint32_t j) {
+  const std::uint32_t h = pair_hash(i, j, n, mask);
+  return (__ldg(words + (h >> 5)) >> (h & 31u)) & 1u;
+}
+
+// ---------------------------------------------------------------------------------- hash set
+
+__global__ void hash_build_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst,
+                                  std::uint64_t m, std::uint32_t n, std::uint32_t mask,
+                                  std::uint32_t* __restrict__ words) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    const std::uint32_t i = src[e], j = dst[e];
+    const std::uint32_t h0 = pair_hash(i, j, n, mask), h1 = pair_hash(j, i, n, mask);
+    atomicOr(words + (h0 >> 5), 1u << (h0 & 31u));
+    atomicOr(words + (h1 >> 5), 1u << (h1 & 31u));
+  }
+}
+
+__global__ void probe_kernel(const std::uint32_t* __restrict__ words, std::uint32_t mask, std::uint32_t n,
+                             const std::uint32_t* __restrict__ i, const std::uint32_t* __restrict__ j,
+                             std::uint64_t count, std::uint8_t* __restrict__ out) {
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < count) out[t] = hash_test(words, mask, n, i[t], j[t]) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------------- sampler
+
+// One thread per sample stream.  Reference mode replays expand_seed32(seed, iter, unit, draw) followed by the
+// LCG "advance, then use" loop of sample_non_edges.  Lanes of a warp retry together until every lane has
+// its partner, so the table probes of one warp stay batched; the accepted partner is counted into its
+// partner's incoming bucket (arrival rank kept for the scatter pass).
+__global__ void __launch_bounds__(kThreads) sample_kernel(const SampleArgs a) {
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t draws = 0;
+  if (t < a.slots) {
+    std::uint32_t anchor;
+    std::uint64_t unit, draw;
+    if (a.neg_mode == 0) {
+      anchor = __ldg(a.csr_src + t);
+      const std::uint32_t er = __ldg(a.eid_role + t);
+      unit = er >> 1;
+      draw = er & 1u;
+    } else {
+      anchor = static_cast<std::uint32_t>(t / a.k);
+      unit = anchor;
+      draw = t - static_cast<std::uint64_t>(anchor) * a.k;
+    }
+    std::uint32_t partner = anchor;
+    bool found = false;
+    if (a.rng == 0) {
+      std::uint32_t s = static_cast<std::uint32_t>(mix(mix(a.stream_base, unit), draw) >> 16);
+      for (int tries = 0; tries < kMaxRetries; ++tries) {
+        s = s * kLcgMul + 1u;
+        ++draws;
+        const std::uint32_t g = uniform_index(s, a.n);
+        if (g == anchor) continue;
+        if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
+        partner = g;
+        found = true;
+        break;
+      }
+    } else {
+      const std::uint64_t slot = a.neg_mode == 0 ? ((unit << 1) | draw) : t;
+      for (int tries = 0; tries < kMaxRetries && !found; tries += 4) {
+        std::uint32_t ctr[4] = {static_cast<std::uint32_t>(slot), static_cast<std::uint32_t>(slot >> 32),
+                                static_cast<std::uint32_t>(tries >> 2), static_cast<std::uint32_t>(a.iter)};
+        philox4x32(ctr, static_cast<std::uint32_t>(a.stream_base), static_cast<std::uint32_t>(a.stream_base >> 32));
+        for (int q = 0; q < 4 && !found; ++q) {
+          ++draws;
+          const std::uint32_t g = static_cast<std::uint32_t>((static_cast<std::uint64_t>(ctr[q]) * a.n) >> 32);
+          if (g == anchor) continue;
+          if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
+          partner = g;
+          found = true;
+        }
+      }
+    }
+    if (!found) {  // near_complete_graph_error (sampler.cpp:18-21); keep memory-safe output
+      atomicOr(a.status + kStatRetryCap, 1u);
+      partner = anchor + 1 < a.n ? anchor + 1 : 0;
+    }
+    a.neg_own[t] = partner;
+    a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
+  }
+  // total draw count (test hook / p-bar of the roofline formula)
+  for (int off = 16; off > 0; off >>= 1) draws += __shfl_xor_sync(kFull, draws, off);
+  if ((threadIdx.x & 31) == 0 && draws) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.status + kStatDrawsLo), static_cast<unsigned long long>(draws));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, const std::uint32_t* __restrict__ in_off,
+                                                           std::uint32_t* __restrict__ in_anchor) {
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= a.slots) return;
+  const std::uint32_t rank = a.in_rank[t];
+  if (rank == kNotLocal) return;
+  const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t) : static_cast<std::uint32_t>(t / a.k);
+  in_anchor[in_off[a.neg_own[t]] + rank] = anchor;
+}
+
+__global__ void unpermute_kernel(const std::uint32_t* __restrict__ neg_own, const std::uint32_t* __restrict__ eid_role,
+                                 std::uint64_t slots, std::uint32_t* __restrict__ out) {
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < slots) out[eid_role[t]] = neg_own[t];
+}
+
+// One warp per vertex: rank-sort of the (small, Poisson-sized) incoming bucket, in place via registers for
+// buckets up to 32*kSortRegs entries; larger buckets fall back to an O(len^2) global pass.
+constexpr int kSortRegs = 8;
+__global__ void __launch_bounds__(kThreads) sort_buckets_kernel(const std::uint32_t* __restrict__ in_off,
+                                                                std::uint32_t* __restrict__ in_anchor, std::uint32_t n) {
+  const std::uint32_t v = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= n) return;
+  const std::uint32_t lo = in_off[v], len = in_off[v + 1] - lo;
+  if (len < 2) return;
+  std::uint32_t* b = in_anchor + lo;
+  if (len <= 32u * kSortRegs) {
+    std::uint32_t val[kSortRegs], pos[kSortRegs];
+#pragma unroll
+    for (int q = 0; q < kSortRegs; ++q) {
+      const std::uint32_t i = lane + 32u * q;
+      val[q] = i < len ? b[i] : 0xffffffffu;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kSortRegs; ++q) {
+      const std::uint32_t i = lane + 32u * q;
+      std::uint32_t p = 0;
+      if (i < len) {
+        for (std::uint32_t j = 0; j < len; ++j) {
+          const std::uint32_t o = b[j];
+          p += (o < val[q]) || (o == val[q] && j < i);
+        }
+      }
+      pos[q] = p;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kSortRegs; ++q) {
+      if (lane + 32u * q < len) b[pos[q]] = val[q];
+    }
+  } else {
+    // odd-even transposition sort by the warp, in place (rare: only heavy-tailed buckets)
+    for (std::uint32_t pass = 0; pass < len; ++pass) {
+      for (std::uint32_t i = (pass & 1u) + 2u * lane; i + 1 < len; i += 64u) {
+        const std::uint32_t x = b[i], y = b[i + 1];
+        if (x > y) {
+          b[i] = y;
+          b[i + 1] = x;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- exclusive scan
+
+constexpr int kScanTile = 4096;  // 256 threads x 16
+
+__global__ void __launch_bounds__(kThreads) scan_tile_sums_kernel(const std::uint32_t* __restrict__ in, std::uint32_t n,
+                                                                  std::uint32_t* __restrict__ tile_sum) {
+  __shared__ std::uint32_t warp_sum[kThreads / 32];
+  const std::uint32_t base = blockIdx.x * kScanTile;
+  std::uint32_t s = 0;
+  for (int q = 0; q < 16; ++q) {
+    const std::uint32_t i = base + q * kThreads + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    std::uint32_t t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += warp_sum[w];
+    tile_sum[blockIdx.x] = t;
+  }
+}
+
+__global__ void scan_tile_offsets_kernel(std::uint32_t* __restrict__ tile_sum, std::uint32_t tiles) {
+  // single block of 1024 threads, in-place exclusive scan with a running carry
+  __shared__ std::uint32_t warp_tot[32];
+  __shared__ std::uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (std::uint32_t base = 0; base < tiles; base += 1024) {
+    const std::uint32_t i = base + threadIdx.x;
+    const std::uint32_t v = i < tiles ? tile_sum[i] : 0;
+    std::uint32_t inc = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+      if (lane >= off) inc += o;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      std::uint32_t w = warp_tot[lane], winc = w;
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, winc, off);
+        if (lane >= off) winc += o;
+      }
+      warp_tot[lane] = winc - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const std::uint32_t excl = carry + warp_tot[warp] + inc - v;
+    if (i < tiles) tile_sum[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_sum[tiles] = carry;
+}
+
+__global__ void __launch_bounds__(kThreads) scan_apply_kernel(const std::uint32_t* __restrict__ in, std::uint32_t n,
+                                                              const std::uint32_t* __restrict__ tile_off,
+                                                              std::uint32_t* __restrict__ out) {
+  __shared__ std::uint32_t warp_tot[kThreads / 32];
+  const std::uint32_t base = blockIdx.x * kScanTile + threadIdx.x * 16;
+  std::uint32_t v[16], s = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    v[q] = base + q < n ? in[base + q] : 0;
+    s += v[q];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  std::uint32_t inc = s;
+  for (int off = 1; off < 32; off <<= 1) {
+    const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+    if (lane >= off) inc += o;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  std::uint32_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += warp_tot[w];
+  std::uint32_t run = tile_off[blockIdx.x] + woff + inc - s;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (base + q < n) out[base + q] = run;
+    run += v[q];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_off[gridDim.x];
+}
+
+// ---------------------------------------------------------------------------------- initial coordinates
+
+__global__ void init_coords_kernel(float* __restrict__ x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld,
+                                   int rule, std::uint64_t state0, double stddev) {
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * ld;
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const std::uint32_t v = static_cast<std::uint32_t>(t / ld), c = static_cast<std::uint32_t>(t % ld);
+  float out = 0.0f;
+  if (c < dim) {
+    const std::uint64_t i = static_cast<std::uint64_t>(v) * dim + c;
+    if (rule == 0) {
+      // SplitMix::next_double of the i-th draw (rng.hpp:48-56): the stream is a counter, state0 + (i+1) golden
+      const std::uint64_t z = sm64(state0 + i * kGolden64);
+      out = __double2float_rn(__ull2double_rn(z >> 11) * 0x1.0p-53);
+    } else if (rule == 1) {
+      const std::uint64_t z = sm64(state0 + i * kGolden64);
+      out = __double2float_rn(2.0 * (__ull2double_rn(z >> 11) * 0x1.0p-53) - 1.0);
+    } else {
+      const std::uint64_t z0 = sm64(state0 + (2 * i) * kGolden64), z1 = sm64(state0 + (2 * i + 1) * kGolden64);
+      const double u0 = (__ull2double_rn(z0 >> 11) + 1.0) * 0x1.0p-53, u1 = __ull2double_rn(z1 >> 11) * 0x1.0p-53;
+      out = __double2float_rn(stddev * sqrt(-2.0 * log(u0)) * cospi(2.0 * u1));
+    }
+  }
+  x[t] = out;
+}
+
+// ---------------------------------------------------------------------------------- gather + update
+
+struct SmemTables {
+  double erf[65];
+  double ratio[65];
+};
+
+// largest s in [0,15] with knots[s] <= x (piecewise.hpp:36-47) for x >= knots[0]
+__device__ __forceinline__ int segment_of(const double* __restrict__ knots, double x) {
+  int s = x >= knots[8] ? 8 : 0;
+  s += x >= knots[s + 4] ? 4 : 0;
+  s += x >= knots[s + 2] ? 2 : 0;
+  s += x >= knots[s + 1] ? 1 : 0;
+  return s;
+}
+
+__device__ __forceinline__ double quad_eval(const double* __restrict__ t, double x) {
+  const int s = segment_of(t, x);
+  return (t[17 + s] * x + t[33 + s]) * x + t[49 + s];
+}
+
+__device__ __forceinline__ double tail_series(double x) {  // sigmoid.hpp:41-44
+  const double r = 1.0 / (x * x);
+  const double series = 1.0 + r * (-0.5 + r * (0.75 + r * (-1.875 + 6.5625 * r)));
+  return x * 1.77245385090551602729816748334 / series;
+}
+
+// G(x) = e^{-x^2} / erfc(x): FastMath::gauss_erfc_ratio (piecewise.hpp:72-79) or ExactMath (sigmoid.hpp:61-65)
+__device__ __forceinline__ double gauss_erfc_ratio(double x, int exact, const SmemTables& tab) {
+  if (exact) return x <= 6.0 ? exp(-x * x) / erfc(x) : tail_series(x);
+  if (x >= -1.0) return x > 8.0 ? tail_series(x) : quad_eval(tab.ratio, x);
+  if (x < -6.0) return 0.0;
+  // 1 - erf_table(x) with the odd-mirrored table: erf_table(x) = -q(-x) for x < 0
+  return exp(-x * x) / (1.0 + quad_eval(tab.erf, -x));
+}
+
+// parabola_impl + the scalar part of add_pair (sigmoid.hpp:88-101, engine.cpp:56-61):
+//   wf = float(w),  sf = delta > 0 ? float(max(d_target, 0) / delta) : 0,  both 0 when !(w > 0).
+__device__ __forceinline__ void pair_terms(double delta, bool is_edge, const RoundMath& m, const SmemTables& tab,
+                                           float& wf, float& sf) {
+  const double dm = delta - m.mu;
+  const double u = dm * m.inv_sqrt2_sigma;
+  const double g = gauss_erfc_ratio(is_edge ? u : -u, m.exact, tab);
+  const double sg = is_edge ? -g : g;
+  const double w = m.A * g * g + m.B * dm * sg;
+  if (!(w > 0.0)) {
+    wf = 0.0f;
+    sf = 0.0f;
+    return;
+  }
+  wf = static_cast<float>(w);
+  // d_target = delta + sign C g / w  =>  max(d_target,0)/delta = max(delta w + sign C g, 0) / (delta w)
+  const double dw = delta * w;
+  const double num = dw + m.C * sg;
+  sf = (delta > 0.0 && num > 0.0) ? static_cast<float>(num / dw) : 0.0f;
+}
+
+template <int VEC>
+__device__ __forceinline__ void load_row(const float* __restrict__ p, float (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (VEC == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    v[0] = __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_row(float* __restrict__ p, const float (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (VEC == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+__device__ __forceinline__ double shfl_xor_f64(double v, int off) {
+  return __shfl_xor_sync(kFull, v, off);
+}
+
+// One warp per work item.  A row of ld floats is spread over LPR lanes, NV vectors of VEC floats per lane
+// (lane r holds vector r + LPR*j); the warp's 32/LPR lane groups walk the item's lists in parallel, U rows
+// per group in flight.  At d = 2 this degenerates to one thread per list entry (LPR = 1), at d >= 128 to one
+// warp per row (LPR = 32).
+template <int LPR, int NV, int VEC, int U>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, std::uint32_t item_lo,
+                                                          std::uint32_t item_hi) {
+  constexpr int G = 32 / LPR;
+  __shared__ unsigned int sh_hist[2 * kBins];
+  __shared__ SmemTables sh_tab;
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
+  for (int i = threadIdx.x; i < 65; i += kThreads) {
+    sh_tab.erf[i] = a.tab.erf[i];
+    sh_tab.ratio[i] = a.tab.ratio[i];
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPR, r = lane % LPR;
+  const std::uint32_t item = item_lo + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+
+  if (item < item_hi) {
+    const uint4 it = __ldg(a.items + item);
+    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
+    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
+    const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
+    const bool first = begin == row_lo;
+    const std::uint32_t ld = a.ld;
+
+    bool act[NV];
+    float xu[NV][VEC];
+    double xud[NV][VEC];
+    float y[NV][VEC];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      act[j] = static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
+      if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) xud[j][c] = static_cast<double>(xu[j][c]);
+    }
+    float zacc = 0.0f;
+
+    // tally: 0 never, 1 always, 2 when u < other (each undirected edge is met from both endpoints)
+    auto walk = [&](const std::uint32_t* __restrict__ ids, std::uint32_t len, bool is_edge, int tally) {
+      for (std::uint32_t base = 0; base < len; base += G * U) {
+        std::uint32_t other[U];
+        float xv[U][NV][VEC];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const std::uint32_t e = base + q * G + grp;
+          other[q] = e < len ? __ldg(ids + e) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const std::uint32_t src_row = other[q] != 0xffffffffu ? other[q] : u;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) xv[q][j][c] = 0.0f;
+            if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[q][j]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          // pair_distance (engine.cpp:45-52): double accumulation of squared double differences
+          double part = 0.0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+              const double diff = xud[j][c] - static_cast<double>(xv[q][j][c]);
+              part = fma(diff, diff, part);
+            }
+          }
+#pragma unroll
+          for (int off = LPR / 2; off > 0; off >>= 1) part += shfl_xor_f64(part, off);
+          if (other[q] != 0xffffffffu) {
+            const double delta = sqrt(part);
+            if (r == 0 && (tally == 1 || (tally == 2 && u < other[q]))) {
+              // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
+              int b = static_cast<int>(delta / 12.0 * 512.0);
+              b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
+              atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
+            }
+            float wf, sf;
+            pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+            // add_pair, own side (engine.cpp:66-72): y_u += wf * (x_v + sf * (x_u - x_v)); z_u += wf
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) {
+                const float diff = xu[j][c] - xv[q][j][c];
+                y[j][c] += wf * (xv[q][j][c] + sf * diff);
+              }
+            }
+            zacc += wf;
+          }
+        }
+      }
+    };
+
+    walk(a.nbr + begin, end - begin, true, 2);
+    if (a.neg_mode == 0) walk(a.neg_own + begin, end - begin, false, 1);
+    if (first) {
+      if (a.neg_mode == 1) walk(a.neg_own + static_cast<std::size_t>(u) * a.k, a.k, false, 1);
+      const std::uint32_t in_lo = __ldg(a.in_off + u), in_hi = __ldg(a.in_off + u + 1);
+      walk(a.in_anchor + in_lo, in_hi - in_lo, false, 0);
+    }
+
+    // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
+    double ys[NV][VEC];
+    double zs = static_cast<double>(zacc);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        double t = static_cast<double>(y[j][c]);
+#pragma unroll
+        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
+        ys[j][c] = t;
+      }
+    }
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) zs += shfl_xor_f64(zs, off);
+
+    bool finalize = true;
+    if (hub != kNoHub) {
+      const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
+      const std::uint32_t slot = p0 + it.w;
+      if (grp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (!act[j]) continue;
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
+        }
+        if (r == 0) a.part_z[slot] = zs;
+      }
+      __threadfence();
+      __syncwarp();
+      std::uint32_t arrived = 0;
+      if (lane == 0) arrived = atomicAdd(a.hub_arrived + hub, 1u);
+      arrived = __shfl_sync(kFull, arrived, 0);
+      finalize = arrived == q - 1;
+      if (finalize) {  // last slice of the hub: consolidate the partials in slot order
+        __threadfence();
+        zs = 0.0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
+        for (std::uint32_t s = p0; s < p0 + q; ++s) {
+          zs += __ldcg(a.part_z + s);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            if (!act[j]) continue;
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(s) * ld + (r + LPR * j) * VEC + c);
+          }
+        }
+        if (lane == 0) a.hub_arrived[hub] = 0;
+      }
+    }
+
+    if (finalize && grp == 0) {
+      // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (!act[j]) continue;
+        float out[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          out[c] = xu[j][c];
+          if (zs > 0.0) {
+            out[c] = static_cast<float>(ys[j][c] / zs);
+            bad |= !isfinite(out[c]);
+          }
+        }
+        const std::uint32_t col = (r + LPR * j) * VEC;
+        store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+        if (a.cap_y) {
+#pragma unroll
+          for (int c = 0; c < VEC; ++c)
+            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
+        }
+      }
+      if (a.cap_z && r == 0) a.cap_z[u] = zs;
+      if (bad) atomicOr(a.status + kStatNonFinite, 1u);
+    }
+  }
+
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
+    const unsigned int c = sh_hist[i];
+    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
+  }
+}
+
+inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
+  return static_cast<unsigned>((work + per_block - 1) / per_block);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------- launchers
+
+int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream) {
+  if (m == 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words);
+  return 1;
+}
+
+int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::uint32_t n, const std::uint32_t* i,
+                 const std::uint32_t* j, std::uint64_t count, std::uint8_t* out, cudaStream_t stream) {
+  if (count == 0) return 0;
+  probe_kernel<<<blocks_for(count, kThreads), kThreads, 0, stream>>>(hash_words, hash_mask, n, i, j, count, out);
+  return 1;
+}
+
+int launch_sample(const SampleArgs& a, cudaStream_t stream) {
+  if (a.slots == 0) return 0;
+  sample_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a);
+  return 1;
+}
+
+int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
+                cudaStream_t stream) {
+  const unsigned tiles = blocks_for(n, kScanTile);
+  scan_tile_sums_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch);
+  scan_tile_offsets_kernel<<<1, 1024, 0, stream>>>(scratch, tiles);
+  scan_apply_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch, in_off);
+  return 3;
+}
+
+int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32_t* in_anchor, cudaStream_t stream) {
+  if (a.slots == 0) return 0;
+  scatter_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a, in_off, in_anchor);
+  return 1;
+}
+
+int launch_sort_buckets(const std::uint32_t* in_off, std::uint32_t* in_anchor, std::uint32_t n, cudaStream_t stream) {
+  sort_buckets_kernel<<<blocks_for(static_cast<std::uint64_t>(n) * 32, kThreads), kThreads, 0, stream>>>(in_off, in_anchor, n);
+  return 1;
+}
+
+int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t* eid_role, std::uint64_t slots,
+                              std::uint32_t* out, cudaStream_t stream) {
+  if (slots == 0) return 0;
+  unpermute_kernel<<<blocks_for(slots, kThreads), kThreads, 0, stream>>>(neg_own, eid_role, slots, out);
+  return 1;
+}
+
+int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule, std::uint64_t seed,
+                       double stddev, cudaStream_t stream) {
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * ld;
+  if (total == 0) return 0;
+  // SplitMix(mix_seed(seed, 0x1217)) for the reference rule (engine.cpp:121); other rules use their own key
+  const std::uint64_t state0 = mix(seed, rule == 0 ? 0x1217ull : 0x1217ull + 0x100ull * rule);
+  init_coords_kernel<<<blocks_for(total, kThreads), kThreads, 0, stream>>>(x, n, dim, ld, rule, state0, stddev);
+  return 1;
+}
+
+namespace {
+template <int LPR, int NV, int VEC, int U>
+void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
+  gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
+}
+}  // namespace
+
+int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
+  if (hi <= lo) return 0;
+  const std::uint32_t ld = a.ld;
+  if (ld == 1) gather_go<1, 1, 1, 4>(a, lo, hi, stream);
+  else if (ld == 2) gather_go<1, 1, 2, 4>(a, lo, hi, stream);
+  else if (ld <= 4) gather_go<1, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 8) gather_go<2, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 16) gather_go<4, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 32) gather_go<8, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 64) gather_go<16, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 128) gather_go<32, 1, 4, 4>(a, lo, hi, stream);
+  else if (ld <= 256) gather_go<32, 2, 4, 2>(a, lo, hi, stream);
+  else if (ld <= 512) gather_go<32, 4, 4, 1>(a, lo, hi, stream);
+  else gather_go<32, 8, 4, 1>(a, lo, hi, stream);  // ld <= 1024 (checked at create)
+  return 1;
+}
+
+}  // namespace gempe

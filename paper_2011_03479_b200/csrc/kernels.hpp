@@ -1,0 +1,109 @@
+// Launch interface between the context (host) and the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gempe {
+
+constexpr int kBins = 512;
+constexpr std::uint32_t kNoHub = 0xffffffffu;
+constexpr std::uint32_t kNotLocal = 0xffffffffu;
+
+// status word layout (device u32[8])
+enum StatusSlot { kStatNonFinite = 0, kStatRetryCap = 1, kStatDrawsLo = 2, kStatDrawsHi = 3 };
+
+// Per-round scalars of parabola_impl (sigmoid.hpp:88-101), folded on the host in double:
+//   u = (delta - mu) * inv_sqrt2_sigma,  w = A g^2 + sign B (delta-mu) g,  d = delta + sign C g / w.
+struct RoundMath {
+  double mu;
+  double inv_sqrt2_sigma;  // 1 / (sqrt(2) sigma)
+  double A;                // 2 / (pi ln2 sigma^2)
+  double B;                // 1 / (sqrt(2 pi) ln2 sigma^3)
+  double C;                // 1 / (sqrt(2 pi) ln2 sigma)
+  int exact;               // 1: exp(-x^2)/erfc(x), 0: piecewise tables
+};
+
+// knots[17] a[16] b[16] c[16] per table (the lo/hi clamps are the first/last knot).
+struct DeviceTables {
+  double erf[65];
+  double ratio[65];
+};
+
+// Vertex ownership under sharding: block-cyclic over work ids, block = block_rows rows:
+// owner(v) = (v / block_rows) % world.  world == 1 => everything is local.
+struct Ownership {
+  std::uint32_t block_rows;
+  std::uint32_t world;
+  std::uint32_t rank;
+};
+
+struct SampleArgs {
+  std::uint32_t n;
+  std::uint64_t slots;            // S
+  int neg_mode;                   // 0 PER_EDGE_2 (slot = CSR position), 1 PER_VERTEX_K (slot = v*k+draw)
+  std::uint32_t k;
+  int rng;                        // 0 reference replay, 1 philox
+  std::uint64_t stream_base;      // mix(seed, iter)  (reference) / seed (philox)
+  std::uint64_t iter;
+  const std::uint32_t* csr_src;   // PER_EDGE_2: anchor of each CSR position
+  const std::uint32_t* eid_role;  // PER_EDGE_2: 2*edge + role (role 0: anchor is src[e], 1: dst[e])
+  const std::uint32_t* hash_words;  // bit-packed direct-mapped table, 2^bits bits
+  std::uint32_t hash_mask;        // 2^bits - 1
+  std::uint32_t* neg_own;         // out: accepted partner per slot
+  std::uint32_t* in_cnt;          // in/out: per-vertex count of incoming samples (zeroed before)
+  std::uint32_t* in_rank;         // out: arrival rank of the slot inside its partner's bucket
+  std::uint32_t* status;
+  Ownership own;
+};
+
+struct GatherArgs {
+  const float* x_cur;
+  float* x_next;
+  std::uint32_t n, dim, ld;
+  const std::uint32_t* rowptr;     // n+1
+  const std::uint32_t* nbr;        // 2m, both directions
+  const std::uint32_t* neg_own;
+  const std::uint32_t* in_off;     // n+1
+  const std::uint32_t* in_anchor;
+  const uint4* items;              // {vertex, first adjacency position, hub id | kNoHub, index inside hub}
+  const std::uint32_t* hub_first;  // first partial slot of hub h
+  const std::uint32_t* hub_items;  // number of items of hub h
+  std::uint32_t* hub_arrived;      // arrival counters (zero between rounds)
+  double* part_y;                  // partial slots x ld
+  double* part_z;
+  unsigned long long* hist;        // [2*kBins]: edge tallies then non-edge tallies
+  std::uint32_t* status;
+  double* cap_y;                   // optional capture (n*dim, n), null when off
+  double* cap_z;
+  std::uint32_t chunk_entries;
+  std::uint32_t k;
+  int neg_mode;
+  RoundMath math;
+  DeviceTables tab;
+};
+
+// ---- launchers (all asynchronous on `stream`; return the number of kernels launched) ---------------
+int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream);
+int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::uint32_t n,
+                 const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out,
+                 cudaStream_t stream);
+int launch_sample(const SampleArgs& a, cudaStream_t stream);
+// exclusive scan of in_cnt[n] into in_off[n+1]; scratch must hold ceil(n/4096)+1 words
+int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
+                cudaStream_t stream);
+int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32_t* in_anchor,
+                   cudaStream_t stream);
+// sorts every incoming bucket ascending (deterministic mode)
+int launch_sort_buckets(const std::uint32_t* in_off, std::uint32_t* in_anchor, std::uint32_t n,
+                        cudaStream_t stream);
+// reorders neg_own (CSR order) into reference slot order 2e+draw (test hook)
+int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t* eid_role, std::uint64_t slots,
+                              std::uint32_t* out, cudaStream_t stream);
+int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, cudaStream_t stream);
+int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,
+                       std::uint64_t seed, double stddev, cudaStream_t stream);
+
+}  // namespace gempe

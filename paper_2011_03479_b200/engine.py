@@ -1,0 +1,412 @@
+"""Host-side mirror of the reference's engine interface over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/entropy_embed/engine.hpp
+(``Graph``, ``IterationConfig``, ``EmbeddingEngine``, ``embed``) and errors.hpp; everything numerical happens
+in libgempe_b200.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import (HIST_BINS, INIT_NORMAL, INIT_REFERENCE, INIT_UNIFORM_PM1, MATH_EXACT, MATH_TABLES,
+                    NEG_PER_EDGE_2, NEG_PER_VERTEX_K, RNG_PHILOX, RNG_REFERENCE)
+
+
+# ---- errors.hpp:10-47 --------------------------------------------------------------------------------
+class ConfigError(RuntimeError):
+    """config_error: invalid configuration or request (exit code 1)."""
+
+
+class DataError(RuntimeError):
+    """data_error: structurally invalid data (exit code 2)."""
+
+
+class NearCompleteGraphError(DataError):
+    """near_complete_graph_error: a sample stream hit the 10^4 retry cap."""
+
+
+class DivergenceError(RuntimeError):
+    """divergence_error: a coordinate became non-finite (exit code 3)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure or no device: the path has no CPU fallback."""
+
+
+def _raise(rc: int, msg: str):
+    if rc == _capi.OK:
+        return
+    if rc == _capi.ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == _capi.ERR_DIVERGENCE:
+        raise DivergenceError(msg)
+    if rc == _capi.ERR_CUDA:
+        raise CudaError(msg)
+    if "near-complete" in msg:
+        raise NearCompleteGraphError(msg)
+    raise DataError(msg)
+
+
+@dataclass
+class Graph:
+    """graph.hpp:12-23: canonical undirected graph, ids 0..n-1, SoA edge arrays."""
+    n: int
+    src: np.ndarray
+    dst: np.ndarray
+
+    def __post_init__(self):
+        self.src = np.ascontiguousarray(self.src, np.uint32)
+        self.dst = np.ascontiguousarray(self.dst, np.uint32)
+        if self.src.shape != self.dst.shape:
+            raise DataError("src/dst length mismatch")
+
+    def edge_count(self) -> int:
+        return int(self.src.size)
+
+    def pair_count(self) -> int:
+        return self.n * (self.n - 1) // 2 if self.n > 0 else 0
+
+
+@dataclass
+class IterationConfig:
+    """engine.hpp:29-38 plus the BASELINE extensions (negatives per vertex, device)."""
+    max_iters: int = 100
+    lane_width: int = 16
+    workers: int = 0
+    convergence_tol: float = 1e-4
+    convergence_window: int = 5
+    relabel_period: int = 0
+    fast_math: bool = True
+    hash_bits: Optional[int] = None
+    neg_mode: int = NEG_PER_EDGE_2
+    negatives: int = 0
+    device: int = 0
+
+
+@dataclass
+class IterationStats:
+    pe_estimate: float = 0.0
+    sigma: float = 0.0
+
+
+@dataclass
+class EmbedResult:
+    """engine.hpp:98-107."""
+    embedding: np.ndarray
+    pe_trace: np.ndarray
+    final_sigma: float = 1.0
+    converged: bool = False
+    degenerate: bool = False
+    iterations: int = 0
+    relabel_forward: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    last_hist_edge: np.ndarray = field(default_factory=lambda: np.zeros(HIST_BINS, np.uint64))
+    last_hist_nonedge: np.ndarray = field(default_factory=lambda: np.zeros(HIST_BINS, np.uint64))
+    last_nonedge_weight: float = 1.0
+
+
+class Context:
+    """One GPU shard of the engine (gempe_ctx): the Jacobi round and its test hooks."""
+
+    def __init__(self, g: Graph, dim: int, seed: int = 1, *, neg_mode=NEG_PER_EDGE_2, negatives=0,
+                 math=MATH_TABLES, rng=RNG_REFERENCE, hash_bits=0, relabel=True, device=0, rank=0, world=1,
+                 comm_chunks=1, chunk_entries=0, deterministic=False):
+        self._L = _capi.load()
+        self._h = C.c_void_p()
+        opt = _capi.Options()
+        self._L.gempe_default_options(C.byref(opt))
+        opt.dim, opt.seed, opt.neg_mode, opt.negatives = dim, seed, neg_mode, negatives
+        opt.math, opt.rng, opt.hash_bits, opt.relabel = math, rng, hash_bits or 0, int(relabel)
+        opt.device, opt.rank, opt.world, opt.comm_chunks = device, rank, world, comm_chunks
+        opt.chunk_entries, opt.deterministic = chunk_entries, int(deterministic)
+        self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
+        rc = self._L.gempe_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), C.byref(opt))
+        if rc != _capi.OK:
+            self._h = C.c_void_p()
+            _raise(rc, self._L.gempe_last_error(None).decode())
+
+    # -- lifetime ------------------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._L.gempe_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != _capi.OK:
+            _raise(rc, self._L.gempe_last_error(self._h).decode())
+
+    # -- properties ----------------------------------------------------------------------------------
+    @property
+    def degenerate(self) -> bool:
+        return bool(self._L.gempe_is_degenerate(self._h))
+
+    @property
+    def hash_bits(self) -> int:
+        return self._L.gempe_hash_bits(self._h)
+
+    @property
+    def sample_slots(self) -> int:
+        return self._L.gempe_sample_slots(self._h)
+
+    @property
+    def pair_terms(self) -> int:
+        return self._L.gempe_pair_terms(self._h)
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        return self._L.gempe_algorithmic_bytes(self._h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return self._L.gempe_kernel_launches(self._h)
+
+    @property
+    def row_stride(self) -> int:
+        return self._L.gempe_row_stride(self._h)
+
+    @property
+    def padded_rows(self) -> int:
+        return self._L.gempe_padded_rows(self._h)
+
+    @property
+    def block_rows(self) -> int:
+        return self._L.gempe_block_rows(self._h)
+
+    # -- graph / coordinates -------------------------------------------------------------------------
+    def work_graph(self):
+        src = np.zeros(self.m, np.uint32)
+        dst = np.zeros(self.m, np.uint32)
+        to_work = np.zeros(self.n, np.uint32)
+        self._check(self._L.gempe_get_work_graph(self._h, _capi.ptr(src), _capi.ptr(dst), _capi.ptr(to_work)))
+        return src, dst, to_work
+
+    def set_coords(self, x_work: np.ndarray):
+        x = np.ascontiguousarray(x_work, np.float32)
+        if x.shape != (self.n, self.dim):
+            raise ConfigError(f"coordinates must be {self.n}x{self.dim}")
+        self._check(self._L.gempe_set_coords(self._h, _capi.ptr(x)))
+
+    def get_coords(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.n, self.dim), np.float32)
+        self._check(self._L.gempe_get_coords(self._h, _capi.ptr(out)))
+        return out
+
+    def init_coords(self, rule=INIT_REFERENCE, seed=1, std=0.01):
+        self._check(self._L.gempe_init_coords(self._h, rule, seed, std))
+
+    def relabel(self, relabel_seed: int):
+        self._check(self._L.gempe_relabel(self._h, relabel_seed))
+
+    # -- the round -----------------------------------------------------------------------------------
+    def iterate(self, mu: float, sigma: float, iter_index: int):
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        self._check(self._L.gempe_iterate(self._h, mu, sigma, iter_index, _capi.ptr(he), _capi.ptr(hn)))
+        return he, hn
+
+    def iterate_async(self, mu: float, sigma: float, iter_index: int):
+        self._check(self._L.gempe_iterate_async(self._h, mu, sigma, iter_index))
+
+    def sync(self):
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        self._check(self._L.gempe_sync(self._h, _capi.ptr(he), _capi.ptr(hn)))
+        return he, hn
+
+    def elapsed_ms(self):
+        out = (C.c_float * 3)()
+        self._check(self._L.gempe_elapsed_ms(self._h, C.byref(out)))
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def set_capture(self, on: bool):
+        self._check(self._L.gempe_set_capture(self._h, int(on)))
+
+    def get_yz(self):
+        y = np.zeros((self.n, self.dim), np.float64)
+        z = np.zeros(self.n, np.float64)
+        self._check(self._L.gempe_get_yz(self._h, _capi.ptr(y), _capi.ptr(z)))
+        return y, z
+
+    # -- bit-exact hooks -----------------------------------------------------------------------------
+    def probe(self, i, j) -> np.ndarray:
+        i = np.ascontiguousarray(i, np.uint32)
+        j = np.ascontiguousarray(j, np.uint32)
+        out = np.zeros(i.size, np.uint8)
+        self._check(self._L.gempe_probe(self._h, _capi.ptr(i), _capi.ptr(j), i.size, _capi.ptr(out)))
+        return out
+
+    def sample(self, iter_index: int):
+        partners = np.zeros(max(self.sample_slots, 1), np.uint32)
+        draws = C.c_uint64()
+        self._check(self._L.gempe_sample(self._h, iter_index, _capi.ptr(partners), C.byref(draws)))
+        return partners[:self.sample_slots], draws.value
+
+    # -- sharded stepping ----------------------------------------------------------------------------
+    def set_stream(self, cuda_stream: int):
+        self._check(self._L.gempe_set_stream(self._h, C.c_void_p(cuda_stream)))
+
+    def device_coords(self, which: int) -> int:
+        return self._L.gempe_device_coords(self._h, which)
+
+    def begin_round(self, mu, sigma, iter_index):
+        self._check(self._L.gempe_begin_round(self._h, mu, sigma, iter_index))
+
+    def gather_chunk(self, chunk: int):
+        self._check(self._L.gempe_gather_chunk(self._h, chunk))
+
+    def end_round(self):
+        self._check(self._L.gempe_end_round(self._h))
+
+
+class EmbeddingEngine:
+    """engine.hpp:112-134 (run-level facade, gempe_engine)."""
+
+    def __init__(self, g: Graph, dim: int, cfg: IterationConfig, seed: int):
+        self._L = _capi.load()
+        self._h = C.c_void_p()
+        c = _capi.IterationConfigC()
+        self._L.gempe_default_iteration_config(C.byref(c))
+        c.max_iters, c.lane_width, c.workers = cfg.max_iters, cfg.lane_width, cfg.workers
+        c.convergence_tol, c.convergence_window = cfg.convergence_tol, cfg.convergence_window
+        c.relabel_period, c.fast_math = cfg.relabel_period, int(cfg.fast_math)
+        c.hash_bits = 0 if cfg.hash_bits is None else cfg.hash_bits
+        if cfg.hash_bits is not None and not (1 <= cfg.hash_bits <= 31):
+            raise ConfigError("hash table bits must be in [1,31]")
+        c.neg_mode, c.negatives, c.device = cfg.neg_mode, cfg.negatives, cfg.device
+        self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
+        self._pe_trace = []
+        rc = self._L.gempe_engine_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,
+                                         C.byref(c), seed)
+        if rc != _capi.OK:
+            self._h = C.c_void_p()
+            _raise(rc, self._L.gempe_last_error(None).decode())
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._L.gempe_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != _capi.OK:
+            _raise(rc, self._L.gempe_engine_last_error(self._h).decode())
+
+    def context(self) -> "Context":
+        """Borrowed low-level view (work graph, coordinates, hooks) of the engine's device context."""
+        ctx = Context.__new__(Context)
+        ctx._L = self._L
+        ctx._h = C.c_void_p(self._L.gempe_engine_context(self._h))
+        ctx.n, ctx.m, ctx.dim = self.n, self.m, self.dim
+        ctx.close = lambda: None  # borrowed: never destroys
+        return ctx
+
+    def degenerate(self) -> bool:
+        return bool(self._L.gempe_engine_degenerate(self._h))
+
+    def iteration(self) -> int:
+        return self._L.gempe_engine_iteration(self._h)
+
+    def sigma(self) -> float:
+        return self._L.gempe_engine_sigma(self._h)
+
+    def pe_trace(self):
+        return list(self._pe_trace)
+
+    def work_graph(self):
+        return self.context().work_graph()
+
+    def work_coords(self) -> np.ndarray:
+        return self.context().get_coords()
+
+    def run_single_iteration(self) -> IterationStats:
+        pe, sg = C.c_double(), C.c_double()
+        self._check(self._L.gempe_engine_run_single_iteration(self._h, C.byref(pe), C.byref(sg)))
+        self._pe_trace.append(pe.value)
+        return IterationStats(pe.value, sg.value)
+
+    def run(self, max_trace: int = 1 << 20) -> EmbedResult:
+        emb = np.zeros((self.n, self.dim), np.float32)
+        trace = np.zeros(max_trace, np.float64)
+        fwd = np.zeros(self.n, np.uint32)
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        r = _capi.EmbedResultC()
+        r.embedding, r.pe_trace, r.pe_trace_cap = _capi.ptr(emb), _capi.ptr(trace), max_trace
+        r.relabel_forward, r.last_hist_edge, r.last_hist_nonedge = _capi.ptr(fwd), _capi.ptr(he), _capi.ptr(hn)
+        self._check(self._L.gempe_engine_run(self._h, C.byref(r)))
+        self._pe_trace = list(trace[:r.pe_trace_len])
+        return EmbedResult(emb, trace[:r.pe_trace_len].copy(), r.final_sigma, bool(r.converged),
+                           bool(r.degenerate), r.iterations, fwd, he, hn, r.last_nonedge_weight)
+
+
+def embed(g: Graph, dim: int, cfg: Optional[IterationConfig] = None, seed: int = 1, *, iterations=None,
+          negatives=None) -> EmbedResult:
+    """``embed(g, dim, cfg, seed)`` (engine.hpp:170-171).  The BASELINE convenience form
+    ``embed(g, dim, iterations=I, negatives=k, seed=s)`` selects k draws per vertex."""
+    cfg = cfg or IterationConfig()
+    if iterations is not None:
+        cfg.max_iters = iterations
+    if negatives is not None:
+        cfg.neg_mode, cfg.negatives = NEG_PER_VERTEX_K, negatives
+    engine = EmbeddingEngine(g, dim, cfg, seed)
+    try:
+        return engine.run()
+    finally:
+        engine.close()
+
+
+# ---- host numerics (no GPU) ----------------------------------------------------------------------------
+def fastmath_table(which: int):
+    out = np.zeros(67, np.float64)
+    odd = _capi.load().gempe_host_fastmath_table(which, out)
+    if odd < 0:
+        raise ConfigError("table build failed")
+    return out, odd
+
+
+def optimize_sigma(hist_edge, hist_nonedge, nonedge_weight, mu=1.5):
+    steps = C.c_int()
+    s = _capi.load().gempe_host_optimize_sigma(np.ascontiguousarray(hist_edge, np.uint64),
+                                               np.ascontiguousarray(hist_nonedge, np.uint64), nonedge_weight, mu,
+                                               C.byref(steps))
+    if s != s:
+        raise ConfigError("cannot optimize sigma on an empty histogram")
+    return s, steps.value
+
+
+def histogram_objective(hist_edge, hist_nonedge, nonedge_weight, mu, sigma):
+    return _capi.load().gempe_host_histogram_objective(np.ascontiguousarray(hist_edge, np.uint64),
+                                                      np.ascontiguousarray(hist_nonedge, np.uint64),
+                                                      nonedge_weight, mu, sigma)
+
+
+def histogram_objective_dsigma(hist_edge, hist_nonedge, nonedge_weight, mu, sigma):
+    return _capi.load().gempe_host_histogram_objective_dsigma(np.ascontiguousarray(hist_edge, np.uint64),
+                                                             np.ascontiguousarray(hist_nonedge, np.uint64),
+                                                             nonedge_weight, mu, sigma)
+
+
+def random_relabel(n: int, seed: int) -> np.ndarray:
+    fwd = np.zeros(n, np.uint32)
+    _capi.load().gempe_host_random_relabel(n, seed, fwd)
+    return fwd
+
+
+def mix_seed(seed: int, component: int) -> int:
+    return _capi.load().gempe_host_mix_seed(seed, component)

