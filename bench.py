@@ -1,0 +1,273 @@
+#!/usr/bin/env python
+"""Benchmark of the GEMPE round (BASELINE.json metric: edge+negative gradient terms per second per iteration,
+and the fraction of the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+A "step" is one GEMPE iteration (sampling passes + gradient gather + update) over the synthetic graph of the
+chosen BASELINE configuration (default c4: R-MAT scale 20, d=128, 20 negatives per vertex).  One JSON line is
+printed by rank 0.  `--impl reference` times the reference's own CPU engine (oracle/_ref) on host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pair_terms_per_second"
+UNIT = "pair-terms/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--neg-mode", default="per_vertex_k", choices=["per_vertex_k", "per_edge_2"])
+    p.add_argument("--comm-chunks", type=int, default=4)
+    p.add_argument("--chunk-entries", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline budget on rank 0")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload_name(cfg):
+    return {"c1": "SBM n=3000 6 blocks d=2 k=5", "c2": "Barabasi-Albert n=1e5 m=8 d=2 k=10",
+            "c3": "Dirichlet-SBM n=2e5 deg20 d=64 k=10", "c4": "R-MAT scale 20 ef16 d=128 k=20",
+            "c5": "R-MAT scale 24 ef16 d=128 k=20"}[cfg]
+
+
+class ClockSampler(threading.Thread):
+    """Samples nvidia-smi clocks and throttle reasons while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        super().__init__(daemon=True)
+        self.index, self.rows, self._halt = index, [], threading.Event()
+
+    def run(self):
+        while not self._halt.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i",
+                                      str(self.index)], capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._halt.wait(0.2)
+
+    def finish(self):
+        self._halt.set()
+        self.join(timeout=6)
+        sm = sorted(int(r[0]) for r in self.rows if r[0].isdigit())
+        mx = [int(r[1]) for r in self.rows if r[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v.lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_arm(n, src, dst, dim, budget_s, steps=None, warmup=1):
+    """Times EmbeddingEngine::run_single_iteration of the UNMODIFIED reference (oracle/_ref) on the host cores.
+    Bounded sample: the leading edges of the workload's edge list on the full vertex set (the reference's
+    own 2-draws-per-edge sampling, so pair-terms = 3 m'), sized from a probe round to fit the budget."""
+    import oracle as O
+    ref = O.Ref()
+    cores = os.cpu_count() or 1
+    # accumulator bank = workers * lanes * n * (d+1) * 4 bytes (engine.cpp:77-86): keep it under ~40% of RAM
+    try:
+        avail = int(open("/proc/meminfo").read().split("MemAvailable:")[1].split()[0]) * 1024
+    except Exception:
+        avail = 32 << 30
+    lanes = 16 if dim <= 8 else 1
+    workers = max(1, min(cores, int(0.4 * avail / max(1, lanes * n * (dim + 1) * 4))))
+    m_probe = min(len(src), 200_000)
+
+    def rate(m_use, rounds, warm):
+        eng = O.RefEngine(ref, n, src[:m_use], dst[:m_use], dim, 1, lane_width=lanes, workers=workers)
+        eng.set_capture(False)
+        for _ in range(warm):
+            eng.iterate(capture=False)
+        times = []
+        for _ in range(rounds):
+            t0 = time.perf_counter()
+            eng.iterate(capture=False)
+            times.append(time.perf_counter() - t0)
+        return 3.0 * m_use / float(np.median(times)), float(np.median(times))
+
+    r_probe, _ = rate(m_probe, 1, 1)
+    rounds = steps if steps else 3
+    m_use = int(min(len(src), max(m_probe, r_probe / 3.0 * budget_s / (rounds + warmup + 1))))
+    value, sec = rate(m_use, rounds, warmup)
+    return {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": f"first {m_use} of {len(src)} edges on all {n} vertices, reference sampling (2 draws/edge, "
+                      f"3m pair-terms), lane_width={lanes}, {rounds} timed rounds, median {sec:.3f} s/round",
+            "host_cores": cores}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2011_03479_b200 import graphgen
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config)
+        base = cpu_reference_arm(n, src, dst, dim, max(args.cpu_seconds, 30.0), steps=args.steps, warmup=args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 coordinates, f64 distance/parabola",
+                "data": "synthetic", "config": {"workload": workload_name(args.config), "n": n, "m": int(len(src))},
+                "cpu_baseline": base,
+                "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2011_03479_b200 as P
+    from paper_2011_03479_b200 import sharded
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    n, src, dst, dim, k, _, init, std = graphgen.make_config(args.config)
+    g = P.Graph(n, src, dst)
+    neg_mode = P.NEG_PER_VERTEX_K if args.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
+    eng = sharded.make_cuda_engine(g, dim, 1, comm_chunks=args.comm_chunks, device=local_rank, neg_mode=neg_mode,
+                                   negatives=k if neg_mode == P.NEG_PER_VERTEX_K else 0,
+                                   chunk_entries=args.chunk_entries)
+    ctx = eng.ops.ctx
+    ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
+    stream = eng.ops.stream
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: real iterations with the host sigma search (the state the timed rounds start from)
+    for _ in range(max(args.warmup, 3)):
+        eng.run_single_iteration()
+    mu, sigma = eng.mu, eng.sigma
+
+    sampler = ClockSampler(local_rank)
+    launches0 = ctx.kernel_launches
+    ctx.elapsed_ms()  # reset the context's event log
+    barrier()
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        if world > 1:
+            eng.round_async(mu, sigma, eng.iter + s)
+        else:
+            ctx.iterate_async(mu, sigma, eng.iter + s)
+    if world > 1:
+        with torch.cuda.stream(stream):
+            eng._wait_pending()
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.finish()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches - launches0
+    he, hn = ctx.sync()  # status check of the last timed round (raises on divergence / retry cap)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pair_terms = ctx.pair_terms  # m + S, job-wide per iteration
+    ms_per_step = ms / args.steps
+    value = pair_terms / (ms_per_step * 1e-3)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 coordinates, f64 distance/parabola", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "n": n, "m": int(len(src)), "dim": dim,
+                       "negatives": "k=%d per vertex" % k if neg_mode == P.NEG_PER_VERTEX_K else "2 per edge",
+                       "pair_terms_per_iteration": int(pair_terms), "sigma": sigma,
+                       "l2": "inputs larger than L2 (X %.0f MB + lists)" % (n * dim * 4 / 1e6) if n * dim * 4 > 126e6
+                             else "working set fits L2 (reported as is)",
+                       "parallelism": f"vertex-sharded x{world}, all-gather chunks={eng.chunks}" if world > 1 else "1 GPU"},
+            "clocks": clocks, "gpu_launches": int(launches)}
+
+    if rank == 0 and world == 1:
+        # roofline of the dominant kernel (gather+update), timed live with CUDA events on its own stream
+        tot, samp_ms, gath_ms = ctx.elapsed_ms()
+        draws = None
+        _, draws = ctx.sample(eng.iter)  # p-bar: LCG draws per accepted sample
+        p_bar = draws / max(1, ctx.sample_slots)
+        b_alg = ctx.algorithmic_bytes + int((p_bar - 1.0) * ctx.sample_slots)
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        gather_s = gath_ms / args.steps * 1e-3
+        achieved = b_alg / gather_s / 1e9
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
+        except Exception:
+            pass
+        line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                            "traffic": traffic, "kernel": "gather_kernel", "algorithmic_bytes": int(b_alg),
+                            "kernel_ms": gath_ms / args.steps, "sampling_passes_ms": samp_ms / args.steps,
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
+                            "draws_per_sample": p_bar}
+
+        # end to end through the C-ABI with HOST buffers: X_t in (pinned), round, X_{t+1} + tallies out
+        x_host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+        x_np = x_host.numpy()
+        ctx.get_coords(x_np)
+        steps_e2e = max(1, args.e2e_steps)
+        t_e2e = []
+        for s in range(steps_e2e + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.set_coords(x_np)
+            ctx.iterate(mu, sigma, eng.iter + s)
+            ctx.get_coords(x_np)
+            t_e2e.append(time.perf_counter() - t0)
+        e2e_s = float(np.median(t_e2e[1:]))
+        line["e2e"] = {"value": pair_terms / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * dim * 4),
+                       "d2h_bytes_per_step": int(n * dim * 4 + 2 * 512 * 8), "ms_per_step": e2e_s * 1e3,
+                       "call": "gempe_set_coords + gempe_iterate + gempe_get_coords (pinned host buffers)"}
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_reference_arm(n, src, dst, dim, args.cpu_seconds)
+            except Exception as e:  # the reference build is test infrastructure; its absence is reported, not fatal
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+    elif rank == 0:
+        x_bytes = n * dim * 4
+        line["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                       "note": "multi-GPU e2e not measured separately; state is device-resident (see N=1 line)",
+                       "allgather_bytes_per_step": int(x_bytes * (world - 1) / world)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -29,12 +29,17 @@ class DeviceBuffer {
     count_ = count;
     if (count == 0) return;
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&ptr_), count * sizeof(T)), "cudaMalloc");
-    if (zero) cuda_check(cudaMemset(ptr_, 0, count * sizeof(T)), "cudaMemset");
+    if (zero) {
+      // the legacy-stream memset is not ordered against the context's non-blocking stream: wait for it
+      cuda_check(cudaMemset(ptr_, 0, count * sizeof(T)), "cudaMemset");
+      cuda_check(cudaDeviceSynchronize(), "cudaMemset");
+    }
   }
   void upload(const std::vector<T>& host) {
     allocate(host.size());
     if (!host.empty()) {
       cuda_check(cudaMemcpy(ptr_, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+      cuda_check(cudaDeviceSynchronize(), "upload");  // pageable H2D may still be in flight on return
     }
   }
   void release() {

@@ -1,0 +1,150 @@
+"""Vertex-sharded GEMPE rounds, one process per GPU.
+
+Every rank holds the full X_t, CSR and edge filter; work ids (already randomly relabelled) are owned
+block-cyclically -- block b of `block_rows` rows belongs to rank b % world, comm chunk b // world -- so the
+updated rows of chunk c of all ranks form ONE contiguous region of X_{t+1}.  That makes the exchange an
+in-place ``all_gather_into_tensor`` per chunk, issued as soon as the chunk's gather kernel is enqueued and
+overlapped with the next chunk's kernel; the sampling passes of round t+1 do not read X and are enqueued
+before the wait on round t's last all-gather.  Partner-side sample terms need no exchange: each rank
+enumerates all sample streams (integer work) and keeps those whose partner it owns.  The 2x512 tallies are
+summed with one all_reduce.
+
+The collective logic is backend-agnostic (`ops` supplies the compute); tests drive it with gloo on CPU
+tensors, the product with `CudaShardOps` over NCCL.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from .engine import Context, Graph, optimize_sigma, histogram_objective
+
+HIST = _capi.HIST_BINS
+
+
+def block_layout(n: int, world: int, comm_chunks: int):
+    """(block_rows, padded_rows) of the block-cyclic ownership map (same rule as gempe_create)."""
+    blocks = world * comm_chunks
+    block_rows = (max(n, 1) + blocks - 1) // blocks
+    return block_rows, blocks * block_rows
+
+
+def owner_of(v, block_rows: int, world: int):
+    return (np.asarray(v) // block_rows) % world
+
+
+class _DeviceArray:
+    def __init__(self, ptr: int, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr, data=(int(ptr), False), version=3)
+
+
+class CudaShardOps:
+    """Compute backend: the CUDA context of this rank, launching on torch's current stream."""
+
+    def __init__(self, g: Graph, dim: int, seed: int, rank: int, world: int, comm_chunks: int, device: int, **kw):
+        self.ctx = Context(g, dim, seed, rank=rank, world=world, comm_chunks=comm_chunks, device=device, **kw)
+        self.device = torch.device("cuda", device)
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.rows, self.ld = self.ctx.padded_rows, self.ctx.row_stride
+
+    def x_next(self) -> torch.Tensor:
+        ptr = self.ctx.device_coords(1)
+        return torch.as_tensor(_DeviceArray(ptr, (self.rows, self.ld)), device=self.device)
+
+    def begin_round(self, mu, sigma, it):
+        self.ctx.begin_round(mu, sigma, it)
+
+    def gather_chunk(self, c):
+        self.ctx.gather_chunk(c)
+
+    def end_round(self):
+        self.ctx.end_round()
+
+    def tallies(self) -> torch.Tensor:
+        """int64[1024] on the compute device (edge bins then non-edge bins); synchronises the round."""
+        he, hn = self.ctx.sync()
+        return torch.from_numpy(np.concatenate([he, hn]).astype(np.int64)).to(self.device)
+
+
+class ShardedEngine:
+    """Drives rounds over a process group.  `ops` needs x_next(), begin_round, gather_chunk, end_round,
+    tallies(); `stream` (optional) is the CUDA stream the ops launch on."""
+
+    def __init__(self, ops, n: int, m: int, world: int, rank: int, comm_chunks: int, group=None, stream=None):
+        self.ops, self.n, self.m, self.world, self.rank, self.chunks = ops, n, m, world, rank, comm_chunks
+        self.group, self.stream = group, stream
+        self.block_rows, self.rows = block_layout(n, world, comm_chunks)
+        self.mu, self.sigma, self.iter = 1.5, 1.0, 0
+        self.pe_trace: List[float] = []
+        self._pending = []
+
+    def _wait_pending(self):
+        for w in self._pending:
+            w.wait()
+        self._pending = []
+
+    def round_async(self, mu: float, sigma: float, it: int):
+        """Enqueues one round: sampling passes, then per comm chunk the gather kernel and the all-gather of
+        that chunk's updated blocks.  Returns without waiting."""
+        ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
+        with ctx:
+            self.ops.begin_round(mu, sigma, it)  # X-independent: overlaps the previous round's last exchange
+            self._wait_pending()                 # X_t must be complete before the first gather reads it
+            x_next = self.ops.x_next()
+            span = self.world * self.block_rows
+            for c in range(self.chunks):
+                self.ops.gather_chunk(c)
+                if self.world > 1:
+                    region = x_next[c * span:(c + 1) * span]
+                    mine = region[self.rank * self.block_rows:(self.rank + 1) * self.block_rows]
+                    self._pending.append(dist.all_gather_into_tensor(region, mine, group=self.group, async_op=True))
+            self.ops.end_round()
+
+    def finish_round(self):
+        """Waits for the exchange and returns the job-wide tallies (edge[512], nonedge[512])."""
+        ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
+        with ctx:
+            self._wait_pending()
+            t = self.ops.tallies()
+            if self.world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        t = t.cpu().numpy().astype(np.uint64)
+        return t[:HIST], t[HIST:]
+
+    def run_single_iteration(self):
+        """EmbeddingEngine::run_single_iteration across the group: every rank computes the same sigma from
+        the reduced tallies (engine.cpp:293-314)."""
+        self.round_async(self.mu, self.sigma, self.iter)
+        he, hn = self.finish_round()
+        pairs = self.n * (self.n - 1) // 2
+        samples = int(hn.sum())
+        weight = (pairs - self.m) / samples if samples else 1.0
+        self.sigma = min(optimize_sigma(he, hn, weight, self.mu)[0], self.sigma * 1.5)
+        pe = histogram_objective(he, hn, weight, self.mu, self.sigma) / pairs
+        self.pe_trace.append(pe)
+        self.iter += 1
+        return pe, self.sigma
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def make_cuda_engine(g: Graph, dim: int, seed: int, *, comm_chunks: int = 4, group=None, device: Optional[int] = None,
+                     **ctx_kw) -> ShardedEngine:
+    """One rank of a sharded engine over the default (NCCL) process group; world 1 without a group."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    device = torch.cuda.current_device() if device is None else device
+    chunks = comm_chunks if world > 1 else 1
+    ops = CudaShardOps(g, dim, seed, rank, world, chunks, device, **ctx_kw)
+    return ShardedEngine(ops, g.n, g.edge_count(), world, rank, chunks, group=group, stream=ops.stream)

@@ -80,8 +80,8 @@ def star_plus_ring(n, hubs=2):
     e = [(i, (i + 1) % n) for i in range(n)]
     for h in range(hubs):
         for v in range(n):
-            if v != h and abs(v - h) not in (1, n - 1):
-                e.append((h, v))
+            if v != h and abs(v - h) not in (1, n - 1) and (v + h) % 3 != 0:
+                e.append((h, v))  # two thirds of all vertices: high degree, yet non-edges remain
     seen = {}
     for a, b in e:
         seen.setdefault((min(a, b), max(a, b)), None)
