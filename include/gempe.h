@@ -64,6 +64,9 @@ typedef struct gempe_options {
   int32_t comm_chunks;    /* all-gather pipeline depth (>= 1; forced to 1 when world == 1) */
   uint32_t chunk_entries; /* hub split: max adjacency entries per work item (0 = default) */
   int32_t deterministic;  /* 1 = sort incoming-sample buckets so the fp32 sums are run-to-run identical */
+  int32_t precise_distance; /* 1 = pair_distance exactly as src/engine.cpp:45-52 (double differences); 0 = fp32
+                             differences with double cross-lane sum and exact-tally recheck (default) */
+  int32_t kernel_variant; /* 0 = batched gather kernel (default), 1 = row-at-a-time kernel (A/B runs) */
 } gempe_options;
 
 /* Fills *opt with defaults (dim must still be set). */

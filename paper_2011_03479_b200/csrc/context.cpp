@@ -243,7 +243,7 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.neg_mode = c->opt.neg_mode;
   g.math = c->math;
   g.tab = c->tables;
-  c->launches += launch_gather(g, item_lo, item_hi, c->stream);
+  c->launches += launch_gather(g, item_lo, item_hi, c->opt.kernel_variant, c->opt.precise_distance != 0, c->stream);
   cuda_check(cudaGetLastError(), "gather launch");
 }
 

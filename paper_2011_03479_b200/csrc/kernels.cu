@@ -586,6 +586,332 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
   }
 }
 
+
+// ---------------------------------------------------------------------------------- gather, batched (v1)
+//
+// Same work decomposition as gather_kernel, but the per-pair scalar math (sqrt, parabola_impl) is no longer
+// evaluated redundantly by all LPR lanes of a row.  A warp walks its item's lists in batches of
+// E = (32/LPR) * TB entries: every lane group keeps TB rows in registers, the TB per-row partial squared
+// distances are reduced with a transposed (recursive-halving) shuffle pattern that leaves entry t of the
+// group in lane t*REP (REP = LPR/TB lanes hold the same total), each lane evaluates the parabola of ITS entry,
+// and (wf, sf) are shuffled back for the fp32 accumulation from the still-resident row registers.
+// The three lists of an item (adjacency / own samples / incoming samples) are walked as one virtual list.
+//
+// PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation).
+// PRECISE = false: differences and the per-lane partial sum in fp32 (relative error <= ~2e-7 on delta), the
+//                  cross-lane sum in double; a tallied pair whose histogram position lands within the error
+//                  bound of a bin edge is recomputed in double, so the 2x512 tallies stay exact.
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE>
+__global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
+                                                                  std::uint32_t item_hi) {
+  constexpr int G = 32 / LPR;
+  constexpr int E = G * TB;
+  constexpr int REP = LPR / TB;
+  static_assert(TB <= LPR && (TB & (TB - 1)) == 0, "TB must be a power of two <= LPR");
+  constexpr std::uint32_t kNone = 0xffffffffu;
+  __shared__ unsigned int sh_hist[2 * kBins];
+  __shared__ SmemTables sh_tab;
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
+  for (int i = threadIdx.x; i < 65; i += kThreads) {
+    sh_tab.erf[i] = a.tab.erf[i];
+    sh_tab.ratio[i] = a.tab.ratio[i];
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPR, r = lane % LPR;
+  const std::uint32_t item = item_lo + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+
+  if (item < item_hi) {
+    const uint4 it = __ldg(a.items + item);
+    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
+    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
+    const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
+    const bool first = begin == row_lo;
+    const std::uint32_t ld = a.ld;
+
+    // virtual list = [adjacency slice | own samples | incoming samples]
+    const std::uint32_t* pA = a.nbr + begin;
+    const std::uint32_t lenA = end - begin;
+    const std::uint32_t* pB = a.neg_own;
+    std::uint32_t lenB = 0;
+    if (a.neg_mode == 0) {
+      pB = a.neg_own + begin;
+      lenB = lenA;
+    } else if (first) {
+      pB = a.neg_own + static_cast<std::size_t>(u) * a.k;
+      lenB = a.k;
+    }
+    const std::uint32_t* pC = a.in_anchor;
+    std::uint32_t lenC = 0;
+    if (first) {
+      const std::uint32_t in_lo = __ldg(a.in_off + u);
+      pC = a.in_anchor + in_lo;
+      lenC = __ldg(a.in_off + u + 1) - in_lo;
+    }
+    const std::uint32_t endB = lenA + lenB, total = endB + lenC;
+
+    bool act[NV];
+    float xu[NV][VEC];
+    float y[NV][VEC];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      act[j] = static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
+      if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
+    }
+    float zacc = 0.0f;
+
+    for (std::uint32_t base = 0; base < total; base += E * U) {
+      // 1. one list entry per lane and sub-batch: id and kind (0 edge, 1 sample tallied here, 2 incoming sample)
+      std::uint32_t my_id[U];
+      int my_kind[U];
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+        const std::uint32_t e = base + s * E + lane;
+        my_id[s] = kNone;
+        my_kind[s] = 0;
+        if (lane < E && e < total) {
+          if (e < lenA) {
+            my_id[s] = __ldg(pA + e);
+          } else if (e < endB) {
+            my_id[s] = __ldg(pB + (e - lenA));
+            my_kind[s] = 1;
+          } else {
+            my_id[s] = __ldg(pC + (e - endB));
+            my_kind[s] = 2;
+          }
+        }
+      }
+      // 2. TB rows per lane group and sub-batch, all loads issued before any use
+      float xv[U][TB][NV][VEC];
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          const std::uint32_t oid = __shfl_sync(kFull, my_id[s], grp * TB + t);
+          const std::uint32_t src_row = oid != kNone ? oid : u;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) xv[s][t][j][c] = 0.0f;
+            if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[s][t][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+        // 3. per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
+        double p[TB];
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          if constexpr (PRECISE) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) {
+                const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
+                acc = fma(diff, diff, acc);
+              }
+            p[t] = acc;
+          } else {
+            float acc = 0.0f;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) {
+                const float diff = xu[j][c] - xv[s][t][j][c];
+                acc = fmaf(diff, diff, acc);
+              }
+            p[t] = static_cast<double>(acc);
+          }
+        }
+        {
+          int width = TB;
+#pragma unroll
+          for (int off = LPR / 2; off >= 1; off >>= 1) {
+            if (width > 1) {
+              const int half = width / 2;
+              const bool upper = (r & off) != 0;
+#pragma unroll
+              for (int i = 0; i < TB / 2; ++i) {
+                if (i < half) {
+                  const double mine = upper ? p[i + half] : p[i];
+                  const double theirs = upper ? p[i] : p[i + half];
+                  p[i] = mine + shfl_xor_f64(theirs, off);
+                }
+              }
+              width = half;
+            } else {
+              p[0] += shfl_xor_f64(p[0], off);
+            }
+          }
+        }
+        // this lane now owns entry (grp, r / REP) of the sub-batch
+        const int own_lane = grp * TB + r / REP;
+        const std::uint32_t own_id = __shfl_sync(kFull, my_id[s], own_lane);
+        const int own_kind = __shfl_sync(kFull, my_kind[s], own_lane);
+        const bool valid = own_id != kNone;
+        const bool is_edge = own_kind == 0;
+        const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < own_id));
+        double d2 = p[0];
+        double delta = sqrt(d2);
+        constexpr double kBinScale = 512.0 / 12.0;
+        if constexpr (!PRECISE) {
+          // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
+          const double pos = delta * kBinScale;
+          const double frac = pos - floor(pos);
+          const double tol = 4e-6 * pos + 1e-9;
+          const bool amb = tally && pos < 513.0 && (frac < tol || frac > 1.0 - tol);
+          unsigned amb_rows = 0;  // bit t: some group needs row t redone
+          {
+            const unsigned ballot = __ballot_sync(kFull, amb);
+            unsigned m = ballot;
+            while (m) {
+              const int l = __ffs(m) - 1;
+              m &= m - 1;
+              amb_rows |= 1u << ((l % LPR) / REP);
+            }
+          }
+          if (amb_rows) {
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+              if (amb_rows & (1u << t)) {
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+#pragma unroll
+                  for (int c = 0; c < VEC; ++c) {
+                    const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
+                    acc = fma(diff, diff, acc);
+                  }
+#pragma unroll
+                for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
+                if (amb && r / REP == t) {
+                  d2 = acc;
+                  delta = sqrt(acc);
+                }
+              }
+            }
+          }
+        }
+        if (tally) {
+          // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
+          int b = static_cast<int>(delta / 12.0 * 512.0);
+          b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
+          atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
+        }
+        float wf = 0.0f, sf = 0.0f;
+        if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+        if (r % REP == 0) zacc += wf;
+        // 5. add_pair, own side, from the resident rows
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
+          const float st = __shfl_sync(kFull, sf, grp * LPR + t * REP);
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+              const float other = xv[s][t][j][c];
+              y[j][c] = fmaf(wt, fmaf(st, xu[j][c] - other, other), y[j][c]);
+            }
+        }
+      }
+    }
+
+    // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
+    double ys[NV][VEC];
+    double zs = static_cast<double>(zacc);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        double t = static_cast<double>(y[j][c]);
+#pragma unroll
+        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
+        ys[j][c] = t;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
+
+    bool finalize = true;
+    if (hub != kNoHub) {
+      const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
+      const std::uint32_t slot = p0 + it.w;
+      if (grp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (!act[j]) continue;
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
+        }
+        if (r == 0) a.part_z[slot] = zs;
+      }
+      __threadfence();
+      __syncwarp();
+      std::uint32_t arrived = 0;
+      if (lane == 0) arrived = atomicAdd(a.hub_arrived + hub, 1u);
+      arrived = __shfl_sync(kFull, arrived, 0);
+      finalize = arrived == q - 1;
+      if (finalize) {  // last slice of the hub: consolidate the partials in slot order
+        __threadfence();
+        zs = 0.0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
+        for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
+          zs += __ldcg(a.part_z + sl);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            if (!act[j]) continue;
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + (r + LPR * j) * VEC + c);
+          }
+        }
+        if (lane == 0) a.hub_arrived[hub] = 0;
+      }
+    }
+
+    if (finalize && grp == 0) {
+      // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (!act[j]) continue;
+        float out[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          out[c] = xu[j][c];
+          if (zs > 0.0) {
+            out[c] = static_cast<float>(ys[j][c] / zs);
+            bad |= !isfinite(out[c]);
+          }
+        }
+        const std::uint32_t col = (r + LPR * j) * VEC;
+        store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+        if (a.cap_y) {
+#pragma unroll
+          for (int c = 0; c < VEC; ++c)
+            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
+        }
+      }
+      if (a.cap_z && r == 0) a.cap_z[u] = zs;
+      if (bad) atomicOr(a.status + kStatNonFinite, 1u);
+    }
+  }
+
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
+    const unsigned int c = sh_hist[i];
+    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
+  }
+}
+
 inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
   return static_cast<unsigned>((work + per_block - 1) / per_block);
 }
@@ -657,22 +983,44 @@ template <int LPR, int NV, int VEC, int U>
 void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
 }
+template <int LPR, int NV, int VEC, int TB, int U>
+void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
+  const unsigned blocks = blocks_for(hi - lo, kThreads / 32);
+  if (precise) gather_batched_kernel<LPR, NV, VEC, TB, U, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+  else gather_batched_kernel<LPR, NV, VEC, TB, U, false><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+}
 }  // namespace
 
-int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
+int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int variant, bool precise,
+                  cudaStream_t stream) {
   if (hi <= lo) return 0;
   const std::uint32_t ld = a.ld;
-  if (ld == 1) gather_go<1, 1, 1, 4>(a, lo, hi, stream);
-  else if (ld == 2) gather_go<1, 1, 2, 4>(a, lo, hi, stream);
-  else if (ld <= 4) gather_go<1, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 8) gather_go<2, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 16) gather_go<4, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 32) gather_go<8, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 64) gather_go<16, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 128) gather_go<32, 1, 4, 4>(a, lo, hi, stream);
-  else if (ld <= 256) gather_go<32, 2, 4, 2>(a, lo, hi, stream);
-  else if (ld <= 512) gather_go<32, 4, 4, 1>(a, lo, hi, stream);
-  else gather_go<32, 8, 4, 1>(a, lo, hi, stream);  // ld <= 1024 (checked at create)
+  if (variant == 1) {  // v0: one row per lane group at a time, kept for A/B runs
+    if (ld == 1) gather_go<1, 1, 1, 4>(a, lo, hi, stream);
+    else if (ld == 2) gather_go<1, 1, 2, 4>(a, lo, hi, stream);
+    else if (ld <= 4) gather_go<1, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 8) gather_go<2, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 16) gather_go<4, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 32) gather_go<8, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 64) gather_go<16, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 128) gather_go<32, 1, 4, 4>(a, lo, hi, stream);
+    else if (ld <= 256) gather_go<32, 2, 4, 2>(a, lo, hi, stream);
+    else if (ld <= 512) gather_go<32, 4, 4, 1>(a, lo, hi, stream);
+    else gather_go<32, 8, 4, 1>(a, lo, hi, stream);  // ld <= 1024 (checked at create)
+    return 1;
+  }
+  //                          LPR NV VEC TB U
+  if (ld == 1) gather_batched_go<1, 1, 1, 1, 8>(a, lo, hi, precise, stream);
+  else if (ld == 2) gather_batched_go<1, 1, 2, 1, 8>(a, lo, hi, precise, stream);
+  else if (ld <= 4) gather_batched_go<1, 1, 4, 1, 8>(a, lo, hi, precise, stream);
+  else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 4>(a, lo, hi, precise, stream);
+  else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
+  else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
+  else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1>(a, lo, hi, precise, stream);
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 8, 1>(a, lo, hi, precise, stream);
+  else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
+  else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
+  else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);
   return 1;
 }
 

@@ -102,7 +102,9 @@ int launch_sort_buckets(const std::uint32_t* in_off, std::uint32_t* in_anchor, s
 // reorders neg_own (CSR order) into reference slot order 2e+draw (test hook)
 int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t* eid_role, std::uint64_t slots,
                               std::uint32_t* out, cudaStream_t stream);
-int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, cudaStream_t stream);
+// variant 0: batched kernel (default), 1: v0 row-at-a-time kernel.  precise: reference-exact double pair_distance.
+int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, int variant, bool precise,
+                  cudaStream_t stream);
 int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,
                        std::uint64_t seed, double stddev, cudaStream_t stream);
 

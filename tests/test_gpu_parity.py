@@ -175,9 +175,15 @@ def test_golden_embed_runs(G):
 
 # ------------------------------------------------------------------------------------- per-round parity
 
+KERNELS = {"batched": dict(), "batched_precise": dict(precise_distance=True), "rowwise": dict(kernel_variant=1)}
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
 @pytest.mark.parametrize("dim", [1, 2, 3, 4, 5, 8, 16, 24, 32, 64, 100, 128, 192, 256, 300, 512, 1024])
-def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim):
-    check_round(G, oracle, golden_fastmath, er_graph(300, 1500, 17 + dim), dim, seed=dim + 2)
+def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim, kernel):
+    check_round(G, oracle, golden_fastmath, er_graph(300, 1500, 17 + dim), dim, seed=dim + 2, **KERNELS[kernel])
+    check_round(G, oracle, golden_fastmath, er_graph(300, 1500, 17 + dim), dim, seed=dim + 2, neg_mode=1, k=3,
+                **KERNELS[kernel])
 
 
 @pytest.mark.parametrize("exact", [False, True])
@@ -196,10 +202,14 @@ def test_hub_vertices_split_across_work_items(G, oracle, golden_fastmath, dim, c
                 k=7)
 
 
-def test_sigma_extremes_and_clamped_pairs(G, oracle, golden_fastmath):
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_sigma_extremes_and_clamped_pairs(G, oracle, golden_fastmath, kernel):
     for sigma0 in (1e-3, 0.05, 16.0):
-        check_round(G, oracle, golden_fastmath, clique_pair(10), 2, seed=3, sigma0=sigma0, iters=1)
-        check_round(G, oracle, golden_fastmath, clique_pair(10), 128, seed=3, sigma0=sigma0, iters=1, exact=True)
+        check_round(G, oracle, golden_fastmath, clique_pair(10), 2, seed=3, sigma0=sigma0, iters=1, **KERNELS[kernel])
+        check_round(G, oracle, golden_fastmath, clique_pair(10), 128, seed=3, sigma0=sigma0, iters=1, exact=True,
+                    **KERNELS[kernel])
+        check_round(G, oracle, golden_fastmath, er_graph(500, 3000, 5), 64, seed=3, sigma0=sigma0, iters=1,
+                    **KERNELS[kernel])
 
 
 def test_untouched_vertices_hold_position(G):

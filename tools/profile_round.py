@@ -1,0 +1,35 @@
+"""Small driver for ncu captures: builds a BASELINE configuration and runs a few rounds of the hot path.
+
+    python tools/profile_round.py [--config c4] [--rounds 3] [--neg-mode per_vertex_k] [--precise] [--variant 0]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2011_03479_b200 as P  # noqa: E402
+from paper_2011_03479_b200 import graphgen  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c4")
+ap.add_argument("--rounds", type=int, default=3)
+ap.add_argument("--neg-mode", default="per_vertex_k")
+ap.add_argument("--precise", action="store_true")
+ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--chunk-entries", type=int, default=0)
+ap.add_argument("--sigma", type=float, default=1.0)
+a = ap.parse_args()
+
+n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config)
+mode = P.NEG_PER_VERTEX_K if a.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
+ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode == P.NEG_PER_VERTEX_K else 0,
+                precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries)
+ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
+sigma = a.sigma
+for it in range(a.rounds):
+    ctx.iterate_async(1.5, sigma, it)
+he, hn = ctx.sync()
+tot, samp, gath = ctx.elapsed_ms()
+print(f"{a.config}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
+      f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
