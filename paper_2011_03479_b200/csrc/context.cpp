@@ -236,6 +236,7 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.part_z = c->part_z.get();
   g.hist = c->hist.get();
   g.status = c->status.get();
+  g.work_cursor = c->work_cursor.get();
   g.cap_y = c->capture ? c->cap_y.get() : nullptr;
   g.cap_z = c->capture ? c->cap_z.get() : nullptr;
   g.chunk_entries = c->chunk_entries;
@@ -355,6 +356,7 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
                              cudaHostAllocDefault), "cudaHostAlloc");
     pack_tables(c->tables);
     c->status.allocate(8, true);
+    c->work_cursor.allocate(1, true);
     c->hist.allocate(2 * kBins, true);
     for (auto& buf : c->x) buf.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
 

@@ -86,7 +86,7 @@ struct gempe_ctx {
   gempe::DeviceBuffer<std::uint32_t> hub_first, hub_items, hub_arrived;
   gempe::DeviceBuffer<double> part_y, part_z;
   gempe::DeviceBuffer<unsigned long long> hist;
-  gempe::DeviceBuffer<std::uint32_t> status;
+  gempe::DeviceBuffer<std::uint32_t> status, work_cursor;
   gempe::DeviceBuffer<double> cap_y, cap_z;
   bool capture = false;
 

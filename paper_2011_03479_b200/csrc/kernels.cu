@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device_fns.cuh"
 
 namespace gempe {
@@ -136,6 +138,7 @@ __global__ void unpermute_kernel(const std::uint32_t* __restrict__ neg_own, cons
 
 // One warp per vertex: rank-sort of the (small, Poisson-sized) incoming bucket, in place via registers for
 // buckets up to 32*kSortRegs entries; larger buckets fall back to an O(len^2) global pass.
+constexpr int kGrab = 4;  // work items claimed per atomic by a persistent warp
 constexpr int kSortRegs = 8;
 __global__ void __launch_bounds__(kThreads) sort_buckets_kernel(const std::uint32_t* __restrict__ in_off,
                                                                 std::uint32_t* __restrict__ in_anchor, std::uint32_t n) {
@@ -620,15 +623,22 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
 
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, r = lane % LPR;
-  const std::uint32_t item = item_lo + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const std::uint32_t ld = a.ld;
 
-  if (item < item_hi) {
+  // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
+  // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
+  for (;;) {
+    std::uint32_t claim = 0;
+    if (lane == 0) claim = atomicAdd(a.work_cursor, static_cast<std::uint32_t>(kGrab));
+    claim = __shfl_sync(kFull, claim, 0);
+    if (claim >= item_hi - item_lo) break;
+    const std::uint32_t claim_end = min(claim + kGrab, item_hi - item_lo);
+  for (std::uint32_t item = item_lo + claim; item < item_lo + claim_end; ++item) {
     const uint4 it = __ldg(a.items + item);
     const std::uint32_t u = it.x, begin = it.y, hub = it.z;
     const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
     const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
     const bool first = begin == row_lo;
-    const std::uint32_t ld = a.ld;
 
     // virtual list = [adjacency slice | own samples | incoming samples]
     const std::uint32_t* pA = a.nbr + begin;
@@ -904,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
       if (bad) atomicOr(a.status + kStatNonFinite, 1u);
     }
   }
+  }
 
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
@@ -983,11 +994,26 @@ template <int LPR, int NV, int VEC, int U>
 void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
 }
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE>
+void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
+  // persistent grid: as many blocks as fit on the device at once (occupancy query cached per instantiation)
+  static int resident_blocks = 0;
+  if (resident_blocks == 0) {
+    int device = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE>, kThreads, 0);
+    resident_blocks = std::max(1, sms * std::max(1, per_sm));
+  }
+  const unsigned needed = blocks_for(blocks_for(hi - lo, kGrab), kThreads / 32);
+  const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
+  cudaMemsetAsync(a.work_cursor, 0, sizeof(std::uint32_t), stream);
+  gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+}
 template <int LPR, int NV, int VEC, int TB, int U>
 void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
-  const unsigned blocks = blocks_for(hi - lo, kThreads / 32);
-  if (precise) gather_batched_kernel<LPR, NV, VEC, TB, U, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
-  else gather_batched_kernel<LPR, NV, VEC, TB, U, false><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+  if (precise) gather_batched_launch<LPR, NV, VEC, TB, U, true>(a, lo, hi, stream);
+  else gather_batched_launch<LPR, NV, VEC, TB, U, false>(a, lo, hi, stream);
 }
 }  // namespace
 

@@ -75,6 +75,7 @@ struct GatherArgs {
   double* part_z;
   unsigned long long* hist;        // [2*kBins]: edge tallies then non-edge tallies
   std::uint32_t* status;
+  std::uint32_t* work_cursor;      // persistent-warp work queue head (reset before every launch)
   double* cap_y;                   // optional capture (n*dim, n), null when off
   double* cap_z;
   std::uint32_t chunk_entries;
