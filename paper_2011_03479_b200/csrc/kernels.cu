@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "device_fns.cuh"
 
@@ -590,28 +591,35 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 }
 
 
-// ---------------------------------------------------------------------------------- gather, batched (v1)
+// ---------------------------------------------------------------------------------- gather, batched
 //
 // Same work decomposition as gather_kernel, but the per-pair scalar math (sqrt, parabola_impl) is no longer
-// evaluated redundantly by all LPR lanes of a row.  A warp walks its item's lists in batches of
-// E = (32/LPR) * TB entries: every lane group keeps TB rows in registers, the TB per-row partial squared
-// distances are reduced with a transposed (recursive-halving) shuffle pattern that leaves entry t of the
-// group in lane t*REP (REP = LPR/TB lanes hold the same total), each lane evaluates the parabola of ITS entry,
-// and (wf, sf) are shuffled back for the fp32 accumulation from the still-resident row registers.
-// The three lists of an item (adjacency / own samples / incoming samples) are walked as one virtual list.
+// evaluated redundantly by all LPR lanes of a row.  A persistent warp claims work items from a global cursor
+// and walks each item's lists in batches of E = (32/LPR) * TB entries: every lane group keeps TB rows in
+// registers, the TB per-row partial squared distances are reduced with a transposed (recursive-halving)
+// shuffle pattern that leaves entry t of the group in lane t*REP (REP = LPR/TB lanes hold the same total),
+// each lane evaluates the parabola of ITS entry, and (wf, sf) are shuffled back for the fp32 accumulation
+// from the still-resident row registers.  The three lists of an item (adjacency / own samples / incoming
+// samples) are walked as one virtual list whose ids are fetched one batch ahead of the rows.
+// Row arithmetic uses the packed fp32x2 FMA of sm_100 (FFMA2).
 //
 // PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation).
-// PRECISE = false: differences and the per-lane partial sum in fp32 (relative error <= ~2e-7 on delta), the
-//                  cross-lane sum in double; a tallied pair whose histogram position lands within the error
-//                  bound of a bin edge is recomputed in double, so the 2x512 tallies stay exact.
-template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE>
+// PRECISE = false: differences, per-lane partial sums and the cross-lane sum in fp32 (relative error of
+//                  delta <= ~3e-7); a tallied pair whose histogram position lands within 4e-6 (relative) of a
+//                  bin edge is recomputed in double, so the 2x512 tallies stay exact.
+// FULL            : ld == LPR*NV*VEC, no column predicates.
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL>
 __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
-                                                                  std::uint32_t item_hi) {
+                                                                     std::uint32_t item_hi) {
   constexpr int G = 32 / LPR;
   constexpr int E = G * TB;
   constexpr int REP = LPR / TB;
   static_assert(TB <= LPR && (TB & (TB - 1)) == 0, "TB must be a power of two <= LPR");
   constexpr std::uint32_t kNone = 0xffffffffu;
+  using red_t = typename std::conditional<PRECISE, double, float>::type;
   __shared__ unsigned int sh_hist[2 * kBins];
   __shared__ SmemTables sh_tab;
   for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
@@ -624,6 +632,9 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, r = lane % LPR;
   const std::uint32_t ld = a.ld;
+  bool act[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) act[j] = FULL || static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
 
   // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
   // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
@@ -633,287 +644,317 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
     claim = __shfl_sync(kFull, claim, 0);
     if (claim >= item_hi - item_lo) break;
     const std::uint32_t claim_end = min(claim + kGrab, item_hi - item_lo);
-  for (std::uint32_t item = item_lo + claim; item < item_lo + claim_end; ++item) {
-    const uint4 it = __ldg(a.items + item);
-    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
-    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
-    const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
-    const bool first = begin == row_lo;
+    for (std::uint32_t item = item_lo + claim; item < item_lo + claim_end; ++item) {
+      const uint4 it = __ldg(a.items + item);
+      const std::uint32_t u = it.x, begin = it.y, hub = it.z;
+      const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
+      const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
+      const bool first = begin == row_lo;
 
-    // virtual list = [adjacency slice | own samples | incoming samples]
-    const std::uint32_t* pA = a.nbr + begin;
-    const std::uint32_t lenA = end - begin;
-    const std::uint32_t* pB = a.neg_own;
-    std::uint32_t lenB = 0;
-    if (a.neg_mode == 0) {
-      pB = a.neg_own + begin;
-      lenB = lenA;
-    } else if (first) {
-      pB = a.neg_own + static_cast<std::size_t>(u) * a.k;
-      lenB = a.k;
-    }
-    const std::uint32_t* pC = a.in_anchor;
-    std::uint32_t lenC = 0;
-    if (first) {
-      const std::uint32_t in_lo = __ldg(a.in_off + u);
-      pC = a.in_anchor + in_lo;
-      lenC = __ldg(a.in_off + u + 1) - in_lo;
-    }
-    const std::uint32_t endB = lenA + lenB, total = endB + lenC;
+      // virtual list = [adjacency slice | own samples | incoming samples]
+      const std::uint32_t* pA = a.nbr + begin;
+      const std::uint32_t lenA = end - begin;
+      const std::uint32_t* pB = a.neg_own;
+      std::uint32_t lenB = 0;
+      if (a.neg_mode == 0) {
+        pB = a.neg_own + begin;
+        lenB = lenA;
+      } else if (first) {
+        pB = a.neg_own + static_cast<std::size_t>(u) * a.k;
+        lenB = a.k;
+      }
+      const std::uint32_t* pC = a.in_anchor;
+      std::uint32_t lenC = 0;
+      if (first) {
+        const std::uint32_t in_lo = __ldg(a.in_off + u);
+        pC = a.in_anchor + in_lo;
+        lenC = __ldg(a.in_off + u + 1) - in_lo;
+      }
+      const std::uint32_t endB = lenA + lenB, total = endB + lenC;
 
-    bool act[NV];
-    float xu[NV][VEC];
-    float y[NV][VEC];
+      // one list entry per lane and sub-batch: id and kind (0 edge, 1 sample tallied here, 2 incoming sample)
+      auto fetch_ids = [&](std::uint32_t base, std::uint32_t (&id)[U], int (&kind)[U]) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      act[j] = static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
-      if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
-    }
-    float zacc = 0.0f;
+        for (int s = 0; s < U; ++s) {
+          const std::uint32_t e = base + s * E + lane;
+          id[s] = kNone;
+          kind[s] = 0;
+          if ((E == 32 || lane < E) && e < total) {
+            if (e < lenA) {
+              id[s] = __ldg(pA + e);
+            } else if (e < endB) {
+              id[s] = __ldg(pB + (e - lenA));
+              kind[s] = 1;
+            } else {
+              id[s] = __ldg(pC + (e - endB));
+              kind[s] = 2;
+            }
+          }
+        }
+      };
 
-    for (std::uint32_t base = 0; base < total; base += E * U) {
-      // 1. one list entry per lane and sub-batch: id and kind (0 edge, 1 sample tallied here, 2 incoming sample)
+      float xu[NV][VEC];
+      float y[NV][VEC];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
+        if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
+      }
+      float zacc = 0.0f;
+
       std::uint32_t my_id[U];
       int my_kind[U];
+      fetch_ids(0, my_id, my_kind);
+
+      for (std::uint32_t base = 0; base < total; base += E * U) {
+        // TB rows per lane group and sub-batch, all loads issued before any use
+        float xv[U][TB][NV][VEC];
 #pragma unroll
-      for (int s = 0; s < U; ++s) {
-        const std::uint32_t e = base + s * E + lane;
-        my_id[s] = kNone;
-        my_kind[s] = 0;
-        if (lane < E && e < total) {
-          if (e < lenA) {
-            my_id[s] = __ldg(pA + e);
-          } else if (e < endB) {
-            my_id[s] = __ldg(pB + (e - lenA));
-            my_kind[s] = 1;
-          } else {
-            my_id[s] = __ldg(pC + (e - endB));
-            my_kind[s] = 2;
-          }
-        }
-      }
-      // 2. TB rows per lane group and sub-batch, all loads issued before any use
-      float xv[U][TB][NV][VEC];
+        for (int s = 0; s < U; ++s) {
 #pragma unroll
-      for (int s = 0; s < U; ++s) {
+          for (int t = 0; t < TB; ++t) {
+            const std::uint32_t oid = __shfl_sync(kFull, my_id[s], grp * TB + t);
+            const std::uint32_t src_row = oid != kNone ? oid : u;
 #pragma unroll
-        for (int t = 0; t < TB; ++t) {
-          const std::uint32_t oid = __shfl_sync(kFull, my_id[s], grp * TB + t);
-          const std::uint32_t src_row = oid != kNone ? oid : u;
+            for (int j = 0; j < NV; ++j) {
+              if constexpr (!FULL) {
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) xv[s][t][j][c] = 0.0f;
-            if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[s][t][j]);
-          }
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < U; ++s) {
-        // 3. per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
-        double p[TB];
-#pragma unroll
-        for (int t = 0; t < TB; ++t) {
-          if constexpr (PRECISE) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < NV; ++j)
-#pragma unroll
-              for (int c = 0; c < VEC; ++c) {
-                const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
-                acc = fma(diff, diff, acc);
+                for (int c = 0; c < VEC; ++c) xv[s][t][j][c] = 0.0f;
               }
-            p[t] = acc;
-          } else {
-            float acc = 0.0f;
+              if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[s][t][j]);
+            }
+          }
+        }
+        // ids of the next batch: their latency hides behind this batch's arithmetic
+        std::uint32_t nxt_id[U];
+        int nxt_kind[U];
+        fetch_ids(base + E * U, nxt_id, nxt_kind);
+
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
+        for (int s = 0; s < U; ++s) {
+          // per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
+          red_t p[TB];
 #pragma unroll
-              for (int c = 0; c < VEC; ++c) {
-                const float diff = xu[j][c] - xv[s][t][j][c];
+          for (int t = 0; t < TB; ++t) {
+            if constexpr (PRECISE) {
+              double acc = 0.0;
+#pragma unroll
+              for (int j = 0; j < NV; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) {
+                  const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
+                  acc = fma(diff, diff, acc);
+                }
+              p[t] = acc;
+            } else if constexpr (VEC % 2 == 0) {
+              float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int j = 0; j < NV; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; c += 2) {
+                  const float2 diff = ffma2(make_float2(xv[s][t][j][c], xv[s][t][j][c + 1]), make_float2(-1.0f, -1.0f),
+                                            make_float2(xu[j][c], xu[j][c + 1]));
+                  acc = ffma2(diff, diff, acc);
+                }
+              p[t] = acc.x + acc.y;
+            } else {
+              float acc = 0.0f;
+#pragma unroll
+              for (int j = 0; j < NV; ++j) {
+                const float diff = xu[j][0] - xv[s][t][j][0];
                 acc = fmaf(diff, diff, acc);
               }
-            p[t] = static_cast<double>(acc);
-          }
-        }
-        {
-          int width = TB;
-#pragma unroll
-          for (int off = LPR / 2; off >= 1; off >>= 1) {
-            if (width > 1) {
-              const int half = width / 2;
-              const bool upper = (r & off) != 0;
-#pragma unroll
-              for (int i = 0; i < TB / 2; ++i) {
-                if (i < half) {
-                  const double mine = upper ? p[i + half] : p[i];
-                  const double theirs = upper ? p[i] : p[i + half];
-                  p[i] = mine + shfl_xor_f64(theirs, off);
-                }
-              }
-              width = half;
-            } else {
-              p[0] += shfl_xor_f64(p[0], off);
+              p[t] = acc;
             }
           }
-        }
-        // this lane now owns entry (grp, r / REP) of the sub-batch
-        const int own_lane = grp * TB + r / REP;
-        const std::uint32_t own_id = __shfl_sync(kFull, my_id[s], own_lane);
-        const int own_kind = __shfl_sync(kFull, my_kind[s], own_lane);
-        const bool valid = own_id != kNone;
-        const bool is_edge = own_kind == 0;
-        const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < own_id));
-        double d2 = p[0];
-        double delta = sqrt(d2);
-        constexpr double kBinScale = 512.0 / 12.0;
-        if constexpr (!PRECISE) {
-          // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
-          const double pos = delta * kBinScale;
-          const double frac = pos - floor(pos);
-          const double tol = 4e-6 * pos + 1e-9;
-          const bool amb = tally && pos < 513.0 && (frac < tol || frac > 1.0 - tol);
-          unsigned amb_rows = 0;  // bit t: some group needs row t redone
           {
-            const unsigned ballot = __ballot_sync(kFull, amb);
-            unsigned m = ballot;
-            while (m) {
-              const int l = __ffs(m) - 1;
-              m &= m - 1;
+            int width = TB;
+#pragma unroll
+            for (int off = LPR / 2; off >= 1; off >>= 1) {
+              if (width > 1) {
+                const int half = width / 2;
+                const bool upper = (r & off) != 0;
+#pragma unroll
+                for (int i = 0; i < TB / 2; ++i) {
+                  if (i < half) {
+                    const red_t mine = upper ? p[i + half] : p[i];
+                    const red_t theirs = upper ? p[i] : p[i + half];
+                    p[i] = mine + __shfl_xor_sync(kFull, theirs, off);
+                  }
+                }
+                width = half;
+              } else {
+                p[0] += __shfl_xor_sync(kFull, p[0], off);
+              }
+            }
+          }
+          // this lane now owns entry (grp, r / REP) of the sub-batch
+          const int own_lane = grp * TB + r / REP;
+          const std::uint32_t own_id = __shfl_sync(kFull, my_id[s], own_lane);
+          const int own_kind = __shfl_sync(kFull, my_kind[s], own_lane);
+          const bool valid = own_id != kNone;
+          const bool is_edge = own_kind == 0;
+          const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < own_id));
+          double delta;
+          if constexpr (PRECISE) {
+            delta = sqrt(p[0]);
+          } else {
+            delta = sqrt(static_cast<double>(p[0]));
+            // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
+            constexpr double kBinScale = 512.0 / 12.0;
+            const double pos = delta * kBinScale;
+            const double frac = pos - floor(pos);
+            const double tol = 4e-6 * pos + 1e-9;
+            const bool amb = tally && pos < 513.0 && (frac < tol || frac > 1.0 - tol);
+            unsigned amb_rows = 0;  // bit t: some group needs row t redone
+            unsigned pending = __ballot_sync(kFull, amb);
+            while (pending) {
+              const int l = __ffs(pending) - 1;
+              pending &= pending - 1;
               amb_rows |= 1u << ((l % LPR) / REP);
             }
-          }
-          if (amb_rows) {
+            if (amb_rows) {
 #pragma unroll
-            for (int t = 0; t < TB; ++t) {
-              if (amb_rows & (1u << t)) {
-                double acc = 0.0;
+              for (int t = 0; t < TB; ++t) {
+                if (amb_rows & (1u << t)) {
+                  double acc = 0.0;
 #pragma unroll
-                for (int j = 0; j < NV; ++j)
+                  for (int j = 0; j < NV; ++j)
 #pragma unroll
-                  for (int c = 0; c < VEC; ++c) {
-                    const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
-                    acc = fma(diff, diff, acc);
-                  }
+                    for (int c = 0; c < VEC; ++c) {
+                      const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
+                      acc = fma(diff, diff, acc);
+                    }
 #pragma unroll
-                for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
-                if (amb && r / REP == t) {
-                  d2 = acc;
-                  delta = sqrt(acc);
+                  for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
+                  if (amb && r / REP == t) delta = sqrt(acc);
                 }
               }
             }
           }
-        }
-        if (tally) {
-          // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
-          int b = static_cast<int>(delta / 12.0 * 512.0);
-          b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
-          atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
-        }
-        float wf = 0.0f, sf = 0.0f;
-        if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
-        if (r % REP == 0) zacc += wf;
-        // 5. add_pair, own side, from the resident rows
+          if (tally) {
+            // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
+            int b = static_cast<int>(delta / 12.0 * 512.0);
+            b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
+            atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
+          }
+          float wf = 0.0f, sf = 0.0f;
+          if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+          if (r % REP == 0) zacc += wf;
+          // add_pair, own side (engine.cpp:66-72), from the resident rows: y += wf * (x_v + sf * (x_u - x_v))
 #pragma unroll
-        for (int t = 0; t < TB; ++t) {
-          const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
-          const float st = __shfl_sync(kFull, sf, grp * LPR + t * REP);
+          for (int t = 0; t < TB; ++t) {
+            const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
+            const float st = __shfl_sync(kFull, sf, grp * LPR + t * REP);
 #pragma unroll
-          for (int j = 0; j < NV; ++j)
+            for (int j = 0; j < NV; ++j) {
+              if constexpr (VEC % 2 == 0) {
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-              const float other = xv[s][t][j][c];
-              y[j][c] = fmaf(wt, fmaf(st, xu[j][c] - other, other), y[j][c]);
+                for (int c = 0; c < VEC; c += 2) {
+                  const float2 other = make_float2(xv[s][t][j][c], xv[s][t][j][c + 1]);
+                  const float2 diff = ffma2(other, make_float2(-1.0f, -1.0f), make_float2(xu[j][c], xu[j][c + 1]));
+                  const float2 tgt = ffma2(make_float2(st, st), diff, other);
+                  const float2 acc = ffma2(make_float2(wt, wt), tgt, make_float2(y[j][c], y[j][c + 1]));
+                  y[j][c] = acc.x;
+                  y[j][c + 1] = acc.y;
+                }
+              } else {
+                const float other = xv[s][t][j][0];
+                y[j][0] = fmaf(wt, fmaf(st, xu[j][0] - other, other), y[j][0]);
+              }
             }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+          my_id[s] = nxt_id[s];
+          my_kind[s] = nxt_kind[s];
         }
       }
-    }
 
-    // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
-    double ys[NV][VEC];
-    double zs = static_cast<double>(zacc);
+      // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
+      double ys[NV][VEC];
+      double zs = static_cast<double>(zacc);
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
+      for (int j = 0; j < NV; ++j) {
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) {
-        double t = static_cast<double>(y[j][c]);
+        for (int c = 0; c < VEC; ++c) {
+          double t = static_cast<double>(y[j][c]);
 #pragma unroll
-        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
-        ys[j][c] = t;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
-
-    bool finalize = true;
-    if (hub != kNoHub) {
-      const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
-      const std::uint32_t slot = p0 + it.w;
-      if (grp == 0) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          if (!act[j]) continue;
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
+          for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
+          ys[j][c] = t;
         }
-        if (r == 0) a.part_z[slot] = zs;
       }
-      __threadfence();
-      __syncwarp();
-      std::uint32_t arrived = 0;
-      if (lane == 0) arrived = atomicAdd(a.hub_arrived + hub, 1u);
-      arrived = __shfl_sync(kFull, arrived, 0);
-      finalize = arrived == q - 1;
-      if (finalize) {  // last slice of the hub: consolidate the partials in slot order
-        __threadfence();
-        zs = 0.0;
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
-        for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
-          zs += __ldcg(a.part_z + sl);
+      for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
+
+      bool finalize = true;
+      if (hub != kNoHub) {
+        const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
+        const std::uint32_t slot = p0 + it.w;
+        if (grp == 0) {
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
             if (!act[j]) continue;
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + (r + LPR * j) * VEC + c);
+            for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
           }
+          if (r == 0) a.part_z[slot] = zs;
         }
-        if (lane == 0) a.hub_arrived[hub] = 0;
+        __threadfence();
+        __syncwarp();
+        std::uint32_t arrived = 0;
+        if (lane == 0) arrived = atomicAdd(a.hub_arrived + hub, 1u);
+        arrived = __shfl_sync(kFull, arrived, 0);
+        finalize = arrived == q - 1;
+        if (finalize) {  // last slice of the hub: consolidate the partials in slot order
+          __threadfence();
+          zs = 0.0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
+          for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
+            zs += __ldcg(a.part_z + sl);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              if (!act[j]) continue;
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + (r + LPR * j) * VEC + c);
+            }
+          }
+          if (lane == 0) a.hub_arrived[hub] = 0;
+        }
       }
-    }
 
-    if (finalize && grp == 0) {
-      // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
-      bool bad = false;
+      if (finalize && grp == 0) {
+        // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
+        bool bad = false;
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        if (!act[j]) continue;
-        float out[VEC];
+        for (int j = 0; j < NV; ++j) {
+          if (!act[j]) continue;
+          float out[VEC];
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          out[c] = xu[j][c];
-          if (zs > 0.0) {
-            out[c] = static_cast<float>(ys[j][c] / zs);
-            bad |= !isfinite(out[c]);
+          for (int c = 0; c < VEC; ++c) {
+            out[c] = xu[j][c];
+            if (zs > 0.0) {
+              out[c] = static_cast<float>(ys[j][c] / zs);
+              bad |= !isfinite(out[c]);
+            }
+          }
+          const std::uint32_t col = (r + LPR * j) * VEC;
+          store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+          if (a.cap_y) {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c)
+              if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
           }
         }
-        const std::uint32_t col = (r + LPR * j) * VEC;
-        store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
-        if (a.cap_y) {
-#pragma unroll
-          for (int c = 0; c < VEC; ++c)
-            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
-        }
+        if (a.cap_z && r == 0) a.cap_z[u] = zs;
+        if (bad) atomicOr(a.status + kStatNonFinite, 1u);
       }
-      if (a.cap_z && r == 0) a.cap_z[u] = zs;
-      if (bad) atomicOr(a.status + kStatNonFinite, 1u);
     }
-  }
   }
 
   __syncthreads();
@@ -994,7 +1035,7 @@ template <int LPR, int NV, int VEC, int U>
 void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
 }
-template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE>
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL>
 void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   // persistent grid: as many blocks as fit on the device at once (occupancy query cached per instantiation)
   static int resident_blocks = 0;
@@ -1002,18 +1043,25 @@ void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t 
     int device = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL>,
+                                                  kThreads, 0);
     resident_blocks = std::max(1, sms * std::max(1, per_sm));
   }
   const unsigned needed = blocks_for(blocks_for(hi - lo, kGrab), kThreads / 32);
   const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
   cudaMemsetAsync(a.work_cursor, 0, sizeof(std::uint32_t), stream);
-  gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+  gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
 }
 template <int LPR, int NV, int VEC, int TB, int U>
 void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
-  if (precise) gather_batched_launch<LPR, NV, VEC, TB, U, true>(a, lo, hi, stream);
-  else gather_batched_launch<LPR, NV, VEC, TB, U, false>(a, lo, hi, stream);
+  const bool full = a.ld == static_cast<std::uint32_t>(LPR * NV * VEC);
+  if (precise) {
+    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, true, true>(a, lo, hi, stream);
+    else gather_batched_launch<LPR, NV, VEC, TB, U, true, false>(a, lo, hi, stream);
+  } else {
+    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, false, true>(a, lo, hi, stream);
+    else gather_batched_launch<LPR, NV, VEC, TB, U, false, false>(a, lo, hi, stream);
+  }
 }
 }  // namespace
 
