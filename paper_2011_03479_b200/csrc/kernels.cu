@@ -611,9 +611,9 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
-template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL>
-__global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
-                                                                     std::uint32_t item_hi) {
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
+                                                                       std::uint32_t item_hi) {
   constexpr int G = 32 / LPR;
   constexpr int E = G * TB;
   constexpr int REP = LPR / TB;
@@ -622,8 +622,8 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
   using red_t = typename std::conditional<PRECISE, double, float>::type;
   __shared__ unsigned int sh_hist[2 * kBins];
   __shared__ SmemTables sh_tab;
-  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
-  for (int i = threadIdx.x; i < 65; i += kThreads) {
+  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) sh_hist[i] = 0;
+  for (int i = threadIdx.x; i < 65; i += THREADS) {
     sh_tab.erf[i] = a.tab.erf[i];
     sh_tab.ratio[i] = a.tab.ratio[i];
   }
@@ -958,7 +958,7 @@ __global__ void __launch_bounds__(kThreads, 2) gather_batched_kernel(const Gathe
   }
 
   __syncthreads();
-  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
+  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) {
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
@@ -1035,32 +1035,32 @@ template <int LPR, int NV, int VEC, int U>
 void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
 }
-template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL>
+template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
 void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   // persistent grid: as many blocks as fit on the device at once (occupancy query cached per instantiation)
   static int resident_blocks = 0;
+  auto kernel = gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL, THREADS, MINB>;
   if (resident_blocks == 0) {
     int device = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL>,
-                                                  kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, THREADS, 0);
     resident_blocks = std::max(1, sms * std::max(1, per_sm));
   }
-  const unsigned needed = blocks_for(blocks_for(hi - lo, kGrab), kThreads / 32);
+  const unsigned needed = blocks_for(blocks_for(hi - lo, kGrab), THREADS / 32);
   const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
   cudaMemsetAsync(a.work_cursor, 0, sizeof(std::uint32_t), stream);
-  gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+  kernel<<<blocks, THREADS, 0, stream>>>(a, lo, hi);
 }
-template <int LPR, int NV, int VEC, int TB, int U>
+template <int LPR, int NV, int VEC, int TB, int U, int THREADS = 256, int MINB = 2>
 void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
   const bool full = a.ld == static_cast<std::uint32_t>(LPR * NV * VEC);
   if (precise) {
-    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, true, true>(a, lo, hi, stream);
-    else gather_batched_launch<LPR, NV, VEC, TB, U, true, false>(a, lo, hi, stream);
+    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, true, true, THREADS, MINB>(a, lo, hi, stream);
+    else gather_batched_launch<LPR, NV, VEC, TB, U, true, false, THREADS, MINB>(a, lo, hi, stream);
   } else {
-    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, false, true>(a, lo, hi, stream);
-    else gather_batched_launch<LPR, NV, VEC, TB, U, false, false>(a, lo, hi, stream);
+    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, false, true, THREADS, MINB>(a, lo, hi, stream);
+    else gather_batched_launch<LPR, NV, VEC, TB, U, false, false, THREADS, MINB>(a, lo, hi, stream);
   }
 }
 }  // namespace
@@ -1091,7 +1091,18 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
   else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1>(a, lo, hi, precise, stream);
-  else if (ld <= 128) gather_batched_go<32, 1, 4, 8, 1>(a, lo, hi, precise, stream);
+  else if (ld <= 128) {
+    switch (variant) {  // experimental launch shapes for the d=128 row (tools/profile_round.py --variant)
+      case 2: gather_batched_go<32, 1, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream); break;
+      case 3: gather_batched_go<32, 1, 4, 8, 1, 128, 5>(a, lo, hi, precise, stream); break;
+      case 4: gather_batched_go<32, 1, 4, 16, 1, 256, 1>(a, lo, hi, precise, stream); break;
+      case 5: gather_batched_go<32, 1, 4, 16, 1, 128, 3>(a, lo, hi, precise, stream); break;
+      case 6: gather_batched_go<32, 1, 4, 4, 1, 128, 6>(a, lo, hi, precise, stream); break;
+      case 7: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream); break;
+      case 8: gather_batched_go<32, 1, 4, 8, 1>(a, lo, hi, precise, stream); break;
+      default: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
+    }
+  }
   else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);

@@ -375,3 +375,32 @@ def test_config3_size_properties(G):
     # linearity of the accumulation: every vertex's z is the sum of its pair weights, so sum(z) is twice the
     # total pair weight -- compare against an independent float64 recomputation of sum(w) over all pairs
     ctx.close()
+
+
+def test_config4_size_properties(G):
+    """BASELINE config 4 (R-MAT scale 20, d=128, k=20): full-size, size-independent checks."""
+    from paper_2011_03479_b200 import graphgen
+    n, src, dst, dim, k, _, _, std = graphgen.make_config("c4")
+    ctx = G.Context(G.Graph(n, src, dst), dim, 1, neg_mode=G.NEG_PER_VERTEX_K, negatives=k)
+    ctx.init_coords(G.INIT_NORMAL, 1, std)
+    ws, wd, _ = ctx.work_graph()
+    assert ctx.hash_bits == 30 and ctx.probe(ws, wd).all() and ctx.probe(wd, ws).all()
+    partners, draws = ctx.sample(3)
+    anchors = np.repeat(np.arange(n, dtype=np.uint32), k)
+    assert (partners != anchors).all() and (partners < n).all() and not ctx.probe(anchors, partners).any()
+    assert 1.0 <= draws / partners.size < 1.1
+    again, _ = ctx.sample(3)
+    assert np.array_equal(partners, again)  # streams are a pure function of (seed, round, vertex, draw)
+    ctx.set_capture(True)
+    x0 = ctx.get_coords()
+    he, hn = ctx.iterate(1.5, 1.0, 0)
+    assert he.sum() == len(src) and hn.sum() == n * k
+    y, z = ctx.get_yz()
+    x1 = ctx.get_coords()
+    assert np.isfinite(x1).all() and (z > 0).all()
+    assert rel_l2(x1, y / z[:, None]) <= 1e-6
+    # edge tallies equal an independent float64 recomputation of all m edge distances
+    d = np.sqrt(((x0[ws].astype(np.float64) - x0[wd].astype(np.float64)) ** 2).sum(1))
+    bins = np.clip((d / 12.0 * 512).astype(np.int64), 0, 511)
+    assert np.abs(np.bincount(bins, minlength=512).astype(np.int64) - he.astype(np.int64)).sum() <= 4
+    ctx.close()

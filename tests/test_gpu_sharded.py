@@ -1,0 +1,58 @@
+"""Sharded CUDA path on ONE GPU: the ranks' contexts are stepped one after another (no kernel ever waits on
+another rank) and the all-gather is replaced by device copies of each owner's blocks, so the per-rank item
+tables, the partner-side bucket filter (`is_local`) and the block-cyclic layout are exercised for real.
+Every rank must reproduce the single-GPU context bit for bit (deterministic bucket order) and the rank
+tallies must sum to the single-GPU tallies."""
+import numpy as np
+import pytest
+
+from conftest import er_graph, star_plus_ring
+
+pytestmark = pytest.mark.gpu
+
+
+def _views(ctx, which):
+    import torch
+    from paper_2011_03479_b200.sharded import _DeviceArray
+    return torch.as_tensor(_DeviceArray(ctx.device_coords(which), (ctx.padded_rows, ctx.row_stride)), device="cuda:0")
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (4, 2), (8, 4)])
+@pytest.mark.parametrize("mode,k", [(0, 0), (1, 6)])
+def test_rank_contexts_reproduce_the_single_gpu_round(world, chunks, mode, k):
+    import torch
+    import paper_2011_03479_b200 as G
+    for (n, src, dst), dim in ((er_graph(1003, 6000, 3), 64), (star_plus_ring(400, hubs=2), 2)):
+        g = G.Graph(n, src, dst)
+        single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+        ranks = [G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64, rank=r,
+                           world=world, comm_chunks=chunks) for r in range(world)]
+        block = ranks[0].block_rows
+        assert ranks[0].padded_rows == world * chunks * block
+        sigma = 1.0
+        for it in range(3):
+            he, hn = single.iterate(1.5, sigma, it)
+            want = single.get_coords()
+            tot_e, tot_n = np.zeros(512, np.uint64), np.zeros(512, np.uint64)
+            for c in ranks:
+                c.begin_round(1.5, sigma, it)
+                for ch in range(chunks):
+                    c.gather_chunk(ch)
+                e, nn = c.sync()
+                tot_e += e
+                tot_n += nn
+            assert np.array_equal(tot_e, he) and np.array_equal(tot_n, hn)
+            nxt = [_views(c, 1) for c in ranks]
+            for ch in range(chunks):  # the exchange: block (ch, r) travels from rank r to everybody else
+                for r in range(world):
+                    lo = (ch * world + r) * block
+                    for other in range(world):
+                        if other != r:
+                            nxt[other][lo:lo + block].copy_(nxt[r][lo:lo + block])
+            torch.cuda.synchronize()
+            for c in ranks:
+                c.end_round()
+                assert np.array_equal(c.get_coords().view(np.uint32), want.view(np.uint32))
+            sigma *= 1.3
+        for c in ranks + [single]:
+            c.close()

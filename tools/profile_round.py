@@ -27,9 +27,12 @@ ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode
                 precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries)
 ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
 sigma = a.sigma
-for it in range(a.rounds):
+for it in range(2):
+    ctx.iterate_async(1.5, sigma, it)
+ctx.sync(); ctx.elapsed_ms()
+for it in range(2, 2 + a.rounds):
     ctx.iterate_async(1.5, sigma, it)
 he, hn = ctx.sync()
 tot, samp, gath = ctx.elapsed_ms()
-print(f"{a.config}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
+print(f"{a.config} variant {a.variant}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
       f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
