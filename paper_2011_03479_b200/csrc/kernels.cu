@@ -361,6 +361,55 @@ __device__ __forceinline__ void pair_terms(double delta, bool is_edge, const Rou
   sf = (delta > 0.0 && num > 0.0) ? static_cast<float>(num / dw) : 0.0f;
 }
 
+// ---- fp32 evaluation of the same formulas (default, non-PRECISE kernels) -------------------------------------
+// delta is only known to ~3e-7 in this mode, so the scalar chain is carried in fp32 as well (relative error
+// ~1e-6 on wf and sf, two orders below the 1e-4 parity bar); tallies stay exact through the double recheck.
+struct SmemTablesF {
+  float erf[65];
+  float ratio[65];
+};
+struct RoundMathF {
+  float mu, inv_sqrt2_sigma, A, B, C;
+};
+
+__device__ __forceinline__ int segment_of_f(const float* __restrict__ knots, float x) {
+  int s = x >= knots[8] ? 8 : 0;
+  s += x >= knots[s + 4] ? 4 : 0;
+  s += x >= knots[s + 2] ? 2 : 0;
+  s += x >= knots[s + 1] ? 1 : 0;
+  return s;
+}
+__device__ __forceinline__ float quad_eval_f(const float* __restrict__ t, float x) {
+  const int s = segment_of_f(t, x);
+  return fmaf(fmaf(t[17 + s], x, t[33 + s]), x, t[49 + s]);
+}
+__device__ __forceinline__ float tail_series_f(float x) {
+  const float r = __fdividef(1.0f, x * x);
+  const float series = fmaf(r, fmaf(r, fmaf(r, fmaf(6.5625f, r, -1.875f), 0.75f), -0.5f), 1.0f);
+  return __fdividef(x * 1.7724538509055160273f, series);
+}
+__device__ __forceinline__ float gauss_erfc_ratio_f(float x, int exact, const SmemTablesF& tab) {
+  if (exact) return x <= 6.0f ? __fdividef(__expf(-x * x), erfcf(x)) : tail_series_f(x);
+  if (x >= -1.0f) return x > 8.0f ? tail_series_f(x) : quad_eval_f(tab.ratio, x);
+  if (x < -6.0f) return 0.0f;
+  return __fdividef(__expf(-x * x), 1.0f + quad_eval_f(tab.erf, -x));
+}
+__device__ __forceinline__ void pair_terms_f(float delta, bool is_edge, const RoundMathF& m, int exact,
+                                             const SmemTablesF& tab, float& wf, float& sf) {
+  const float dm = delta - m.mu;
+  const float g = gauss_erfc_ratio_f(is_edge ? dm * m.inv_sqrt2_sigma : -dm * m.inv_sqrt2_sigma, exact, tab);
+  const float sg = is_edge ? -g : g;
+  const float w = fmaf(m.A * g, g, m.B * dm * sg);
+  wf = 0.0f;
+  sf = 0.0f;
+  if (w > 0.0f) {
+    wf = w;
+    const float dw = delta * w;
+    const float num = fmaf(m.C, sg, dw);
+    if (delta > 0.0f && num > 0.0f) sf = __fdividef(num, dw);
+  }
+}
+
 template <int VEC>
 __device__ __forceinline__ void load_row(const float* __restrict__ p, float (&v)[VEC]) {
   if constexpr (VEC == 4) {
@@ -596,20 +645,28 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 // Same work decomposition as gather_kernel, but the per-pair scalar math (sqrt, parabola_impl) is no longer
 // evaluated redundantly by all LPR lanes of a row.  A persistent warp claims work items from a global cursor
 // and walks each item's lists in batches of E = (32/LPR) * TB entries: every lane group keeps TB rows in
-// registers, the TB per-row partial squared distances are reduced with a transposed (recursive-halving)
-// shuffle pattern that leaves entry t of the group in lane t*REP (REP = LPR/TB lanes hold the same total),
-// each lane evaluates the parabola of ITS entry, and (wf, sf) are shuffled back for the fp32 accumulation
-// from the still-resident row registers.  The three lists of an item (adjacency / own samples / incoming
-// samples) are walked as one virtual list whose ids are fetched one batch ahead of the rows.
-// Row arithmetic uses the packed fp32x2 FMA of sm_100 (FFMA2).
+// registers -- as DIFFERENCES x_u - x_v, the only form both the distance and the update need -- the TB per-row
+// partial squared distances are reduced with a transposed (recursive-halving) shuffle pattern that leaves
+// entry t of the group in lane t*REP (REP = LPR/TB lanes hold the same total), each lane evaluates the parabola
+// of ITS entry, and one coefficient per row is shuffled back for the accumulation
+//     y_u = sum_t wf_t (x_v + sf_t (x_u - x_v)) = (sum_t wf_t) x_u + sum_t wf_t (sf_t - 1) (x_u - x_v),
+// i.e. one packed FFMA2 per two floats and row (add_pair, engine.cpp:66-72, regrouped; exact same real value).
+// The three lists of an item (adjacency / own samples / incoming samples) are walked as one virtual list whose
+// entries (id | kind << 30) are fetched two batches ahead; the rows of the next batch are pulled into L2 with
+// prefetch.global.L2 while the current batch is being computed.
 //
-// PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation).
-// PRECISE = false: differences, per-lane partial sums and the cross-lane sum in fp32 (relative error of
-//                  delta <= ~3e-7); a tallied pair whose histogram position lands within 4e-6 (relative) of a
-//                  bin edge is recomputed in double, so the 2x512 tallies stay exact.
+// PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation), double
+//                  parabola chain.
+// PRECISE = false: differences, per-lane partial sums, the cross-lane sum and the parabola chain in fp32 (relative
+//                  error <= ~3e-7 on delta, ~1e-6 on the weights); a tallied pair whose histogram position lands
+//                  within 4e-6 (relative) of a bin edge is recomputed in double, so the 2x512 tallies stay exact.
 // FULL            : ld == LPR*NV*VEC, no column predicates.
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+constexpr std::uint32_t kEntryNone = 0xffffffffu;   // list entry = id | kind << 30 (ids < 2^30, checked at create)
+constexpr std::uint32_t kEntryIdMask = 0x3fffffffu;
 
 template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
@@ -618,15 +675,20 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   constexpr int E = G * TB;
   constexpr int REP = LPR / TB;
   static_assert(TB <= LPR && (TB & (TB - 1)) == 0, "TB must be a power of two <= LPR");
-  constexpr std::uint32_t kNone = 0xffffffffu;
+  constexpr int ROW_BYTES_MAX = LPR * NV * VEC * 4;
+  constexpr int LINES = ROW_BYTES_MAX >= 128 ? ROW_BYTES_MAX / 128 : 1;  // 128-byte lines per row
+  constexpr bool kPrefetch = ROW_BYTES_MAX >= 128 && U == 1 && (E * LINES) % 32 == 0;
   using red_t = typename std::conditional<PRECISE, double, float>::type;
   __shared__ unsigned int sh_hist[2 * kBins];
-  __shared__ SmemTables sh_tab;
+  using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
+  __shared__ tab_t sh_tab;
   for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) sh_hist[i] = 0;
   for (int i = threadIdx.x; i < 65; i += THREADS) {
-    sh_tab.erf[i] = a.tab.erf[i];
-    sh_tab.ratio[i] = a.tab.ratio[i];
+    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
+    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
   }
+  const RoundMathF mf{static_cast<float>(a.math.mu), static_cast<float>(a.math.inv_sqrt2_sigma),
+                      static_cast<float>(a.math.A), static_cast<float>(a.math.B), static_cast<float>(a.math.C)};
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -635,6 +697,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   bool act[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) act[j] = FULL || static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
+  const float* x_lane = a.x_cur + r * VEC;  // this lane's column block of every row
 
   // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
   // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
@@ -648,64 +711,53 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       const uint4 it = __ldg(a.items + item);
       const std::uint32_t u = it.x, begin = it.y, hub = it.z;
       const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
-      const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
       const bool first = begin == row_lo;
 
-      // virtual list = [adjacency slice | own samples | incoming samples]
-      const std::uint32_t* pA = a.nbr + begin;
-      const std::uint32_t lenA = end - begin;
-      const std::uint32_t* pB = a.neg_own;
-      std::uint32_t lenB = 0;
-      if (a.neg_mode == 0) {
-        pB = a.neg_own + begin;
-        lenB = lenA;
-      } else if (first) {
-        pB = a.neg_own + static_cast<std::size_t>(u) * a.k;
-        lenB = a.k;
+      // virtual list = [adjacency slice | own samples | incoming samples], as offsets into nbr / neg_own / in_anchor
+      const std::uint32_t lenA = min(begin + a.chunk_entries, row_hi) - begin;
+      std::uint32_t offB = begin, lenB = lenA;
+      if (a.neg_mode != 0) {
+        offB = u * a.k;
+        lenB = first ? a.k : 0u;
       }
-      const std::uint32_t* pC = a.in_anchor;
-      std::uint32_t lenC = 0;
+      std::uint32_t offC = 0, lenC = 0;
       if (first) {
-        const std::uint32_t in_lo = __ldg(a.in_off + u);
-        pC = a.in_anchor + in_lo;
-        lenC = __ldg(a.in_off + u + 1) - in_lo;
+        offC = __ldg(a.in_off + u);
+        lenC = __ldg(a.in_off + u + 1) - offC;
       }
       const std::uint32_t endB = lenA + lenB, total = endB + lenC;
 
-      // one list entry per lane and sub-batch: id and kind (0 edge, 1 sample tallied here, 2 incoming sample)
-      auto fetch_ids = [&](std::uint32_t base, std::uint32_t (&id)[U], int (&kind)[U]) {
+      // one list entry per lane and sub-batch: id | kind << 30 (kind 0 edge, 1 sample tallied here, 2 incoming sample)
+      auto fetch = [&](std::uint32_t base, std::uint32_t (&ent)[U]) {
 #pragma unroll
         for (int s = 0; s < U; ++s) {
           const std::uint32_t e = base + s * E + lane;
-          id[s] = kNone;
-          kind[s] = 0;
+          ent[s] = kEntryNone;
           if ((E == 32 || lane < E) && e < total) {
             if (e < lenA) {
-              id[s] = __ldg(pA + e);
+              ent[s] = __ldg(a.nbr + begin + e);
             } else if (e < endB) {
-              id[s] = __ldg(pB + (e - lenA));
-              kind[s] = 1;
+              ent[s] = __ldg(a.neg_own + offB + (e - lenA)) | (1u << 30);
             } else {
-              id[s] = __ldg(pC + (e - endB));
-              kind[s] = 2;
+              ent[s] = __ldg(a.in_anchor + offC + (e - endB)) | (2u << 30);
             }
           }
         }
       };
 
       float xu[NV][VEC];
-      float y[NV][VEC];
+      float y[NV][VEC];  // sum_t wf_t (sf_t - 1) (x_u - x_v)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
 #pragma unroll
         for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
-        if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
+        if (act[j]) load_row<VEC>(x_lane + static_cast<std::size_t>(u) * ld + LPR * j * VEC, xu[j]);
       }
       float zacc = 0.0f;
 
-      std::uint32_t my_id[U];
-      int my_kind[U];
-      fetch_ids(0, my_id, my_kind);
+      std::uint32_t cur[U], nxt[U];
+      fetch(0, cur);
+      fetch(E * U, nxt);
 
       for (std::uint32_t base = 0; base < total; base += E * U) {
         // TB rows per lane group and sub-batch, all loads issued before any use
@@ -714,26 +766,36 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         for (int s = 0; s < U; ++s) {
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const std::uint32_t oid = __shfl_sync(kFull, my_id[s], grp * TB + t);
-            const std::uint32_t src_row = oid != kNone ? oid : u;
+            const std::uint32_t ent = __shfl_sync(kFull, cur[s], grp * TB + t);
+            const std::uint32_t src_row = ent != kEntryNone ? (ent & kEntryIdMask) : u;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (!FULL) {
 #pragma unroll
                 for (int c = 0; c < VEC; ++c) xv[s][t][j][c] = 0.0f;
               }
-              if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[s][t][j]);
+              if (act[j]) load_row<VEC>(x_lane + static_cast<std::size_t>(src_row) * ld + LPR * j * VEC, xv[s][t][j]);
             }
           }
         }
-        // ids of the next batch: their latency hides behind this batch's arithmetic
-        std::uint32_t nxt_id[U];
-        int nxt_kind[U];
-        fetch_ids(base + E * U, nxt_id, nxt_kind);
+        // rows of the next batch -> L2 (their entries arrived during the previous batch), entries of the batch
+        // after that -> registers
+        if constexpr (kPrefetch) {
+#pragma unroll
+          for (int i = 0; i < E * LINES / 32; ++i) {
+            const int slot = i * 32 + lane;
+            const std::uint32_t ent = __shfl_sync(kFull, nxt[0], slot / LINES);
+            if (ent != kEntryNone) {
+              prefetch_l2(a.x_cur + static_cast<std::size_t>(ent & kEntryIdMask) * ld + (slot % LINES) * 32);
+            }
+          }
+        }
+        std::uint32_t nn[U];
+        fetch(base + 2 * E * U, nn);
 
 #pragma unroll
         for (int s = 0; s < U; ++s) {
-          // per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
+          // rows become differences x_u - x_v; per-row partial squared distance; transposed reduction
           red_t p[TB];
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
@@ -745,6 +807,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
                 for (int c = 0; c < VEC; ++c) {
                   const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
                   acc = fma(diff, diff, acc);
+                  xv[s][t][j][c] = xu[j][c] - xv[s][t][j][c];
                 }
               p[t] = acc;
             } else if constexpr (VEC % 2 == 0) {
@@ -756,6 +819,8 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
                   const float2 diff = ffma2(make_float2(xv[s][t][j][c], xv[s][t][j][c + 1]), make_float2(-1.0f, -1.0f),
                                             make_float2(xu[j][c], xu[j][c + 1]));
                   acc = ffma2(diff, diff, acc);
+                  xv[s][t][j][c] = diff.x;
+                  xv[s][t][j][c + 1] = diff.y;
                 }
               p[t] = acc.x + acc.y;
             } else {
@@ -764,6 +829,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
               for (int j = 0; j < NV; ++j) {
                 const float diff = xu[j][0] - xv[s][t][j][0];
                 acc = fmaf(diff, diff, acc);
+                xv[s][t][j][0] = diff;
               }
               p[t] = acc;
             }
@@ -790,92 +856,95 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             }
           }
           // this lane now owns entry (grp, r / REP) of the sub-batch
-          const int own_lane = grp * TB + r / REP;
-          const std::uint32_t own_id = __shfl_sync(kFull, my_id[s], own_lane);
-          const int own_kind = __shfl_sync(kFull, my_kind[s], own_lane);
-          const bool valid = own_id != kNone;
+          const std::uint32_t own = __shfl_sync(kFull, cur[s], grp * TB + r / REP);
+          const bool valid = own != kEntryNone;
+          const std::uint32_t own_kind = own >> 30;
           const bool is_edge = own_kind == 0;
-          const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < own_id));
-          double delta;
+          const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < (own & kEntryIdMask)));
+          float wf = 0.0f, sf = 0.0f;
+          int bin;
           if constexpr (PRECISE) {
-            delta = sqrt(p[0]);
+            const double delta = sqrt(p[0]);
+            bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
+            if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
           } else {
-            delta = sqrt(static_cast<double>(p[0]));
+            float delta = sqrtf(p[0]);
             // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
-            constexpr double kBinScale = 512.0 / 12.0;
-            const double pos = delta * kBinScale;
-            const double frac = pos - floor(pos);
-            const double tol = 4e-6 * pos + 1e-9;
-            const bool amb = tally && pos < 513.0 && (frac < tol || frac > 1.0 - tol);
-            unsigned amb_rows = 0;  // bit t: some group needs row t redone
+            const float pos = delta * (512.0f / 12.0f);
+            const float frac = pos - floorf(pos);
+            const float tol = 4e-6f * pos + 1e-9f;
+            const bool amb = tally && pos < 513.0f && (frac < tol || frac > 1.0f - tol);
+            bin = static_cast<int>(pos);
             unsigned pending = __ballot_sync(kFull, amb);
-            while (pending) {
+            while (pending) {  // rare: one exact pair_distance per ambiguous pair, rows re-read (they are L1/L2 hot)
               const int l = __ffs(pending) - 1;
               pending &= pending - 1;
-              amb_rows |= 1u << ((l % LPR) / REP);
-            }
-            if (amb_rows) {
+              const std::uint32_t other = __shfl_sync(kFull, own, l) & kEntryIdMask;
+              double acc = 0.0;
+              if (lane < LPR) {
 #pragma unroll
-              for (int t = 0; t < TB; ++t) {
-                if (amb_rows & (1u << t)) {
-                  double acc = 0.0;
-#pragma unroll
-                  for (int j = 0; j < NV; ++j)
+                for (int j = 0; j < NV; ++j) {
+                  if (static_cast<std::uint32_t>((lane + LPR * j) * VEC) < ld) {
+                    float xo[VEC], xs[VEC];
+                    load_row<VEC>(a.x_cur + static_cast<std::size_t>(other) * ld + (lane + LPR * j) * VEC, xo);
+                    load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (lane + LPR * j) * VEC, xs);
 #pragma unroll
                     for (int c = 0; c < VEC; ++c) {
-                      const double diff = static_cast<double>(xu[j][c]) - static_cast<double>(xv[s][t][j][c]);
+                      const double diff = static_cast<double>(xs[c]) - static_cast<double>(xo[c]);
                       acc = fma(diff, diff, acc);
                     }
-#pragma unroll
-                  for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
-                  if (amb && r / REP == t) delta = sqrt(acc);
+                  }
                 }
               }
+#pragma unroll
+              for (int off = 16; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
+              if (lane == l) {
+                const double exact = sqrt(acc);
+                bin = static_cast<int>(exact / 12.0 * 512.0);
+                delta = static_cast<float>(exact);
+              }
             }
+            if (valid) pair_terms_f(delta, is_edge, mf, a.math.exact, sh_tab, wf, sf);
           }
-          if (tally) {
-            // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
-            int b = static_cast<int>(delta / 12.0 * 512.0);
-            b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
-            atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
+          if (tally) {  // tallied before the w > 0 test (engine.cpp:221-222)
+            bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
+            atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + bin], 1u);
           }
-          float wf = 0.0f, sf = 0.0f;
-          if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
           if (r % REP == 0) zacc += wf;
-          // add_pair, own side (engine.cpp:66-72), from the resident rows: y += wf * (x_v + sf * (x_u - x_v))
+          const float coef = wf * (sf - 1.0f);
+          // y += wf (sf - 1) (x_u - x_v) from the resident differences
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
-            const float st = __shfl_sync(kFull, sf, grp * LPR + t * REP);
+            const float ct = __shfl_sync(kFull, coef, grp * LPR + t * REP);
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (VEC % 2 == 0) {
 #pragma unroll
                 for (int c = 0; c < VEC; c += 2) {
-                  const float2 other = make_float2(xv[s][t][j][c], xv[s][t][j][c + 1]);
-                  const float2 diff = ffma2(other, make_float2(-1.0f, -1.0f), make_float2(xu[j][c], xu[j][c + 1]));
-                  const float2 tgt = ffma2(make_float2(st, st), diff, other);
-                  const float2 acc = ffma2(make_float2(wt, wt), tgt, make_float2(y[j][c], y[j][c + 1]));
+                  const float2 acc = ffma2(make_float2(ct, ct), make_float2(xv[s][t][j][c], xv[s][t][j][c + 1]),
+                                           make_float2(y[j][c], y[j][c + 1]));
                   y[j][c] = acc.x;
                   y[j][c + 1] = acc.y;
                 }
               } else {
-                const float other = xv[s][t][j][0];
-                y[j][0] = fmaf(wt, fmaf(st, xu[j][0] - other, other), y[j][0]);
+                y[j][0] = fmaf(ct, xv[s][t][j][0], y[j][0]);
               }
             }
           }
         }
 #pragma unroll
         for (int s = 0; s < U; ++s) {
-          my_id[s] = nxt_id[s];
-          my_kind[s] = nxt_kind[s];
+          cur[s] = nxt[s];
+          nxt[s] = nn[s];
         }
       }
 
-      // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
+      // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107);
+      // y_u = z_u x_u + sum of the weighted differences
       double ys[NV][VEC];
       double zs = static_cast<double>(zacc);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
 #pragma unroll
@@ -883,11 +952,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           double t = static_cast<double>(y[j][c]);
 #pragma unroll
           for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
-          ys[j][c] = t;
+          ys[j][c] = fma(zs, static_cast<double>(xu[j][c]), t);
         }
       }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
 
       bool finalize = true;
       if (hub != kNoHub) {
@@ -955,6 +1022,400 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         if (bad) atomicOr(a.status + kStatNonFinite, 1u);
       }
     }
+  }
+
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) {
+    const unsigned int c = sh_hist[i];
+    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
+  }
+}
+
+// ---------------------------------------------------------------------------------- gather, cp.async pipeline
+//
+// The batched gather with the row loads decoupled from the arithmetic, for 16 < ld <= 128 (rows of 128..512
+// bytes: the HBM-bound shapes).  Every warp software-pipelines its own stream of 16-row batches ACROSS work
+// items: while batch b is being computed from registers, the rows of batch b+1 are in flight as 16-byte
+// `cp.async.cg` (LDGSTS) copies into the warp's shared-memory stage and the list ids of batch b+2 are being
+// fetched.  Lane (grp, r) copies exactly the 16-byte chunk it will later read, so a stage is lane-private
+// storage: completion is a per-thread `cp.async.wait_group`, no barrier, no bank conflicts.  The vertex's own
+// row rides in an extra slot of the item's first batch; item descriptors are fetched eight items per claim.
+// (A warp-specialised variant with a TMA `cp.async.bulk` producer warp was measured first: correct, but the
+// uniform-register bulk copies serialise per lane and one producer per block could not feed 3-7 consumers --
+// 18.7 ms vs 7.4 ms on c4.)
+
+namespace pipe {
+
+constexpr int kE = 16;      // rows per batch / stage
+constexpr int kClaim = 8;   // work items per claim (descriptors live in lanes 0..7)
+constexpr unsigned kHead = 1u, kLast = 2u;
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(std::uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Cursor over the warp's stream of batches.  Descriptor fields are per lane (lane i describes claimed item
+// i); count/cur/pos are warp-uniform; nid/nkind hold, per lane, entry `lane` of the batch at the cursor.
+struct Feed {
+  std::uint32_t u, begin, hub, sub, lenA, lenB, in_lo, lenC;
+  std::uint32_t count, cur, pos;
+  std::uint32_t nid, nkind;
+};
+
+__device__ __forceinline__ void feed_claim(Feed& f, const GatherArgs& a, std::uint32_t item_lo, std::uint32_t n_items,
+                                           int lane) {
+  std::uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(a.work_cursor, static_cast<std::uint32_t>(kClaim));
+  base = __shfl_sync(kFull, base, 0);
+  f.cur = 0;
+  f.pos = 0;
+  if (base >= n_items) {
+    f.count = 0;
+    return;
+  }
+  f.count = min(static_cast<std::uint32_t>(kClaim), n_items - base);
+  f.u = f.begin = f.sub = f.lenA = f.lenB = f.in_lo = f.lenC = 0;
+  f.hub = kNoHub;
+  if (lane < static_cast<int>(f.count)) {
+    const uint4 it = __ldg(a.items + item_lo + base + lane);
+    f.u = it.x;
+    f.begin = it.y;
+    f.hub = it.z;
+    f.sub = it.w;
+    const std::uint32_t row_lo = __ldg(a.rowptr + it.x), row_hi = __ldg(a.rowptr + it.x + 1);
+    f.lenA = min(it.y + a.chunk_entries, row_hi) - it.y;
+    const bool first = it.y == row_lo;
+    f.lenB = a.neg_mode == 0 ? f.lenA : (first ? a.k : 0u);
+    if (first) {
+      f.in_lo = __ldg(a.in_off + it.x);
+      f.lenC = __ldg(a.in_off + it.x + 1) - f.in_lo;
+    }
+  }
+}
+
+// ids of the batch at the cursor, one entry per lane
+__device__ __forceinline__ void feed_prefetch(Feed& f, const GatherArgs& a, int lane) {
+  const std::uint32_t u = __shfl_sync(kFull, f.u, f.cur), begin = __shfl_sync(kFull, f.begin, f.cur);
+  const std::uint32_t lenA = __shfl_sync(kFull, f.lenA, f.cur), lenB = __shfl_sync(kFull, f.lenB, f.cur);
+  const std::uint32_t in_lo = __shfl_sync(kFull, f.in_lo, f.cur), lenC = __shfl_sync(kFull, f.lenC, f.cur);
+  const std::uint32_t e = f.pos + lane, endB = lenA + lenB, total = endB + lenC;
+  f.nid = 0xffffffffu;
+  f.nkind = 0;
+  if (lane < kE && e < total) {
+    if (e < lenA) {
+      f.nid = __ldg(a.nbr + begin + e);
+    } else if (e < endB) {
+      f.nid = a.neg_mode == 0 ? __ldg(a.neg_own + begin + (e - lenA))
+                              : __ldg(a.neg_own + static_cast<std::size_t>(u) * a.k + (e - lenA));
+      f.nkind = 1;
+    } else {
+      f.nid = __ldg(a.in_anchor + in_lo + (e - endB));
+      f.nkind = 2;
+    }
+  }
+}
+
+// what the arithmetic needs to know about a batch whose rows are in (or on their way to) a stage
+struct BatchMeta {
+  std::uint32_t u, nvalid, flags, hub, sub;  // warp-uniform
+  std::uint32_t own_id;                      // per lane: id / kind of the entry this lane will own after the reduction
+  int own_kind;
+};
+
+}  // namespace pipe
+
+template <int LPR, int TB, bool PRECISE, bool FULL, int WARPS, int MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const GatherArgs a, std::uint32_t item_lo,
+                                                                        std::uint32_t item_hi) {
+  using namespace pipe;
+  constexpr int THREADS = 32 * WARPS;
+  constexpr int G = 32 / LPR;
+  constexpr int REP = LPR / TB;
+  constexpr int PITCH = LPR * 16;              // bytes between row slots of a stage
+  constexpr int STAGE = (kE + G) * PITCH;      // 16 rows + one own-row slot per lane group
+  static_assert(G * TB == kE, "a stage holds exactly one batch");
+  constexpr std::uint32_t kNone = 0xffffffffu;
+  using red_t = typename std::conditional<PRECISE, double, float>::type;
+
+  extern __shared__ __align__(128) unsigned char stage_mem[];  // [WARPS][2][STAGE]
+  __shared__ unsigned int sh_hist[2 * kBins];
+  using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
+  __shared__ tab_t sh_tab;
+  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) sh_hist[i] = 0;
+  for (int i = threadIdx.x; i < 65; i += THREADS) {
+    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
+    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
+  }
+  const RoundMathF mf{static_cast<float>(a.math.mu), static_cast<float>(a.math.inv_sqrt2_sigma),
+                      static_cast<float>(a.math.A), static_cast<float>(a.math.B), static_cast<float>(a.math.C)};
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / LPR, r = lane % LPR;
+  const std::uint32_t ld = a.ld;
+  const std::uint32_t n_items = item_hi - item_lo;
+  const bool act = FULL || static_cast<std::uint32_t>(r * 4) < ld;
+  // this lane's private 16-byte column of both stages
+  const std::uint32_t lane_base = smem_u32(stage_mem) + static_cast<std::uint32_t>(warp) * 2u * STAGE + r * 16;
+  const unsigned char* lane_ptr = stage_mem + static_cast<std::size_t>(warp) * 2 * STAGE + r * 16;
+  const float* x_lane = a.x_cur + r * 4;
+
+  Feed f;
+  feed_claim(f, a, item_lo, n_items, lane);
+  if (f.count) feed_prefetch(f, a, lane);
+
+  // Issues the copies of the batch at the cursor into stage `slot`, records its metadata, advances the cursor
+  // and starts the id fetch of the batch after it.  Returns false when the queue is exhausted.
+  auto post = [&](int slot, BatchMeta& m) -> bool {
+    if (f.count == 0) return false;
+    const std::uint32_t total = __shfl_sync(kFull, f.lenA + f.lenB + f.lenC, f.cur);
+    m.u = __shfl_sync(kFull, f.u, f.cur);
+    m.hub = __shfl_sync(kFull, f.hub, f.cur);
+    m.sub = __shfl_sync(kFull, f.sub, f.cur);
+    m.nvalid = min(static_cast<std::uint32_t>(kE), total - f.pos);
+    const bool head = f.pos == 0, last = f.pos + kE >= total;
+    m.flags = (head ? kHead : 0u) | (last ? kLast : 0u);
+    m.own_id = __shfl_sync(kFull, f.nid, grp * TB + r / REP);
+    m.own_kind = static_cast<int>(__shfl_sync(kFull, f.nkind, grp * TB + r / REP));
+    const std::uint32_t dst = lane_base + static_cast<std::uint32_t>(slot) * STAGE;
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const std::uint32_t id = __shfl_sync(kFull, f.nid, grp * TB + t);
+      if (act && id != kNone) cp_async16(dst + (grp * TB + t) * PITCH, x_lane + static_cast<std::size_t>(id) * ld);
+    }
+    if (head && act) cp_async16(dst + (kE + grp) * PITCH, x_lane + static_cast<std::size_t>(m.u) * ld);
+    cp_async_commit();
+    if (last) {
+      ++f.cur;
+      f.pos = 0;
+      if (f.cur == f.count) feed_claim(f, a, item_lo, n_items, lane);
+    } else {
+      f.pos += kE;
+    }
+    if (f.count) feed_prefetch(f, a, lane);
+    return true;
+  };
+
+  float xu[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float zacc = 0.0f;
+
+  // The arithmetic of one batch (identical to gather_batched_kernel), rows read from stage `slot`.
+  auto compute = [&](int slot, const BatchMeta& m) {
+    const unsigned char* st = lane_ptr + static_cast<std::size_t>(slot) * STAGE;
+    if (m.flags & kHead) {
+      const float4 t = act ? *reinterpret_cast<const float4*>(st + (kE + grp) * PITCH) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      xu[0] = t.x; xu[1] = t.y; xu[2] = t.z; xu[3] = t.w;
+      y[0] = y[1] = y[2] = y[3] = 0.0f;
+      zacc = 0.0f;
+    }
+    float xv[TB][4];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const bool have = act && static_cast<std::uint32_t>(grp * TB + t) < m.nvalid;
+      const float4 q = have ? *reinterpret_cast<const float4*>(st + (grp * TB + t) * PITCH) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      xv[t][0] = q.x; xv[t][1] = q.y; xv[t][2] = q.z; xv[t][3] = q.w;
+    }
+    const std::uint32_t u = m.u;
+    // per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
+    red_t p[TB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      if constexpr (PRECISE) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double diff = static_cast<double>(xu[c]) - static_cast<double>(xv[t][c]);
+          acc = fma(diff, diff, acc);
+        }
+        p[t] = acc;
+      } else {
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int c = 0; c < 4; c += 2) {
+          const float2 diff = ffma2(make_float2(xv[t][c], xv[t][c + 1]), make_float2(-1.0f, -1.0f),
+                                    make_float2(xu[c], xu[c + 1]));
+          acc = ffma2(diff, diff, acc);
+        }
+        p[t] = acc.x + acc.y;
+      }
+    }
+    {
+      int width = TB;
+#pragma unroll
+      for (int off = LPR / 2; off >= 1; off >>= 1) {
+        if (width > 1) {
+          const int half = width / 2;
+          const bool upper = (r & off) != 0;
+#pragma unroll
+          for (int i = 0; i < TB / 2; ++i) {
+            if (i < half) {
+              const red_t mine = upper ? p[i + half] : p[i];
+              const red_t theirs = upper ? p[i] : p[i + half];
+              p[i] = mine + __shfl_xor_sync(kFull, theirs, off);
+            }
+          }
+          width = half;
+        } else {
+          p[0] += __shfl_xor_sync(kFull, p[0], off);
+        }
+      }
+    }
+    const bool valid = m.own_id != kNone;
+    const bool is_edge = m.own_kind == 0;
+    const bool tally = valid && (r % REP == 0) && (m.own_kind == 1 || (m.own_kind == 0 && u < m.own_id));
+    float wf = 0.0f, sf = 0.0f;
+    int bin;
+    if constexpr (PRECISE) {
+      const double delta = sqrt(p[0]);
+      bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
+      if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+    } else {
+      float delta = sqrtf(p[0]);
+      // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
+      const float pos = delta * (512.0f / 12.0f);
+      const float frac = pos - floorf(pos);
+      const float tol = 4e-6f * pos + 1e-9f;
+      const bool amb = tally && pos < 513.0f && (frac < tol || frac > 1.0f - tol);
+      bin = static_cast<int>(pos);
+      unsigned amb_rows = 0;
+      unsigned pending = __ballot_sync(kFull, amb);
+      while (pending) {
+        const int l = __ffs(pending) - 1;
+        pending &= pending - 1;
+        amb_rows |= 1u << ((l % LPR) / REP);
+      }
+      if (amb_rows) {
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          if (amb_rows & (1u << t)) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double diff = static_cast<double>(xu[c]) - static_cast<double>(xv[t][c]);
+              acc = fma(diff, diff, acc);
+            }
+#pragma unroll
+            for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
+            if (amb && r / REP == t) {
+              const double exact = sqrt(acc);
+              bin = static_cast<int>(exact / 12.0 * 512.0);
+              delta = static_cast<float>(exact);
+            }
+          }
+        }
+      }
+      if (valid) pair_terms_f(delta, is_edge, mf, a.math.exact, sh_tab, wf, sf);
+    }
+    if (tally) {  // tallied before the w > 0 test (engine.cpp:221-222)
+      bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
+      atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + bin], 1u);
+    }
+    if (r % REP == 0) zacc += wf;
+    // add_pair, own side (engine.cpp:66-72): y += wf * (x_v + sf * (x_u - x_v))
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
+      const float st2 = __shfl_sync(kFull, sf, grp * LPR + t * REP);
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        const float2 other = make_float2(xv[t][c], xv[t][c + 1]);
+        const float2 diff = ffma2(other, make_float2(-1.0f, -1.0f), make_float2(xu[c], xu[c + 1]));
+        const float2 tgt = ffma2(make_float2(st2, st2), diff, other);
+        const float2 acc = ffma2(make_float2(wt, wt), tgt, make_float2(y[c], y[c + 1]));
+        y[c] = acc.x;
+        y[c + 1] = acc.y;
+      }
+    }
+
+    if (m.flags & kLast) {
+      // item complete: cross-group reduction in double, hub consolidation, y / z update (engine.cpp:253-276)
+      double ys[4];
+      double zs = static_cast<double>(zacc);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double t = static_cast<double>(y[c]);
+#pragma unroll
+        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
+        ys[c] = t;
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
+      bool finalize = true;
+      if (m.hub != kNoHub) {
+        const std::uint32_t p0 = __ldg(a.hub_first + m.hub), q = __ldg(a.hub_items + m.hub);
+        const std::uint32_t hslot = p0 + m.sub;
+        if (grp == 0) {
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a.part_y[static_cast<std::size_t>(hslot) * ld + r * 4 + c] = ys[c];
+          }
+          if (r == 0) a.part_z[hslot] = zs;
+        }
+        __threadfence();
+        __syncwarp();
+        std::uint32_t arrived = 0;
+        if (lane == 0) arrived = atomicAdd(a.hub_arrived + m.hub, 1u);
+        arrived = __shfl_sync(kFull, arrived, 0);
+        finalize = arrived == q - 1;
+        if (finalize) {  // last slice of the hub: consolidate the partials in slot order
+          __threadfence();
+          zs = 0.0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ys[c] = 0.0;
+          for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
+            zs += __ldcg(a.part_z + sl);
+            if (act) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) ys[c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + r * 4 + c);
+            }
+          }
+          if (lane == 0) a.hub_arrived[m.hub] = 0;
+        }
+      }
+      if (finalize && grp == 0 && act) {
+        bool bad = false;
+        float out[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          out[c] = xu[c];
+          if (zs > 0.0) {
+            out[c] = static_cast<float>(ys[c] / zs);
+            bad |= !isfinite(out[c]);
+          }
+        }
+        const std::uint32_t col = r * 4;
+        store_row<4>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+        if (a.cap_y) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[c];
+        }
+        if (a.cap_z && r == 0) a.cap_z[u] = zs;
+        if (bad) atomicOr(a.status + kStatNonFinite, 1u);
+      }
+    }
+  };
+
+  // two-stage software pipeline, unrolled by two so that the stage index is a compile-time constant
+  BatchMeta m0, m1;
+  bool have0 = post(0, m0), have1 = false;
+  while (have0) {
+    have1 = post(1, m1);
+    if (have1) cp_async_wait<1>(); else cp_async_wait<0>();
+    compute(0, m0);
+    if (!have1) break;
+    have0 = post(0, m0);
+    if (have0) cp_async_wait<1>(); else cp_async_wait<0>();
+    compute(1, m1);
   }
 
   __syncthreads();
@@ -1063,6 +1524,36 @@ void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, 
     else gather_batched_launch<LPR, NV, VEC, TB, U, false, false, THREADS, MINB>(a, lo, hi, stream);
   }
 }
+template <int LPR, int TB, bool PRECISE, bool FULL, int WARPS, int MINB>
+void gather_async_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
+  constexpr int THREADS = 32 * WARPS;
+  constexpr int kSmem = WARPS * 2 * (pipe::kE + 32 / LPR) * LPR * 16;
+  auto kernel = gather_async_kernel<LPR, TB, PRECISE, FULL, WARPS, MINB>;
+  static int resident_blocks = 0;
+  if (resident_blocks == 0) {
+    int device = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, THREADS, kSmem);
+    resident_blocks = std::max(1, sms * std::max(1, per_sm));
+  }
+  const unsigned needed = blocks_for(blocks_for(hi - lo, pipe::kClaim), WARPS);
+  const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
+  cudaMemsetAsync(a.work_cursor, 0, sizeof(std::uint32_t), stream);
+  kernel<<<blocks, THREADS, kSmem, stream>>>(a, lo, hi);
+}
+template <int LPR, int TB, int WARPS = 4, int MINB = 3>
+void gather_async_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
+  const bool full = a.ld == static_cast<std::uint32_t>(LPR * 4);
+  if (precise) {
+    if (full) gather_async_launch<LPR, TB, true, true, WARPS, MINB>(a, lo, hi, stream);
+    else gather_async_launch<LPR, TB, true, false, WARPS, MINB>(a, lo, hi, stream);
+  } else {
+    if (full) gather_async_launch<LPR, TB, false, true, WARPS, MINB>(a, lo, hi, stream);
+    else gather_async_launch<LPR, TB, false, false, WARPS, MINB>(a, lo, hi, stream);
+  }
+}
 }  // namespace
 
 int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int variant, bool precise,
@@ -1083,6 +1574,16 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
     else gather_go<32, 8, 4, 1>(a, lo, hi, stream);  // ld <= 1024 (checked at create)
     return 1;
   }
+  if (variant >= 10 && ld > 16 && ld <= 128) {  // cp.async pipeline (experimental: register pressure caps it at 8 warps/SM)
+    if (ld <= 32) gather_async_go<8, 4>(a, lo, hi, precise, stream);
+    else if (ld <= 64) gather_async_go<16, 8>(a, lo, hi, precise, stream);
+    else if (variant == 10) gather_async_go<32, 16, 4, 2>(a, lo, hi, precise, stream);
+    else if (variant == 11) gather_async_go<32, 16, 5, 2>(a, lo, hi, precise, stream);
+    else if (variant == 12) gather_async_go<32, 16, 6, 2>(a, lo, hi, precise, stream);
+    else if (variant == 13) gather_async_go<32, 16, 2, 6>(a, lo, hi, precise, stream);
+    else gather_async_go<32, 16, 4, 3>(a, lo, hi, precise, stream);
+    return 1;
+  }
   //                          LPR NV VEC TB U
   if (ld == 1) gather_batched_go<1, 1, 1, 1, 8>(a, lo, hi, precise, stream);
   else if (ld == 2) gather_batched_go<1, 1, 2, 1, 8>(a, lo, hi, precise, stream);
@@ -1100,6 +1601,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
       case 6: gather_batched_go<32, 1, 4, 4, 1, 128, 6>(a, lo, hi, precise, stream); break;
       case 7: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream); break;
       case 8: gather_batched_go<32, 1, 4, 8, 1>(a, lo, hi, precise, stream); break;
+      case 9:  // register-resident batched kernel (the pre-pipeline default)
       default: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
     }
   }
