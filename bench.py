@@ -132,7 +132,7 @@ def main():
         base = cpu_reference_arm(n, src, dst, dim, max(args.cpu_seconds, 30.0), steps=args.steps, warmup=args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 coordinates, f64 distance/parabola",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": {"workload": workload_name(args.config), "n": n, "m": int(len(src))},
                 "cpu_baseline": base,
                 "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -200,7 +200,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 coordinates, f64 distance/parabola", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "n": n, "m": int(len(src)), "dim": dim,
                        "negatives": "k=%d per vertex" % k if neg_mode == P.NEG_PER_VERTEX_K else "2 per edge",
                        "pair_terms_per_iteration": int(pair_terms), "sigma": sigma,

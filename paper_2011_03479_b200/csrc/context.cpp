@@ -286,7 +286,6 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw config_error("bad rank/world");
   if (o.comm_chunks < 1) throw config_error("comm_chunks must be >= 1");
   if (m > 0 && (!src || !dst)) throw data_error("null edge arrays");
-  if (n > (1u << 30)) throw config_error("vertex count above 2^30 is not supported by the packed list entries");
   if (2 * m >= 0xffffffffull) throw config_error("edge count exceeds the 32-bit adjacency index");
   const std::uint64_t slots = o.neg_mode == GEMPE_NEG_PER_EDGE_2 ? 2 * m : static_cast<std::uint64_t>(n) * o.negatives;
   if (slots >= 0xffffffffull) throw config_error("sample count exceeds the 32-bit bucket index");

@@ -61,7 +61,7 @@ __global__ void probe_kernel(const std::uint32_t* __restrict__ words, std::uint3
 // LCG "advance, then use" loop of sample_non_edges.  Lanes of a warp retry together until every lane has
 // its partner, so the table probes of one warp stay batched; the accepted partner is counted into its
 // partner's incoming bucket (arrival rank kept for the scatter pass).
-__global__ void __launch_bounds__(kThreads) sample_kernel(const SampleArgs a) {
+__global__ void __launch_bounds__(kThreads, 8) sample_kernel(const SampleArgs a) {
   const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   std::uint32_t draws = 0;
   if (t < a.slots) {
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 //     y_u = sum_t wf_t (x_v + sf_t (x_u - x_v)) = (sum_t wf_t) x_u + sum_t wf_t (sf_t - 1) (x_u - x_v),
 // i.e. one packed FFMA2 per two floats and row (add_pair, engine.cpp:66-72, regrouped; exact same real value).
 // The three lists of an item (adjacency / own samples / incoming samples) are walked as one virtual list whose
-// entries (id | kind << 30) are fetched two batches ahead; the rows of the next batch are pulled into L2 with
+// ids are fetched two batches ahead; the rows of the next batch are pulled into L2 with
 // prefetch.global.L2 while the current batch is being computed.
 //
 // PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation), double
@@ -665,8 +665,6 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-constexpr std::uint32_t kEntryNone = 0xffffffffu;   // list entry = id | kind << 30 (ids < 2^30, checked at create)
-constexpr std::uint32_t kEntryIdMask = 0x3fffffffu;
 
 template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const GatherArgs a, std::uint32_t item_lo,
@@ -727,20 +725,16 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       }
       const std::uint32_t endB = lenA + lenB, total = endB + lenC;
 
-      // one list entry per lane and sub-batch: id | kind << 30 (kind 0 edge, 1 sample tallied here, 2 incoming sample)
+      // one list entry (vertex id) per lane and sub-batch.  Validity and kind (0 edge, 1 sample tallied here, 2
+      // incoming sample) follow from the entry's position alone, so nothing has to wait on these loads until the
+      // ids are needed as addresses two batches later.
       auto fetch = [&](std::uint32_t base, std::uint32_t (&ent)[U]) {
 #pragma unroll
         for (int s = 0; s < U; ++s) {
           const std::uint32_t e = base + s * E + lane;
-          ent[s] = kEntryNone;
+          ent[s] = u;
           if ((E == 32 || lane < E) && e < total) {
-            if (e < lenA) {
-              ent[s] = __ldg(a.nbr + begin + e);
-            } else if (e < endB) {
-              ent[s] = __ldg(a.neg_own + offB + (e - lenA)) | (1u << 30);
-            } else {
-              ent[s] = __ldg(a.in_anchor + offC + (e - endB)) | (2u << 30);
-            }
+            ent[s] = __ldg(e < lenA ? a.nbr + begin + e : (e < endB ? a.neg_own + offB + (e - lenA) : a.in_anchor + offC + (e - endB)));
           }
         }
       };
@@ -766,8 +760,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         for (int s = 0; s < U; ++s) {
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const std::uint32_t ent = __shfl_sync(kFull, cur[s], grp * TB + t);
-            const std::uint32_t src_row = ent != kEntryNone ? (ent & kEntryIdMask) : u;
+            const std::uint32_t src_row = __shfl_sync(kFull, cur[s], grp * TB + t);  // own row u past the list end
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (!FULL) {
@@ -784,9 +777,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
 #pragma unroll
           for (int i = 0; i < E * LINES / 32; ++i) {
             const int slot = i * 32 + lane;
-            const std::uint32_t ent = __shfl_sync(kFull, nxt[0], slot / LINES);
-            if (ent != kEntryNone) {
-              prefetch_l2(a.x_cur + static_cast<std::size_t>(ent & kEntryIdMask) * ld + (slot % LINES) * 32);
+            const std::uint32_t row = __shfl_sync(kFull, nxt[0], slot / LINES);
+            if (base + E + slot / LINES < total) {
+              prefetch_l2(a.x_cur + static_cast<std::size_t>(row) * ld + (slot % LINES) * 32);
             }
           }
         }
@@ -857,10 +850,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           }
           // this lane now owns entry (grp, r / REP) of the sub-batch
           const std::uint32_t own = __shfl_sync(kFull, cur[s], grp * TB + r / REP);
-          const bool valid = own != kEntryNone;
-          const std::uint32_t own_kind = own >> 30;
-          const bool is_edge = own_kind == 0;
-          const bool tally = valid && (r % REP == 0) && (own_kind == 1 || (own_kind == 0 && u < (own & kEntryIdMask)));
+          const std::uint32_t own_e = base + s * E + grp * TB + r / REP;
+          const bool valid = own_e < total;
+          const bool is_edge = own_e < lenA;
+          const bool tally = valid && (r % REP == 0) && (is_edge ? u < own : own_e < endB);
           float wf = 0.0f, sf = 0.0f;
           int bin;
           if constexpr (PRECISE) {
@@ -879,7 +872,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             while (pending) {  // rare: one exact pair_distance per ambiguous pair, rows re-read (they are L1/L2 hot)
               const int l = __ffs(pending) - 1;
               pending &= pending - 1;
-              const std::uint32_t other = __shfl_sync(kFull, own, l) & kEntryIdMask;
+              const std::uint32_t other = __shfl_sync(kFull, own, l);
               double acc = 0.0;
               if (lane < LPR) {
 #pragma unroll
