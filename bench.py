@@ -37,6 +37,7 @@ def parse():
     p.add_argument("--neg-mode", default="per_vertex_k", choices=["per_vertex_k", "per_edge_2"])
     p.add_argument("--comm-chunks", type=int, default=4)
     p.add_argument("--chunk-entries", type=int, default=0)
+    p.add_argument("--bucket-mode", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline budget on rank 0")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -125,10 +126,19 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
     from paper_2011_03479_b200 import graphgen
+
+    def gen_device():
+        """torch CUDA device for the R-MAT generator when a GPU is present (same graph as the numpy path)."""
+        try:
+            import torch
+            return torch.device("cuda", local_rank) if torch.cuda.is_available() else None
+        except Exception:
+            return None
+
     if args.impl == "reference":
         if rank != 0:
             return
-        n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config)
+        n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config, device=gen_device())
         base = cpu_reference_arm(n, src, dst, dim, max(args.cpu_seconds, 30.0), steps=args.steps, warmup=args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
@@ -148,12 +158,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    n, src, dst, dim, k, _, init, std = graphgen.make_config(args.config)
+    n, src, dst, dim, k, _, init, std = graphgen.make_config(args.config, device=gen_device())
+    torch.cuda.empty_cache()
     g = P.Graph(n, src, dst)
     neg_mode = P.NEG_PER_VERTEX_K if args.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
     eng = sharded.make_cuda_engine(g, dim, 1, comm_chunks=args.comm_chunks, device=local_rank, neg_mode=neg_mode,
                                    negatives=k if neg_mode == P.NEG_PER_VERTEX_K else 0,
-                                   chunk_entries=args.chunk_entries)
+                                   chunk_entries=args.chunk_entries, bucket_mode=args.bucket_mode)
     ctx = eng.ops.ctx
     ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
     stream = eng.ops.stream

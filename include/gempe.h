@@ -67,6 +67,8 @@ typedef struct gempe_options {
   int32_t precise_distance; /* 1 = pair_distance exactly as src/engine.cpp:45-52 (double differences); 0 = fp32
                              differences with double cross-lane sum and exact-tally recheck (default) */
   int32_t kernel_variant; /* 0 = batched gather kernel (default), 1 = row-at-a-time kernel (A/B runs) */
+  int32_t bucket_mode;    /* incoming-sample bucketing: 0 = auto, 1 = per-partner atomics + scan + scatter,
+                             2 = two-level counting sort (streaming traffic only; auto for n >= 2^22) */
 } gempe_options;
 
 /* Fills *opt with defaults (dim must still be set). */

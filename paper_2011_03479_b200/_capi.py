@@ -40,7 +40,7 @@ class Options(C.Structure):
                 ("negatives", C.c_uint32), ("math", C.c_int32), ("rng", C.c_int32), ("relabel", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("comm_chunks", C.c_int32),
                 ("chunk_entries", C.c_uint32), ("deterministic", C.c_int32), ("precise_distance", C.c_int32),
-                ("kernel_variant", C.c_int32)]
+                ("kernel_variant", C.c_int32), ("bucket_mode", C.c_int32)]
 
 
 class IterationConfigC(C.Structure):

@@ -155,9 +155,33 @@ void build_structures(gempe_ctx* c) {
 
   c->slots = per_edge ? 2 * m : static_cast<std::uint64_t>(n) * c->opt.negatives;
   c->neg_own.allocate(c->slots);
-  c->in_rank.allocate(c->slots);
   c->in_anchor.allocate(c->slots);
-  c->in_cnt.allocate(n);
+  // bucketing method: per-partner atomics while the per-vertex counters fit L2 comfortably, else the two-level
+  // counting sort (opt.bucket_mode: 0 auto, 1 atomics, 2 counting sort)
+  c->partition = PartitionArgs{};
+  std::uint32_t shift = 8;
+  while ((static_cast<std::uint64_t>(n) + (1ull << shift) - 1) >> shift > 4096) ++shift;
+  const bool can_partition = shift <= 15 && c->slots > 0;
+  const bool want_partition = c->opt.bucket_mode == 2 || (c->opt.bucket_mode == 0 && n >= (1u << 22));
+  if (can_partition && want_partition) {
+    c->partition.shift = shift;
+    c->partition.buckets = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) + (1ull << shift) - 1) >> shift);
+    c->partition.grid = partition_grid(c->slots);
+    c->block_hist.allocate(static_cast<std::size_t>(c->partition.grid) * c->partition.buckets);
+    c->bucket_off.allocate(c->partition.buckets + 1);
+    c->records.allocate(c->slots);
+    c->partition.block_hist = c->block_hist.get();
+    c->partition.bucket_off = c->bucket_off.get();
+    c->partition.records = c->records.get();
+    c->in_rank.release();
+    c->in_cnt.release();
+  } else {
+    c->block_hist.release();
+    c->bucket_off.release();
+    c->records.release();
+    c->in_rank.allocate(c->slots);
+    c->in_cnt.allocate(n);
+  }
   c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
   c->scan_scratch.allocate((n + 4095) / 4096 + 2);
 
@@ -207,11 +231,15 @@ void require_live(gempe_ctx* c) {
 void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
   cuda_check(cudaMemsetAsync(c->status.get(), 0, 8 * sizeof(std::uint32_t), c->stream), "memset status");
   cuda_check(cudaMemsetAsync(c->hist.get(), 0, 2 * kBins * sizeof(unsigned long long), c->stream), "memset hist");
-  cuda_check(cudaMemsetAsync(c->in_cnt.get(), 0, c->n * sizeof(std::uint32_t), c->stream), "memset in_cnt");
   const SampleArgs a = sample_args(c, iter);
-  c->launches += launch_sample(a, c->stream);
-  c->launches += launch_scan(c->in_cnt.get(), c->in_off.get(), c->n, c->scan_scratch.get(), c->stream);
-  c->launches += launch_scatter(a, c->in_off.get(), c->in_anchor.get(), c->stream);
+  if (c->partition.buckets) {
+    c->launches += launch_sample_partition(a, c->partition, c->in_off.get(), c->in_anchor.get(), c->stream);
+  } else {
+    cuda_check(cudaMemsetAsync(c->in_cnt.get(), 0, c->n * sizeof(std::uint32_t), c->stream), "memset in_cnt");
+    c->launches += launch_sample(a, c->stream);
+    c->launches += launch_scan(c->in_cnt.get(), c->in_off.get(), c->n, c->scan_scratch.get(), c->stream);
+    c->launches += launch_scatter(a, c->in_off.get(), c->in_anchor.get(), c->stream);
+  }
   if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
   cuda_check(cudaGetLastError(), "sampling passes");
 }

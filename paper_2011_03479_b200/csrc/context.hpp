@@ -81,6 +81,10 @@ struct gempe_ctx {
   gempe::DeviceBuffer<std::uint32_t> rowptr, nbr, eid_role, csr_src;
   gempe::DeviceBuffer<std::uint32_t> hash_words;
   gempe::DeviceBuffer<std::uint32_t> neg_own, in_cnt, in_off, in_rank, in_anchor, scan_scratch;
+  // large-n bucketing (two-level counting sort); partition.buckets == 0 selects the atomic method
+  gempe::PartitionArgs partition{};
+  gempe::DeviceBuffer<std::uint32_t> block_hist, bucket_off;
+  gempe::DeviceBuffer<uint2> records;
   gempe::DeviceBuffer<uint4> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
   gempe::DeviceBuffer<std::uint32_t> hub_first, hub_items, hub_arrived;

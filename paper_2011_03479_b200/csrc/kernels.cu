@@ -22,6 +22,7 @@ namespace gempe {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPartThreads = 512;
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ bool is_local(const Ownership& o, std::uint32_t v) {
@@ -57,68 +58,71 @@ __global__ void probe_kernel(const std::uint32_t* __restrict__ words, std::uint3
 
 // ---------------------------------------------------------------------------------- sampler
 
-// One thread per sample stream.  Reference mode replays expand_seed32(seed, iter, unit, draw) followed by the
-// LCG "advance, then use" loop of sample_non_edges.  Lanes of a warp retry together until every lane has
-// its partner, so the table probes of one warp stay batched; the accepted partner is counted into its
-// partner's incoming bucket (arrival rank kept for the scatter pass).
-__global__ void __launch_bounds__(kThreads, 8) sample_kernel(const SampleArgs a) {
-  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  std::uint32_t draws = 0;
-  if (t < a.slots) {
-    std::uint32_t anchor;
-    std::uint64_t unit, draw;
-    if (a.neg_mode == 0) {
-      anchor = __ldg(a.csr_src + t);
-      const std::uint32_t er = __ldg(a.eid_role + t);
-      unit = er >> 1;
-      draw = er & 1u;
-    } else {
-      anchor = static_cast<std::uint32_t>(t / a.k);
-      unit = anchor;
-      draw = t - static_cast<std::uint64_t>(anchor) * a.k;
+// One sample stream: replays expand_seed32(seed, iter, unit, draw) followed by the LCG "advance, then use" loop
+// of sample_non_edges (reference mode), or a Philox4x32-10 stream.  Returns the accepted partner.
+__device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::uint64_t t, std::uint32_t& anchor,
+                                                     std::uint32_t& draws) {
+  std::uint64_t unit, draw;
+  if (a.neg_mode == 0) {
+    anchor = __ldg(a.csr_src + t);
+    const std::uint32_t er = __ldg(a.eid_role + t);
+    unit = er >> 1;
+    draw = er & 1u;
+  } else {
+    anchor = static_cast<std::uint32_t>(t / a.k);
+    unit = anchor;
+    draw = t - static_cast<std::uint64_t>(anchor) * a.k;
+  }
+  if (a.rng == 0) {
+    std::uint32_t s = static_cast<std::uint32_t>(mix(mix(a.stream_base, unit), draw) >> 16);
+    for (int tries = 0; tries < kMaxRetries; ++tries) {
+      s = s * kLcgMul + 1u;
+      ++draws;
+      const std::uint32_t g = uniform_index(s, a.n);
+      if (g == anchor) continue;
+      if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
+      return g;
     }
-    std::uint32_t partner = anchor;
-    bool found = false;
-    if (a.rng == 0) {
-      std::uint32_t s = static_cast<std::uint32_t>(mix(mix(a.stream_base, unit), draw) >> 16);
-      for (int tries = 0; tries < kMaxRetries; ++tries) {
-        s = s * kLcgMul + 1u;
+  } else {
+    const std::uint64_t slot = a.neg_mode == 0 ? ((unit << 1) | draw) : t;
+    for (int tries = 0; tries < kMaxRetries; tries += 4) {
+      std::uint32_t ctr[4] = {static_cast<std::uint32_t>(slot), static_cast<std::uint32_t>(slot >> 32),
+                              static_cast<std::uint32_t>(tries >> 2), static_cast<std::uint32_t>(a.iter)};
+      philox4x32(ctr, static_cast<std::uint32_t>(a.stream_base), static_cast<std::uint32_t>(a.stream_base >> 32));
+      for (int q = 0; q < 4; ++q) {
         ++draws;
-        const std::uint32_t g = uniform_index(s, a.n);
+        const std::uint32_t g = static_cast<std::uint32_t>((static_cast<std::uint64_t>(ctr[q]) * a.n) >> 32);
         if (g == anchor) continue;
         if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
-        partner = g;
-        found = true;
-        break;
-      }
-    } else {
-      const std::uint64_t slot = a.neg_mode == 0 ? ((unit << 1) | draw) : t;
-      for (int tries = 0; tries < kMaxRetries && !found; tries += 4) {
-        std::uint32_t ctr[4] = {static_cast<std::uint32_t>(slot), static_cast<std::uint32_t>(slot >> 32),
-                                static_cast<std::uint32_t>(tries >> 2), static_cast<std::uint32_t>(a.iter)};
-        philox4x32(ctr, static_cast<std::uint32_t>(a.stream_base), static_cast<std::uint32_t>(a.stream_base >> 32));
-        for (int q = 0; q < 4 && !found; ++q) {
-          ++draws;
-          const std::uint32_t g = static_cast<std::uint32_t>((static_cast<std::uint64_t>(ctr[q]) * a.n) >> 32);
-          if (g == anchor) continue;
-          if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
-          partner = g;
-          found = true;
-        }
+        return g;
       }
     }
-    if (!found) {  // near_complete_graph_error (sampler.cpp:18-21); keep memory-safe output
-      atomicOr(a.status + kStatRetryCap, 1u);
-      partner = anchor + 1 < a.n ? anchor + 1 : 0;
-    }
-    a.neg_own[t] = partner;
-    a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
   }
+  // near_complete_graph_error (sampler.cpp:18-21); keep memory-safe output
+  atomicOr(a.status + kStatRetryCap, 1u);
+  return anchor + 1 < a.n ? anchor + 1 : 0;
+}
+
+__device__ __forceinline__ void add_draws(const SampleArgs& a, std::uint32_t draws) {
   // total draw count (test hook / p-bar of the roofline formula)
   for (int off = 16; off > 0; off >>= 1) draws += __shfl_xor_sync(kFull, draws, off);
   if ((threadIdx.x & 31) == 0 && draws) {
     atomicAdd(reinterpret_cast<unsigned long long*>(a.status + kStatDrawsLo), static_cast<unsigned long long>(draws));
   }
+}
+
+// ---- bucketing by partner, method A (small n): one returning atomic per sample on the partner's counter, then
+// scan + scatter.  Every array it touches at random (in_cnt, in_off) fits L2 for n up to a few million.
+__global__ void __launch_bounds__(kThreads, 8) sample_kernel(const SampleArgs a) {
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t draws = 0;
+  if (t < a.slots) {
+    std::uint32_t anchor;
+    const std::uint32_t partner = sample_slot(a, t, anchor, draws);
+    a.neg_own[t] = partner;
+    a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
+  }
+  add_draws(a, draws);
 }
 
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, const std::uint32_t* __restrict__ in_off,
@@ -129,6 +133,150 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, c
   if (rank == kNotLocal) return;
   const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t) : static_cast<std::uint32_t>(t / a.k);
   in_anchor[in_off[a.neg_own[t]] + rank] = anchor;
+}
+
+// ---- bucketing by partner, method B (large n): two-level counting sort with streaming traffic only.
+//   1. sample_count_kernel: persistent blocks sample their slots (grid-stride tiles) and histogram the partners'
+//      COARSE buckets (partner >> shift, <= 8192 buckets) in shared memory; one histogram row per block.
+//   2. bucket_scan kernels: column scan over the blocks (base of every (block, bucket) run) + bucket offsets.
+//   3. partition_kernel: same tiles; (partner, anchor) records go to their run of the coarse bucket, positions from
+//      shared-memory cursors -- no global atomics, writes land in a few hundred open runs.
+//   4. bucket_finalize_kernel: one block per coarse bucket counts its vertices in shared memory, scans, writes
+//      in_off for its vertex range and places the anchors; random writes stay inside the bucket's window (L2).
+__global__ void __launch_bounds__(kPartThreads) sample_count_kernel(const SampleArgs a, const PartitionArgs p) {
+  extern __shared__ std::uint32_t sh_cnt[];
+  for (std::uint32_t b = threadIdx.x; b < p.buckets; b += kPartThreads) sh_cnt[b] = 0;
+  __syncthreads();
+  std::uint32_t draws = 0;
+  for (std::uint64_t base = static_cast<std::uint64_t>(blockIdx.x) * kPartThreads; base < a.slots;
+       base += static_cast<std::uint64_t>(gridDim.x) * kPartThreads) {
+    const std::uint64_t t = base + threadIdx.x;
+    if (t < a.slots) {
+      std::uint32_t anchor;
+      const std::uint32_t partner = sample_slot(a, t, anchor, draws);
+      a.neg_own[t] = partner;
+      if (is_local(a.own, partner)) atomicAdd(&sh_cnt[partner >> p.shift], 1u);
+    }
+  }
+  add_draws(a, draws);
+  __syncthreads();
+  for (std::uint32_t b = threadIdx.x; b < p.buckets; b += kPartThreads) {
+    p.block_hist[static_cast<std::size_t>(blockIdx.x) * p.buckets + b] = sh_cnt[b];
+  }
+}
+
+__global__ void bucket_column_scan_kernel(const PartitionArgs p, std::uint32_t blocks) {
+  const std::uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= p.buckets) return;
+  std::uint32_t run = 0;
+  for (std::uint32_t k = 0; k < blocks; ++k) {
+    const std::size_t at = static_cast<std::size_t>(k) * p.buckets + b;
+    const std::uint32_t c = p.block_hist[at];
+    p.block_hist[at] = run;
+    run += c;
+  }
+  p.bucket_off[b] = run;  // bucket total, turned into an offset by bucket_offsets_kernel
+}
+
+__global__ void bucket_offsets_kernel(const PartitionArgs p, std::uint32_t* __restrict__ in_off, std::uint32_t n) {
+  // single block of 1024 threads: in-place exclusive scan of bucket_off[0..buckets) with a running carry
+  __shared__ std::uint32_t warp_tot[32];
+  __shared__ std::uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (std::uint32_t base = 0; base < p.buckets; base += 1024) {
+    const std::uint32_t i = base + threadIdx.x;
+    const std::uint32_t v = i < p.buckets ? p.bucket_off[i] : 0;
+    std::uint32_t inc = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+      if (lane >= off) inc += o;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const std::uint32_t w = warp_tot[lane];
+      std::uint32_t winc = w;
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, winc, off);
+        if (lane >= off) winc += o;
+      }
+      warp_tot[lane] = winc - w;
+    }
+    __syncthreads();
+    const std::uint32_t excl = carry + warp_tot[warp] + inc - v;
+    if (i < p.buckets) p.bucket_off[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.bucket_off[p.buckets] = carry;
+    in_off[n] = carry;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads) partition_kernel(const SampleArgs a, const PartitionArgs p) {
+  extern __shared__ std::uint32_t sh_cur[];
+  for (std::uint32_t b = threadIdx.x; b < p.buckets; b += kPartThreads) {
+    sh_cur[b] = p.bucket_off[b] + p.block_hist[static_cast<std::size_t>(blockIdx.x) * p.buckets + b];
+  }
+  __syncthreads();
+  for (std::uint64_t base = static_cast<std::uint64_t>(blockIdx.x) * kPartThreads; base < a.slots;
+       base += static_cast<std::uint64_t>(gridDim.x) * kPartThreads) {
+    const std::uint64_t t = base + threadIdx.x;
+    if (t < a.slots) {
+      const std::uint32_t partner = a.neg_own[t];
+      if (is_local(a.own, partner)) {
+        const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t) : static_cast<std::uint32_t>(t / a.k);
+        const std::uint32_t pos = atomicAdd(&sh_cur[partner >> p.shift], 1u);
+        p.records[pos] = make_uint2(partner, anchor);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads) bucket_finalize_kernel(const PartitionArgs p, std::uint32_t n,
+                                                                       std::uint32_t* __restrict__ in_off,
+                                                                       std::uint32_t* __restrict__ in_anchor) {
+  extern __shared__ std::uint32_t sh_v[];  // per-vertex counts, then cursors; [vb]
+  __shared__ std::uint32_t warp_tot[kPartThreads / 32];
+  const std::uint32_t b = blockIdx.x, vb = 1u << p.shift, vmask = vb - 1;
+  const std::uint32_t lo = p.bucket_off[b], hi = p.bucket_off[b + 1];
+  for (std::uint32_t v = threadIdx.x; v < vb; v += kPartThreads) sh_v[v] = 0;
+  __syncthreads();
+  for (std::uint32_t i = lo + threadIdx.x; i < hi; i += kPartThreads) atomicAdd(&sh_v[p.records[i].x & vmask], 1u);
+  __syncthreads();
+  // block-wide exclusive scan of sh_v[0..vb): each thread owns a contiguous chunk
+  const std::uint32_t chunk = (vb + kPartThreads - 1) / kPartThreads;
+  const std::uint32_t first = threadIdx.x * chunk;
+  std::uint32_t local = 0;
+  for (std::uint32_t q = 0; q < chunk; ++q) local += first + q < vb ? sh_v[first + q] : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  std::uint32_t inc = local;
+  for (int off = 1; off < 32; off <<= 1) {
+    const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+    if (lane >= off) inc += o;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  std::uint32_t run = inc - local;
+  for (int w = 0; w < warp; ++w) run += warp_tot[w];
+  for (std::uint32_t q = 0; q < chunk; ++q) {
+    if (first + q < vb) {
+      const std::uint32_t c = sh_v[first + q];
+      sh_v[first + q] = run;  // cursor of this vertex inside the bucket
+      const std::uint64_t v = static_cast<std::uint64_t>(b) * vb + first + q;
+      if (v < n) in_off[v] = lo + run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (std::uint32_t i = lo + threadIdx.x; i < hi; i += kPartThreads) {
+    const uint2 rec = p.records[i];
+    in_anchor[lo + atomicAdd(&sh_v[rec.x & vmask], 1u)] = rec.y;
+  }
 }
 
 __global__ void unpermute_kernel(const std::uint32_t* __restrict__ neg_own, const std::uint32_t* __restrict__ eid_role,
@@ -1445,6 +1593,33 @@ int launch_sample(const SampleArgs& a, cudaStream_t stream) {
   if (a.slots == 0) return 0;
   sample_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a);
   return 1;
+}
+
+std::uint32_t partition_grid(std::uint64_t slots) {
+  int device = 0, sms = 148;
+  cudaGetDevice(&device);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return static_cast<std::uint32_t>(std::min<std::uint64_t>((slots + kPartThreads - 1) / kPartThreads,
+                                                            static_cast<std::uint64_t>(sms) * 4));
+}
+
+int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::uint32_t* in_off, std::uint32_t* in_anchor,
+                            cudaStream_t stream) {
+  if (a.slots == 0) return 0;
+  const std::uint32_t grid = p.grid;
+  const std::size_t hist_smem = static_cast<std::size_t>(p.buckets) * sizeof(std::uint32_t);
+  const std::size_t vert_smem = (static_cast<std::size_t>(1) << p.shift) * sizeof(std::uint32_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(bucket_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    configured = true;
+  }
+  sample_count_kernel<<<grid, kPartThreads, hist_smem, stream>>>(a, p);
+  bucket_column_scan_kernel<<<blocks_for(p.buckets, 128), 128, 0, stream>>>(p, grid);
+  bucket_offsets_kernel<<<1, 1024, 0, stream>>>(p, in_off, a.n);
+  partition_kernel<<<grid, kPartThreads, hist_smem, stream>>>(a, p);
+  bucket_finalize_kernel<<<p.buckets, kPartThreads, vert_smem, stream>>>(p, a.n, in_off, in_anchor);
+  return 5;
 }
 
 int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,

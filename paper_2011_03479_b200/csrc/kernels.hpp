@@ -58,6 +58,16 @@ struct SampleArgs {
   Ownership own;
 };
 
+// Two-level counting sort of the accepted samples by partner (large n).
+struct PartitionArgs {
+  std::uint32_t shift;          // coarse bucket = partner >> shift (2^shift vertices per bucket)
+  std::uint32_t buckets;        // ceil(n / 2^shift) <= 8192
+  std::uint32_t grid;           // persistent blocks of the sampling / partition passes
+  std::uint32_t* block_hist;    // [grid][buckets] per-block bucket counts, then run bases
+  std::uint32_t* bucket_off;    // [buckets + 1]
+  uint2* records;               // [S] (partner, anchor), grouped by coarse bucket
+};
+
 struct GatherArgs {
   const float* x_cur;
   float* x_next;
@@ -92,6 +102,10 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
                  const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out,
                  cudaStream_t stream);
 int launch_sample(const SampleArgs& a, cudaStream_t stream);
+std::uint32_t partition_grid(std::uint64_t slots);
+// sampling + bucketing by partner with streaming traffic only (fills neg_own, in_off[n+1], in_anchor)
+int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::uint32_t* in_off, std::uint32_t* in_anchor,
+                            cudaStream_t stream);
 // exclusive scan of in_cnt[n] into in_off[n+1]; scratch must hold ceil(n/4096)+1 words
 int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
                 cudaStream_t stream);

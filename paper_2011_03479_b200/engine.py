@@ -114,7 +114,7 @@ class Context:
 
     def __init__(self, g: Graph, dim: int, seed: int = 1, *, neg_mode=NEG_PER_EDGE_2, negatives=0,
                  math=MATH_TABLES, rng=RNG_REFERENCE, hash_bits=0, relabel=True, device=0, rank=0, world=1,
-                 comm_chunks=1, chunk_entries=0, deterministic=False, precise_distance=False, kernel_variant=0):
+                 comm_chunks=1, chunk_entries=0, deterministic=False, precise_distance=False, kernel_variant=0, bucket_mode=0):
         self._L = _capi.load()
         self._h = C.c_void_p()
         opt = _capi.Options()
@@ -124,6 +124,7 @@ class Context:
         opt.device, opt.rank, opt.world, opt.comm_chunks = device, rank, world, comm_chunks
         opt.chunk_entries, opt.deterministic = chunk_entries, int(deterministic)
         opt.precise_distance, opt.kernel_variant = int(precise_distance), kernel_variant
+        opt.bucket_mode = bucket_mode
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         rc = self._L.gempe_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), C.byref(opt))
         if rc != _capi.OK:

@@ -186,12 +186,29 @@ def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim, kernel)
                 **KERNELS[kernel])
 
 
+@pytest.mark.parametrize("bucket_mode", [1, 2])
 @pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5), (1, 20)])
-def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k):
+def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k, bucket_mode):
     for dim in (2, 64, 128):
         check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, neg_mode=neg_mode, k=k,
-                    exact=exact, iters=3)
+                    exact=exact, iters=3, bucket_mode=bucket_mode)
+
+
+@pytest.mark.parametrize("n", [300, 5000, 70001])
+def test_counting_sort_buckets_equal_atomic_buckets(G, n):
+    """Both bucketing methods must hand the gather the same multiset of incoming anchors per vertex: with
+    sorted buckets (deterministic mode) the rounds are bit-identical."""
+    _, src, dst = er_graph(n, 4 * n, 11)
+    outs = []
+    for mode in (1, 2):
+        ctx = G.Context(G.Graph(n, src, dst), 8, 3, neg_mode=1, negatives=9, deterministic=True, bucket_mode=mode)
+        for it in range(2):
+            he, hn = ctx.iterate(1.5, 1.0, it)
+        outs.append((ctx.get_coords(), he, hn))
+        ctx.close()
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
 @pytest.mark.parametrize("dim", [2, 64, 128])

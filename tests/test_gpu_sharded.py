@@ -18,15 +18,16 @@ def _views(ctx, which):
 
 
 @pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (4, 2), (8, 4)])
-@pytest.mark.parametrize("mode,k", [(0, 0), (1, 6)])
-def test_rank_contexts_reproduce_the_single_gpu_round(world, chunks, mode, k):
+@pytest.mark.parametrize("mode,k,bucket_mode", [(0, 0, 1), (1, 6, 1), (1, 6, 2)])
+def test_rank_contexts_reproduce_the_single_gpu_round(world, chunks, mode, k, bucket_mode):
     import torch
     import paper_2011_03479_b200 as G
     for (n, src, dst), dim in ((er_graph(1003, 6000, 3), 64), (star_plus_ring(400, hubs=2), 2)):
         g = G.Graph(n, src, dst)
-        single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+        single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64,
+                           bucket_mode=bucket_mode)
         ranks = [G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64, rank=r,
-                           world=world, comm_chunks=chunks) for r in range(world)]
+                           world=world, comm_chunks=chunks, bucket_mode=bucket_mode) for r in range(world)]
         block = ranks[0].block_rows
         assert ranks[0].padded_rows == world * chunks * block
         sigma = 1.0

@@ -19,12 +19,15 @@ ap.add_argument("--precise", action="store_true")
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--chunk-entries", type=int, default=0)
 ap.add_argument("--sigma", type=float, default=1.0)
+ap.add_argument("--bucket-mode", type=int, default=0)
 a = ap.parse_args()
 
-n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config)
+import torch  # noqa: E402
+n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config, device=torch.device('cuda', 0))
+torch.cuda.empty_cache()
 mode = P.NEG_PER_VERTEX_K if a.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
 ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode == P.NEG_PER_VERTEX_K else 0,
-                precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries)
+                precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries, bucket_mode=a.bucket_mode)
 ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
 sigma = a.sigma
 for it in range(2):
@@ -34,5 +37,5 @@ for it in range(2, 2 + a.rounds):
     ctx.iterate_async(1.5, sigma, it)
 he, hn = ctx.sync()
 tot, samp, gath = ctx.elapsed_ms()
-print(f"{a.config} variant {a.variant}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
+print(f"{a.config} variant {a.variant} bucket_mode {a.bucket_mode}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
       f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
