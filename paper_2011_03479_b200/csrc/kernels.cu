@@ -217,21 +217,37 @@ __global__ void bucket_offsets_kernel(const PartitionArgs p, std::uint32_t* __re
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads) partition_kernel(const SampleArgs a, const PartitionArgs p) {
+// One partition block replays the tile sets of several counting blocks one after another (rows row, row + gridDim,
+// ...), so that only gridDim.x * buckets runs are open at any time: with one block per SM their partially written
+// sectors (a few tens of MB) stay in L2 until they are complete.
+__global__ void __launch_bounds__(1024) partition_kernel(const SampleArgs a, const PartitionArgs p) {
   extern __shared__ std::uint32_t sh_cur[];
-  for (std::uint32_t b = threadIdx.x; b < p.buckets; b += kPartThreads) {
-    sh_cur[b] = p.bucket_off[b] + p.block_hist[static_cast<std::size_t>(blockIdx.x) * p.buckets + b];
-  }
-  __syncthreads();
-  for (std::uint64_t base = static_cast<std::uint64_t>(blockIdx.x) * kPartThreads; base < a.slots;
-       base += static_cast<std::uint64_t>(gridDim.x) * kPartThreads) {
-    const std::uint64_t t = base + threadIdx.x;
-    if (t < a.slots) {
-      const std::uint32_t partner = a.neg_own[t];
-      if (is_local(a.own, partner)) {
-        const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t) : static_cast<std::uint32_t>(t / a.k);
-        const std::uint32_t pos = atomicAdd(&sh_cur[partner >> p.shift], 1u);
-        p.records[pos] = make_uint2(partner, anchor);
+  for (std::uint32_t row = blockIdx.x; row < p.grid; row += gridDim.x) {
+    __syncthreads();
+    for (std::uint32_t b = threadIdx.x; b < p.buckets; b += blockDim.x) {
+      sh_cur[b] = p.bucket_off[b] + p.block_hist[static_cast<std::size_t>(row) * p.buckets + b];
+    }
+    __syncthreads();
+    // the counting block used kPartThreads-wide tiles at row*kPartThreads + j*grid*kPartThreads: the two halves of
+    // this 1024-thread block take alternate tiles of the row
+    constexpr int kIlp = 4;  // independent tiles in flight per thread
+    const std::uint64_t stride = blockDim.x / kPartThreads;
+    for (std::uint64_t tile = threadIdx.x / kPartThreads;; tile += stride * kIlp) {
+      if ((static_cast<std::uint64_t>(row) + tile * p.grid) * kPartThreads >= a.slots) break;
+      std::uint64_t t[kIlp];
+      std::uint32_t partner[kIlp];
+#pragma unroll
+      for (int q = 0; q < kIlp; ++q) {
+        t[q] = (static_cast<std::uint64_t>(row) + (tile + q * stride) * p.grid) * kPartThreads + threadIdx.x % kPartThreads;
+        partner[q] = t[q] < a.slots ? a.neg_own[t[q]] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int q = 0; q < kIlp; ++q) {
+        if (t[q] < a.slots && is_local(a.own, partner[q])) {
+          const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t[q]) : static_cast<std::uint32_t>(t[q] / a.k);
+          const std::uint32_t pos = atomicAdd(&sh_cur[partner[q] >> p.shift], 1u);
+          p.records[pos] = make_uint2(partner[q], anchor);
+        }
       }
     }
   }
@@ -1617,7 +1633,12 @@ int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::ui
   sample_count_kernel<<<grid, kPartThreads, hist_smem, stream>>>(a, p);
   bucket_column_scan_kernel<<<blocks_for(p.buckets, 128), 128, 0, stream>>>(p, grid);
   bucket_offsets_kernel<<<1, 1024, 0, stream>>>(p, in_off, a.n);
-  partition_kernel<<<grid, kPartThreads, hist_smem, stream>>>(a, p);
+  {
+    int device = 0, sms = 148;
+    cudaGetDevice(&device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    partition_kernel<<<std::min<std::uint32_t>(grid, static_cast<std::uint32_t>(sms)), 1024, hist_smem, stream>>>(a, p);
+  }
   bucket_finalize_kernel<<<p.buckets, kPartThreads, vert_smem, stream>>>(p, a.n, in_off, in_anchor);
   return 5;
 }
