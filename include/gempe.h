@@ -117,6 +117,21 @@ int gempe_iterate(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index,
 int gempe_iterate_async(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index);
 int gempe_sync(gempe_ctx* ctx, uint64_t* hist_edge, uint64_t* hist_nonedge);
 
+/* Device-resident sigma feedback: optimize_sigma_detail, the 1.5x growth cap and the PE
+ * estimate of run_single_iteration (src/slope.cpp:75-125, src/engine.cpp:293-314) evaluated on the GPU from the
+ * round's tallies, so that consecutive rounds need no host round trip.  gempe_set_sigma seeds the device state;
+ * gempe_iterate_auto runs one round with the device's sigma, updates it, and returns the new sigma, the PE
+ * estimate and the non-edge reweighting (any output pointer may be NULL).  The _async form only enqueues;
+ * gempe_get_sigma_state waits and reads the state.  gempe_sigma_update_async applies the update to the current
+ * device tallies (used after a cross-rank reduction of gempe_device_tallies, 1024 x u64). */
+int gempe_set_sigma(gempe_ctx* ctx, double mu, double sigma);
+int gempe_iterate_auto(gempe_ctx* ctx, uint64_t iter_index, double* sigma, double* pe_estimate,
+                       double* nonedge_weight, uint64_t* hist_edge, uint64_t* hist_nonedge);
+int gempe_iterate_auto_async(gempe_ctx* ctx, uint64_t iter_index);
+int gempe_get_sigma_state(gempe_ctx* ctx, double* sigma, double* pe_estimate, double* nonedge_weight);
+int gempe_sigma_update_async(gempe_ctx* ctx);
+void* gempe_device_tallies(gempe_ctx* ctx);
+
 /* IterationCapture (include/entropy_embed/engine.hpp:92-96): consolidated y (n*dim) and z (n) of the last
  * round, in double.  Capture must be switched on before the round. */
 int gempe_set_capture(gempe_ctx* ctx, int on);
@@ -175,6 +190,7 @@ typedef struct gempe_iteration_config { /* IterationConfig, engine.hpp:29-38 */
   int32_t neg_mode;
   uint32_t negatives;
   int32_t device;
+  int32_t host_sigma;         /* 1 = run the sigma search on the host (hostmath.cpp) instead of the device kernel */
 } gempe_iteration_config;
 
 typedef struct gempe_embed_result { /* EmbedResult, engine.hpp:98-107 */

@@ -271,6 +271,7 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.k = c->opt.negatives;
   g.neg_mode = c->opt.neg_mode;
   g.math = c->math;
+  g.math_dev = c->use_dev_math ? &c->sigma_state.get()->math : nullptr;
   g.tab = c->tables;
   c->launches += launch_gather(g, item_lo, item_hi, c->opt.kernel_variant, c->opt.precise_distance != 0, c->stream);
   cuda_check(cudaGetLastError(), "gather launch");
@@ -385,6 +386,7 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     pack_tables(c->tables);
     c->status.allocate(8, true);
     c->work_cursor.allocate(1, true);
+    c->sigma_state.allocate(1, true);
     c->hist.allocate(2 * kBins, true);
     for (auto& buf : c->x) buf.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
 
@@ -550,6 +552,67 @@ int gempe_iterate(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_inde
   if (rc != GEMPE_OK) return rc;
   return gempe_sync(c, hist_edge, hist_nonedge);
 }
+
+int gempe_set_sigma(gempe_ctx* c, double mu, double sigma) {
+  return guarded(c, [&] {
+    set_round_math(c, mu, sigma);
+    c->mu_dev = mu;
+    SigmaState st{};
+    st.sigma = sigma;
+    st.math = c->math;
+    cuda_check(cudaMemcpyAsync(c->sigma_state.get(), &st, sizeof st, cudaMemcpyHostToDevice, c->stream), "set_sigma");
+    cuda_check(cudaStreamSynchronize(c->stream), "set_sigma");
+  });
+}
+
+int gempe_sigma_update_async(gempe_ctx* c) {
+  return guarded(c, [&] {
+    require_live(c);
+    const double pairs = static_cast<double>(static_cast<std::uint64_t>(c->n) * (c->n - 1) / 2);
+    c->launches += launch_sigma_update(c->hist.get(), c->mu_dev, pairs, static_cast<double>(c->m),
+                                       c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->stream);
+    cuda_check(cudaGetLastError(), "sigma update");
+  });
+}
+
+int gempe_iterate_auto_async(gempe_ctx* c, std::uint64_t iter_index) {
+  return guarded(c, [&] {
+    require_live(c);
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    c->round_iter = iter_index;
+    c->use_dev_math = true;
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    sampling_passes(c, iter_index);
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
+    cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
+    c->use_dev_math = false;
+    c->cur ^= 1;
+    if (gempe_sigma_update_async(c) != GEMPE_OK) throw cuda_error(c->error);
+  });
+}
+
+int gempe_get_sigma_state(gempe_ctx* c, double* sigma, double* pe_estimate, double* nonedge_weight) {
+  return guarded(c, [&] {
+    SigmaState st{};
+    cuda_check(cudaMemcpyAsync(&st, c->sigma_state.get(), sizeof st, cudaMemcpyDeviceToHost, c->stream), "sigma D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sigma D2H");
+    if (sigma) *sigma = st.sigma;
+    if (pe_estimate) *pe_estimate = st.pe_estimate;
+    if (nonedge_weight) *nonedge_weight = st.nonedge_weight;
+  });
+}
+
+int gempe_iterate_auto(gempe_ctx* c, std::uint64_t iter_index, double* sigma, double* pe_estimate,
+                       double* nonedge_weight, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
+  int rc = gempe_iterate_auto_async(c, iter_index);
+  if (rc != GEMPE_OK) return rc;
+  rc = gempe_sync(c, hist_edge, hist_nonedge);
+  if (rc != GEMPE_OK) return rc;
+  return gempe_get_sigma_state(c, sigma, pe_estimate, nonedge_weight);
+}
+
+void* gempe_device_tallies(gempe_ctx* c) { return c->hist.get(); }
 
 int gempe_elapsed_ms(gempe_ctx* c, float out3[3]) {
   return guarded(c, [&] {

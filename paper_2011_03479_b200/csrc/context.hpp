@@ -91,6 +91,9 @@ struct gempe_ctx {
   gempe::DeviceBuffer<double> part_y, part_z;
   gempe::DeviceBuffer<unsigned long long> hist;
   gempe::DeviceBuffer<std::uint32_t> status, work_cursor;
+  gempe::DeviceBuffer<gempe::SigmaState> sigma_state;  // device-resident (mu, sigma) feedback
+  double mu_dev = gempe::kDefaultMu;
+  bool use_dev_math = false;  // gather reads RoundMath from sigma_state instead of kernel parameters
   gempe::DeviceBuffer<double> cap_y, cap_z;
   bool capture = false;
 

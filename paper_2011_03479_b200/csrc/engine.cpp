@@ -23,6 +23,7 @@ struct gempe_engine {
   std::vector<double> pe_trace;
   Tallies last_hist;
   bool have_hist = false;
+  bool sigma_seeded = false;
   double best_pe = std::numeric_limits<double>::infinity();
   DeviceBuffer<float> best_x;               // device snapshot, WORK indexing of the moment it was taken
   std::vector<std::uint32_t> best_to_work;
@@ -86,14 +87,24 @@ void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {
     rethrow(c, gempe_relabel(c, mix_seed(mix_seed(e->seed, 0xA11BE11), static_cast<std::uint64_t>(e->iter))));
   }
   Tallies t;
-  rethrow(c, gempe_iterate(c, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(), t.nonedge.data()));
-
-  const std::uint64_t samples = t.nonedge_total();
+  double pe = 0.0;
   const std::uint64_t pairs = static_cast<std::uint64_t>(e->n) * (e->n > 0 ? e->n - 1 : 0) / 2;
-  t.nonedge_weight = samples > 0 ? static_cast<double>(pairs - e->m) / static_cast<double>(samples) : 1.0;
-  // growth-capped sigma update (engine.cpp:302-307)
-  e->sigma = std::min(optimize_sigma(t, e->mu).sigma, e->sigma * 1.5);
-  const double pe = histogram_objective(t, e->mu, e->sigma) / static_cast<double>(pairs);
+  if (e->cfg.host_sigma) {
+    rethrow(c, gempe_iterate(c, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(), t.nonedge.data()));
+    const std::uint64_t samples = t.nonedge_total();
+    t.nonedge_weight = samples > 0 ? static_cast<double>(pairs - e->m) / static_cast<double>(samples) : 1.0;
+    // growth-capped sigma update (engine.cpp:302-307)
+    e->sigma = std::min(optimize_sigma(t, e->mu).sigma, e->sigma * 1.5);
+    pe = histogram_objective(t, e->mu, e->sigma) / static_cast<double>(pairs);
+  } else {
+    // sigma search, growth cap and PE estimate on the device (sigma_update_kernel)
+    if (!e->sigma_seeded) {
+      rethrow(c, gempe_set_sigma(c, e->mu, e->sigma));
+      e->sigma_seeded = true;
+    }
+    rethrow(c, gempe_iterate_auto(c, static_cast<std::uint64_t>(e->iter), &e->sigma, &pe, &t.nonedge_weight,
+                                  t.edge.data(), t.nonedge.data()));
+  }
   e->pe_trace.push_back(pe);
   e->last_hist = t;
   e->have_hist = true;
@@ -127,6 +138,7 @@ void gempe_default_iteration_config(gempe_iteration_config* cfg) {
   cfg->neg_mode = GEMPE_NEG_PER_EDGE_2;
   cfg->negatives = 0;
   cfg->device = 0;
+  cfg->host_sigma = 0;
 }
 
 int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,

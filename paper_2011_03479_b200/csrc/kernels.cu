@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
     sh_tab.erf[i] = a.tab.erf[i];
     sh_tab.ratio[i] = a.tab.ratio[i];
   }
+  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
               atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
             }
             float wf, sf;
-            pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+            pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
             // add_pair, own side (engine.cpp:66-72): y_u += wf * (x_v + sf * (x_u - x_v)); z_u += wf
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
@@ -849,8 +850,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
     sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
     sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
   }
-  const RoundMathF mf{static_cast<float>(a.math.mu), static_cast<float>(a.math.inv_sqrt2_sigma),
-                      static_cast<float>(a.math.A), static_cast<float>(a.math.B), static_cast<float>(a.math.C)};
+  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;  // sigma may live on the device (sigma_update_kernel)
+  const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
+                      static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -1023,7 +1025,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           if constexpr (PRECISE) {
             const double delta = sqrt(p[0]);
             bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
-            if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+            if (valid) pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
           } else {
             float delta = sqrtf(p[0]);
             // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
@@ -1061,7 +1063,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
                 delta = static_cast<float>(exact);
               }
             }
-            if (valid) pair_terms_f(delta, is_edge, mf, a.math.exact, sh_tab, wf, sf);
+            if (valid) pair_terms_f(delta, is_edge, mf, rm.exact, sh_tab, wf, sf);
           }
           if (tally) {  // tallied before the w > 0 test (engine.cpp:221-222)
             bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
@@ -1311,8 +1313,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
     sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
     sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
   }
-  const RoundMathF mf{static_cast<float>(a.math.mu), static_cast<float>(a.math.inv_sqrt2_sigma),
-                      static_cast<float>(a.math.A), static_cast<float>(a.math.B), static_cast<float>(a.math.C)};
+  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;  // sigma may live on the device (sigma_update_kernel)
+  const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
+                      static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1434,7 +1437,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
     if constexpr (PRECISE) {
       const double delta = sqrt(p[0]);
       bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
-      if (valid) pair_terms(delta, is_edge, a.math, sh_tab, wf, sf);
+      if (valid) pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
     } else {
       float delta = sqrtf(p[0]);
       // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
@@ -1470,7 +1473,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
           }
         }
       }
-      if (valid) pair_terms_f(delta, is_edge, mf, a.math.exact, sh_tab, wf, sf);
+      if (valid) pair_terms_f(delta, is_edge, mf, rm.exact, sh_tab, wf, sf);
     }
     if (tally) {  // tallied before the w > 0 test (engine.cpp:221-222)
       bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
@@ -1579,6 +1582,130 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
   for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) {
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
+  }
+}
+
+// ---------------------------------------------------------------------------------- sigma search on the device
+//
+// optimize_sigma_detail + the growth cap + the PE estimate of run_single_iteration (slope.cpp:75-125,
+// engine.cpp:293-314) on the round's 2x512 tallies: one block, thread b owns bin b of both tallies, every objective
+// evaluation is one block-wide double sum.  Removes the host round trip (8 KiB D2H + ~0.3 ms of libm) between
+// rounds; the next round's gather reads the folded RoundMath straight from device memory.
+namespace sigma {
+
+constexpr double kLn2 = 0.693147180559945309417232121458176568;
+constexpr double kSqrt2 = 1.41421356237309504880168872420969808;
+constexpr double kSqrtPi = 1.77245385090551602729816748334;
+
+__device__ __forceinline__ double tail_ratio(double x) {  // gauss_over_erfc, sigmoid.hpp:39-45
+  if (x <= 6.0) return exp(-x * x) / erfc(x);
+  const double r = 1.0 / (x * x);
+  return x * kSqrtPi / (1.0 + r * (-0.5 + r * (0.75 + r * (-1.875 + 6.5625 * r))));
+}
+__device__ __forceinline__ double cost_tail(double mid, double mu, double s, bool edge) {  // sigmoid.hpp:50-59
+  const double u = (mid - mu) / (kSqrt2 * s);
+  const double x = edge ? u : -u;
+  if (x <= 6.0) return 1.0 - log2(erfc(x));
+  const double r = 1.0 / (x * x);
+  const double series = 1.0 + r * (-0.5 + r * (0.75 + r * (-1.875 + 6.5625 * r)));
+  return 1.0 - (-x * x - log(x * kSqrtPi) + log(series)) / kLn2;
+}
+__device__ __forceinline__ double cost_floor(double mid, double mu, double s, bool edge) {  // sigmoid.hpp:69-81
+  const double e = erf((mid - mu) / (kSqrt2 * s));
+  double pr = edge ? 0.5 - 0.5 * e : 0.5 + 0.5 * e;
+  pr = fmin(fmax(pr, 1e-12), 1.0 - 1e-12);
+  return -log2(pr);
+}
+__device__ __forceinline__ double cost_dsigma(double mid, double mu, double s, bool edge) {  // sigmoid.hpp:108-113
+  const double u = (mid - mu) / (kSqrt2 * s);
+  const double v = 2.0 / (kSqrtPi * kLn2) * u * tail_ratio(edge ? u : -u) / s;
+  return edge ? -v : v;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < kBins / 32; ++w) t += scratch[w];
+  return t;
+}
+
+}  // namespace sigma
+
+__global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long long* __restrict__ hist, double mu,
+                                                             double pairs, double edges, int exact_math,
+                                                             SigmaState* __restrict__ state) {
+  using namespace sigma;
+  __shared__ double scratch[kBins / 32];
+  const int b = threadIdx.x;
+  const double ec = static_cast<double>(hist[b]), nc = static_cast<double>(hist[kBins + b]);
+  const double mid = (b + 0.5) * 12.0 / kBins;  // histogram.hpp:52
+  const double samples = block_sum(nc, scratch);
+  const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;  // engine.cpp:296-300
+  auto total = [&](double s, int which) {
+    double v = 0.0;
+    if (which == 0) {
+      if (ec != 0.0) v += ec * cost_tail(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_tail(mid, mu, s, false);
+    } else if (which == 1) {
+      if (ec != 0.0) v += ec * cost_dsigma(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_dsigma(mid, mu, s, false);
+    } else {
+      if (ec != 0.0) v += ec * cost_floor(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_floor(mid, mu, s, false);
+    }
+    return block_sum(v, scratch);
+  };
+  // coarse geometric scan of the unfloored cost, then bisection on dF/dsigma inside the best cell
+  constexpr int kGrid = 17;
+  double grid[kGrid], best_cost = 0.0;
+  int best = 0;
+  for (int i = 0; i < kGrid; ++i) {
+    grid[i] = 1e-3 * pow(16.0 / 1e-3, static_cast<double>(i) / (kGrid - 1));
+    const double cost = total(grid[i], 0);
+    if (i == 0 || cost < best_cost) best_cost = cost, best = i;
+  }
+  double sigma_opt = grid[best];
+  double lo = grid[best > 0 ? best - 1 : 0], hi = grid[best < kGrid - 1 ? best + 1 : kGrid - 1];
+  double f_lo = total(lo, 1);
+  const double f_hi = total(hi, 1);
+  int steps = 0;
+  if (f_lo < 0.0 && f_hi > 0.0) {
+    while (hi - lo > 1e-4 && steps < 60) {
+      ++steps;
+      const double m = 0.5 * (lo + hi);
+      const double f_mid = total(m, 1);
+      if (f_mid == 0.0) {
+        lo = hi = m;
+        break;
+      }
+      if ((f_mid > 0.0) == (f_lo > 0.0)) {
+        lo = m;
+        f_lo = f_mid;
+      } else {
+        hi = m;
+      }
+    }
+    const double refined = 0.5 * (lo + hi);
+    if (total(refined, 0) <= best_cost) sigma_opt = refined;
+  }
+  const double sigma_new = fmin(sigma_opt, state->sigma * 1.5);  // growth cap, engine.cpp:302-307
+  const double pe = total(sigma_new, 2) / pairs;
+  if (b == 0) {
+    const double c1 = 2.0 / (3.14159265358979323846264338327950288 * kLn2);
+    const double c2 = 1.0 / (2.50662827463100050241576528481 * kLn2);
+    state->sigma = sigma_new;
+    state->pe_estimate = pe;
+    state->nonedge_weight = nw;
+    state->bisection_steps = steps;
+    state->math.mu = mu;
+    state->math.inv_sqrt2_sigma = 1.0 / (kSqrt2 * sigma_new);
+    state->math.A = c1 / (sigma_new * sigma_new);
+    state->math.B = c2 / (sigma_new * sigma_new * sigma_new);
+    state->math.C = c2 / sigma_new;
+    state->math.exact = exact_math;
   }
 }
 
@@ -1797,6 +1924,12 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);
+  return 1;
+}
+
+int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
+                        SigmaState* state, cudaStream_t stream) {
+  sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
   return 1;
 }
 

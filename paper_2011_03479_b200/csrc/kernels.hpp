@@ -25,6 +25,16 @@ struct RoundMath {
   int exact;               // 1: exp(-x^2)/erfc(x), 0: piecewise tables
 };
 
+// Device-resident sigma feedback (sigma_update_kernel): the state after the latest round's tallies.
+struct SigmaState {
+  double sigma;
+  double pe_estimate;
+  double nonedge_weight;
+  int bisection_steps;
+  int pad;
+  RoundMath math;  // folded constants of `sigma` for the next round's gather
+};
+
 // knots[17] a[16] b[16] c[16] per table (the lo/hi clamps are the first/last knot).
 struct DeviceTables {
   double erf[65];
@@ -92,6 +102,7 @@ struct GatherArgs {
   std::uint32_t k;
   int neg_mode;
   RoundMath math;
+  const RoundMath* math_dev;       // non-null: read the round's constants from device memory (device sigma feedback)
   DeviceTables tab;
 };
 
@@ -120,6 +131,9 @@ int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t*
 // variant 0: batched kernel (default), 1: v0 row-at-a-time kernel.  precise: reference-exact double pair_distance.
 int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, int variant, bool precise,
                   cudaStream_t stream);
+// optimize_sigma + growth cap + PE estimate on the device tallies; updates *state (and state->math)
+int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
+                        SigmaState* state, cudaStream_t stream);
 int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,
                        std::uint64_t seed, double stddev, cudaStream_t stream);
 

@@ -86,6 +86,7 @@ class IterationConfig:
     neg_mode: int = NEG_PER_EDGE_2
     negatives: int = 0
     device: int = 0
+    host_sigma: bool = False  # True: sigma search on the host instead of the device kernel
 
 
 @dataclass
@@ -226,6 +227,34 @@ class Context:
         self._check(self._L.gempe_sync(self._h, _capi.ptr(he), _capi.ptr(hn)))
         return he, hn
 
+    # -- device-resident sigma feedback ----------------------------------------------------------------
+    def set_sigma(self, mu: float, sigma: float):
+        self._check(self._L.gempe_set_sigma(self._h, mu, sigma))
+
+    def iterate_auto(self, iter_index: int):
+        """One round with the device's sigma, then the device sigma search.  Returns (sigma, pe, nonedge_weight,
+        hist_edge, hist_nonedge)."""
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        s, pe, nw = C.c_double(), C.c_double(), C.c_double()
+        self._check(self._L.gempe_iterate_auto(self._h, iter_index, C.byref(s), C.byref(pe), C.byref(nw), _capi.ptr(he),
+                                               _capi.ptr(hn)))
+        return s.value, pe.value, nw.value, he, hn
+
+    def iterate_auto_async(self, iter_index: int):
+        self._check(self._L.gempe_iterate_auto_async(self._h, iter_index))
+
+    def sigma_state(self):
+        s, pe, nw = C.c_double(), C.c_double(), C.c_double()
+        self._check(self._L.gempe_get_sigma_state(self._h, C.byref(s), C.byref(pe), C.byref(nw)))
+        return s.value, pe.value, nw.value
+
+    def sigma_update_async(self):
+        self._check(self._L.gempe_sigma_update_async(self._h))
+
+    def device_tallies(self) -> int:
+        return self._L.gempe_device_tallies(self._h)
+
     def elapsed_ms(self):
         out = (C.c_float * 3)()
         self._check(self._L.gempe_elapsed_ms(self._h, C.byref(out)))
@@ -286,6 +315,7 @@ class EmbeddingEngine:
         if cfg.hash_bits is not None and not (1 <= cfg.hash_bits <= 31):
             raise ConfigError("hash table bits must be in [1,31]")
         c.neg_mode, c.negatives, c.device = cfg.neg_mode, cfg.negatives, cfg.device
+        c.host_sigma = int(cfg.host_sigma)
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         self._pe_trace = []
         rc = self._L.gempe_engine_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,

@@ -421,3 +421,37 @@ def test_config4_size_properties(G):
     bins = np.clip((d / 12.0 * 512).astype(np.int64), 0, 511)
     assert np.abs(np.bincount(bins, minlength=512).astype(np.int64) - he.astype(np.int64)).sum() <= 4
     ctx.close()
+
+
+def test_device_sigma_search_matches_host_search(G):
+    """sigma_update_kernel (device) against hostmath.cpp (pinned to the reference by tests/test_host_numerics.py)
+    on the tallies of real rounds, including the growth cap and the PE estimate."""
+    from paper_2011_03479_b200 import engine as E
+    for (n, src, dst), dim, mode, k in ((er_graph(800, 4000, 5), 2, 0, 0), (er_graph(3000, 20000, 6), 32, 1, 7),
+                                        (clique_pair(12), 2, 0, 0)):
+        ctx = G.Context(G.Graph(n, src, dst), dim, 4, neg_mode=mode, negatives=k)
+        ctx.set_sigma(1.5, 1.0)
+        sigma = 1.0
+        pairs = n * (n - 1) // 2
+        for it in range(8):
+            s_dev, pe_dev, nw_dev, he, hn = ctx.iterate_auto(it)
+            nw = (pairs - len(src)) / hn.sum()
+            s_host = min(E.optimize_sigma(he, hn, nw, 1.5)[0], sigma * 1.5)
+            pe_host = E.histogram_objective(he, hn, nw, 1.5, s_host) / pairs
+            assert abs(nw_dev - nw) <= 1e-12 * nw
+            assert abs(s_dev - s_host) <= 1e-9 * s_host, (it, s_dev, s_host)
+            assert abs(pe_dev - pe_host) <= 1e-9 * abs(pe_host)
+            sigma = s_dev
+        ctx.close()
+
+
+def test_engine_host_and_device_sigma_paths_agree(G):
+    n, src, dst = er_graph(500, 2500, 12)
+    runs = []
+    for host in (False, True):
+        eng = G.EmbeddingEngine(G.Graph(n, src, dst), 2, G.IterationConfig(host_sigma=host), 3)
+        trace = [eng.run_single_iteration() for _ in range(6)]
+        runs.append(([t.sigma for t in trace], [t.pe_estimate for t in trace], eng.work_coords()))
+        eng.close()
+    assert np.allclose(runs[0][0], runs[1][0], rtol=1e-6) and np.allclose(runs[0][1], runs[1][1], rtol=1e-6)
+    assert rel_l2(runs[0][2], runs[1][2]) <= 1e-4
