@@ -246,6 +246,23 @@ def main():
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
                             "draws_per_sample": p_bar}
 
+        # whole iterations with the device-resident sigma feedback (round + sigma search + PE estimate, no host sync)
+        ctx.set_sigma(mu, sigma)
+        for s in range(3):
+            ctx.iterate_auto_async(eng.iter + s)
+        torch.cuda.synchronize()
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fe0.record(stream)
+        for s in range(args.steps):
+            ctx.iterate_auto_async(eng.iter + 3 + s)
+        fe1.record(stream)
+        torch.cuda.synchronize()
+        ctx.sync()
+        full_ms = fe0.elapsed_time(fe1) / args.steps
+        line["full_iteration"] = {"ms_per_step": full_ms, "value": pair_terms / (full_ms * 1e-3), "unit": UNIT,
+                                  "what": "round + device sigma search + PE estimate (run_single_iteration), no host sync"}
+        ctx.elapsed_ms()
+
         # end to end through the C-ABI with HOST buffers: X_t in (pinned), round, X_{t+1} + tallies out
         x_host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
         x_np = x_host.numpy()

@@ -152,6 +152,7 @@ uint32_t gempe_row_stride(const gempe_ctx* ctx);                   /* floats per
 uint32_t gempe_padded_rows(const gempe_ctx* ctx);                  /* world*comm_chunks*block rows */
 uint32_t gempe_block_rows(const gempe_ctx* ctx);                   /* rows per (chunk, rank) ownership block */
 int gempe_begin_round(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index); /* sampling passes */
+int gempe_begin_round_auto(gempe_ctx* ctx, uint64_t iter_index); /* same, sigma taken from the device state */
 int gempe_gather_chunk(gempe_ctx* ctx, int chunk);                 /* gradient+update for one comm chunk */
 int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t / X_{t+1} */
 /* Device time in ms of the last `rounds` enqueued through gempe_iterate_async since the previous call

@@ -514,6 +514,16 @@ int gempe_begin_round(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_
   });
 }
 
+int gempe_begin_round_auto(gempe_ctx* c, std::uint64_t iter_index) {
+  return guarded(c, [&] {
+    require_live(c);
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    c->round_iter = iter_index;
+    c->use_dev_math = true;  // until gempe_end_round
+    sampling_passes(c, iter_index);
+  });
+}
+
 int gempe_gather_chunk(gempe_ctx* c, int chunk) {
   return guarded(c, [&] {
     require_live(c);
@@ -523,6 +533,7 @@ int gempe_gather_chunk(gempe_ctx* c, int chunk) {
 }
 
 int gempe_end_round(gempe_ctx* c) {
+  c->use_dev_math = false;
   c->cur ^= 1;
   return GEMPE_OK;
 }

@@ -293,6 +293,9 @@ class Context:
     def begin_round(self, mu, sigma, iter_index):
         self._check(self._L.gempe_begin_round(self._h, mu, sigma, iter_index))
 
+    def begin_round_auto(self, iter_index):
+        self._check(self._L.gempe_begin_round_auto(self._h, iter_index))
+
     def gather_chunk(self, chunk: int):
         self._check(self._L.gempe_gather_chunk(self._h, chunk))
 

@@ -57,10 +57,27 @@ class CudaShardOps:
         return torch.as_tensor(_DeviceArray(ptr, (self.rows, self.ld)), device=self.device)
 
     def begin_round(self, mu, sigma, it):
-        self.ctx.begin_round(mu, sigma, it)
+        if mu is None:
+            self.ctx.begin_round_auto(it)  # sigma lives on the device (sigma_update_kernel)
+        else:
+            self.ctx.begin_round(mu, sigma, it)
 
     def gather_chunk(self, c):
         self.ctx.gather_chunk(c)
+
+    # device-resident sigma feedback: tallies are reduced across ranks on the device, every rank runs the same search
+    def seed_sigma(self, mu, sigma):
+        self.ctx.set_sigma(mu, sigma)
+
+    def tallies_tensor(self) -> torch.Tensor:
+        return torch.as_tensor(_DeviceArray(self.ctx.device_tallies(), (2 * HIST,), "<i8"), device=self.device)
+
+    def sigma_update(self):
+        self.ctx.sigma_update_async()
+
+    def sigma_state(self):
+        self.ctx.sync()  # raises on divergence / retry cap of the round
+        return self.ctx.sigma_state()
 
     def end_round(self):
         self.ctx.end_round()
@@ -82,6 +99,7 @@ class ShardedEngine:
         self.mu, self.sigma, self.iter = 1.5, 1.0, 0
         self.pe_trace: List[float] = []
         self._pending = []
+        self._seeded = False
 
     def _wait_pending(self):
         for w in self._pending:
@@ -118,7 +136,23 @@ class ShardedEngine:
 
     def run_single_iteration(self):
         """EmbeddingEngine::run_single_iteration across the group: every rank computes the same sigma from
-        the reduced tallies (engine.cpp:293-314)."""
+        the reduced tallies (engine.cpp:293-314).  With a CUDA backend nothing but the scalar results leaves the
+        device: the tallies are all-reduced in place and the sigma search runs on every rank's GPU."""
+        if hasattr(self.ops, "sigma_update"):
+            if not self._seeded:
+                self.ops.seed_sigma(self.mu, self.sigma)
+                self._seeded = True
+            self.round_async(None, None, self.iter)
+            ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
+            with ctx:
+                self._wait_pending()
+                if self.world > 1:
+                    dist.all_reduce(self.ops.tallies_tensor(), op=dist.ReduceOp.SUM, group=self.group)
+                self.ops.sigma_update()
+            self.sigma, pe, _ = self.ops.sigma_state()
+            self.pe_trace.append(pe)
+            self.iter += 1
+            return pe, self.sigma
         self.round_async(self.mu, self.sigma, self.iter)
         he, hn = self.finish_round()
         pairs = self.n * (self.n - 1) // 2
