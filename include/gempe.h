@@ -175,6 +175,31 @@ double gempe_host_histogram_objective_dsigma(const uint64_t* hist_edge, const ui
 int gempe_host_random_relabel(uint32_t n, uint64_t seed, uint32_t* forward);
 uint64_t gempe_host_mix_seed(uint64_t seed, uint64_t component);   /* include/entropy_embed/rng.hpp:26-28 */
 
+/* ---- graph ingest and embedding export (host side) ------------------------------ */
+typedef struct gempe_graph {   /* Graph, include/entropy_embed/graph.hpp:12-23; arrays owned by the library */
+  uint32_t n;
+  uint64_t m;
+  uint32_t* src;
+  uint32_t* dst;
+  uint64_t* raw_labels;        /* original input id of every compact vertex (edge lists only, else NULL) */
+} gempe_graph;
+
+/* load_edge_list (src/graph.cpp:75-133): "i<ws>j" lines; '#'/'%' comments and blank lines skipped; self-loops
+ * dropped; duplicate undirected edges merged; ids compacted in first-appearance order.  A malformed line returns
+ * GEMPE_ERR_DATA with *error_line set (parse_error::line()); no surviving edge returns GEMPE_ERR_DATA with
+ * *error_line = 0 (data_error).  Messages through gempe_last_error(NULL). */
+int gempe_parse_edge_list(const char* text, uint64_t len, gempe_graph* out, uint64_t* error_line);
+/* load_graph_snapshot (src/graph.cpp:149-170): "GEMP", u32 n, u64 m, src[m], dst[m], little-endian. */
+int gempe_parse_graph_snapshot(const void* bytes, uint64_t len, gempe_graph* out);
+/* looks_like_snapshot ? load_graph_snapshot : load_edge_list (tools/embed_main.cpp:150-153). */
+int gempe_load_graph_file(const char* path, gempe_graph* out, uint64_t* error_line);
+int gempe_write_graph_snapshot(const char* path, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst);
+void gempe_graph_free(gempe_graph* g);
+/* write_embedding_tsv (src/io.cpp:17-46): rows in ascending label order, "%.6g" coordinates; labels NULL =
+ * identity; perm_forward non-NULL reads row perm_forward[v] for vertex v. */
+int gempe_write_embedding_tsv(const char* path, uint32_t n, uint32_t dim, const float* coords, const uint64_t* labels,
+                              const uint32_t* perm_forward);
+
 /* ---- run-level facade: EmbeddingEngine / embed() (include/entropy_embed/engine.hpp:112-171) ------- */
 typedef struct gempe_engine gempe_engine;
 

@@ -252,9 +252,16 @@ class Ref:
                                      C.POINTER(C.c_double)]
         L.ref_pe_exact.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, C.c_uint32, f32p,
                                    C.POINTER(C.c_double)]
+        L.ref_load_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.ref_write_embedding_tsv.restype = C.c_long
+        L.ref_write_embedding_tsv.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_long]
+        L.ref_save_graph_snapshot.restype = C.c_long
+        L.ref_save_graph_snapshot.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, C.c_void_p, C.c_long]
 
     def error(self):
-        return self.lib.ref_last_error().decode()
+        return self.lib.ref_last_error().decode(errors="replace")
 
     def fastmath_table(self, which):
         out = np.zeros(67, np.float64)
@@ -287,6 +294,55 @@ class Ref:
         out = np.empty((n, dim), np.float32)
         self.lib.ref_init_embedding(n, dim, seed, out)
         return out
+
+    def load_edge_list(self, text: bytes):
+        """load_edge_list: dict(rc, n, src, dst, labels, line, error)."""
+        n, m, line = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        rc = self.lib.ref_load_edge_list(text, len(text), C.byref(n), C.byref(m), None, None, None, C.byref(line))
+        if rc:
+            return dict(rc=rc, line=line.value, error=self.error())
+        src = np.zeros(m.value, np.uint32)
+        dst = np.zeros(m.value, np.uint32)
+        lab = np.zeros(n.value, np.uint64)
+        self.lib.ref_load_edge_list(text, len(text), C.byref(n), C.byref(m), src.ctypes.data_as(C.c_void_p),
+                                    dst.ctypes.data_as(C.c_void_p), lab.ctypes.data_as(C.c_void_p), C.byref(line))
+        return dict(rc=0, n=n.value, src=src, dst=dst, labels=lab)
+
+    def write_embedding_tsv(self, coords, labels=None, perm_forward=None) -> bytes:
+        """write_embedding_tsv of the reference.  Runs in a numpy-free child process: inside a process that has
+        imported numpy the reference's iostream/snprintf path segfaults in this image (the same call is fine from
+        plain ctypes or C++), and this is test infrastructure, not something to debug in the reference."""
+        import json
+        import sys
+        coords = np.ascontiguousarray(coords, np.float32)
+        payload = json.dumps({"so": REF_SO, "n": int(coords.shape[0]), "dim": int(coords.shape[1]),
+                              "bits": [int(v) for v in coords.view(np.uint32).ravel()],
+                              "labels": None if labels is None else [int(v) for v in labels],
+                              "perm": None if perm_forward is None else [int(v) for v in perm_forward]})
+        child = (
+            "import ctypes as C, json, sys\n"
+            "p = json.loads(sys.stdin.read())\n"
+            "L = C.CDLL(p['so'])\n"
+            "L.ref_write_embedding_tsv.restype = C.c_long\n"
+            "L.ref_write_embedding_tsv.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long]\n"
+            "x = (C.c_uint32 * len(p['bits']))(*p['bits'])\n"
+            "lab = (C.c_uint64 * p['n'])(*p['labels']) if p['labels'] is not None else None\n"
+            "perm = (C.c_uint32 * p['n'])(*p['perm']) if p['perm'] is not None else None\n"
+            "buf = C.create_string_buffer(1 << 22)\n"
+            "k = L.ref_write_embedding_tsv(p['n'], p['dim'], C.cast(x, C.c_void_p), C.cast(lab, C.c_void_p) if lab else None,"
+            " C.cast(perm, C.c_void_p) if perm else None, C.cast(buf, C.c_void_p), len(buf))\n"
+            "sys.stdout.buffer.write(buf.raw[:k] if k >= 0 else b'')\n"
+            "sys.exit(0 if k >= 0 else 1)\n")
+        out = subprocess.run([sys.executable, "-c", child], input=payload.encode(), capture_output=True)
+        if out.returncode != 0:
+            raise RuntimeError("reference write_embedding_tsv failed: " + out.stderr.decode(errors="replace")[-300:])
+        return out.stdout
+
+    def save_graph_snapshot(self, n, src, dst) -> bytes:
+        buf = C.create_string_buffer(16 + 8 * len(src) + 16)
+        k = self.lib.ref_save_graph_snapshot(n, len(src), np.ascontiguousarray(src, np.uint32),
+                                             np.ascontiguousarray(dst, np.uint32), C.cast(buf, C.c_void_p), len(buf))
+        return buf.raw[:k]
 
     def pe_exact(self, n, src, dst, coords):
         pe = C.c_double()

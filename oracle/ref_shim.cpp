@@ -12,6 +12,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,7 @@
 #include "entropy_embed/graph.hpp"
 #include "entropy_embed/hash_set.hpp"
 #include "entropy_embed/histogram.hpp"
+#include "entropy_embed/io.hpp"
 #include "entropy_embed/metrics.hpp"
 #include "entropy_embed/piecewise.hpp"
 #include "entropy_embed/rng.hpp"
@@ -320,6 +322,62 @@ int ref_pe_exact(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
   } catch (const std::exception& e) {
     return classify(e);
   }
+}
+
+// ---- graph.cpp:75-170, io.cpp:17-46 (text formats) ---------------------------------------------------------
+// Returns 0 and fills n / m (call again with arrays sized n / m to receive them), 2 on data_error, 5 on
+// parse_error with *line set.
+int ref_load_edge_list(const char* text, std::uint64_t len, std::uint32_t* n, std::uint64_t* m, std::uint32_t* src,
+                       std::uint32_t* dst, std::uint64_t* labels, std::uint64_t* line) {
+  try {
+    std::istringstream in(std::string(text, len));
+    std::vector<std::uint64_t> raw;
+    const ee::Graph g = ee::load_edge_list(in, &raw);
+    *n = g.n;
+    *m = g.edge_count();
+    if (src) std::copy(g.src.begin(), g.src.end(), src);
+    if (dst) std::copy(g.dst.begin(), g.dst.end(), dst);
+    if (labels) std::copy(raw.begin(), raw.end(), labels);
+    return 0;
+  } catch (const ee::parse_error& e) {
+    g_error = e.what();
+    if (line) *line = e.line();
+    return 5;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+// write_embedding_tsv into a caller buffer; returns the text length (or -1 when cap is too small / on error)
+long ref_write_embedding_tsv(std::uint32_t n, std::uint32_t dim, const float* coords, const std::uint64_t* labels,
+                             const std::uint32_t* perm_forward, char* out, long cap) {
+  try {
+    ee::Embedding e;
+    e.n = n;
+    e.dim = dim;
+    e.coords.assign(coords, coords + static_cast<std::size_t>(n) * dim);
+    std::vector<std::uint64_t> lab;
+    if (labels) lab.assign(labels, labels + n);
+    ee::Permutation perm;
+    if (perm_forward) perm.forward.assign(perm_forward, perm_forward + n);
+    std::ostringstream os;
+    ee::write_embedding_tsv(e, lab, os, perm_forward ? &perm : nullptr);
+    const std::string s = os.str();
+    if (static_cast<long>(s.size()) > cap) return -1;
+    std::memcpy(out, s.data(), s.size());
+    return static_cast<long>(s.size());
+  } catch (const std::exception& e) {
+    classify(e);
+    return -1;
+  }
+}
+long ref_save_graph_snapshot(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const std::uint32_t* dst,
+                             char* out, long cap) {
+  std::ostringstream os(std::ios::binary);
+  ee::save_graph_snapshot(make_graph(n, m, src, dst), os);
+  const std::string s = os.str();
+  if (static_cast<long>(s.size()) > cap) return -1;
+  std::memcpy(out, s.data(), s.size());
+  return static_cast<long>(s.size());
 }
 
 }  // extern "C"

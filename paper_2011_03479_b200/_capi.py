@@ -32,7 +32,9 @@ SYMBOLS = [
     "gempe_host_histogram_objective", "gempe_host_histogram_objective_dsigma", "gempe_host_random_relabel",
     "gempe_host_mix_seed", "gempe_default_iteration_config", "gempe_engine_create", "gempe_engine_destroy",
     "gempe_engine_last_error", "gempe_engine_context", "gempe_engine_degenerate", "gempe_engine_iteration",
-    "gempe_engine_sigma", "gempe_engine_run_single_iteration", "gempe_engine_run",
+    "gempe_engine_sigma", "gempe_engine_run_single_iteration", "gempe_engine_run", "gempe_parse_edge_list",
+    "gempe_parse_graph_snapshot", "gempe_load_graph_file", "gempe_write_graph_snapshot", "gempe_graph_free",
+    "gempe_write_embedding_tsv",
 ]
 
 
@@ -49,6 +51,11 @@ class IterationConfigC(C.Structure):
                 ("convergence_tol", C.c_double), ("convergence_window", C.c_int32), ("relabel_period", C.c_int32),
                 ("fast_math", C.c_int32), ("hash_bits", C.c_int32), ("neg_mode", C.c_int32),
                 ("negatives", C.c_uint32), ("device", C.c_int32), ("host_sigma", C.c_int32)]
+
+
+class GraphC(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("m", C.c_uint64), ("src", C.POINTER(C.c_uint32)), ("dst", C.POINTER(C.c_uint32)),
+                ("raw_labels", C.POINTER(C.c_uint64))]
 
 
 class EmbedResultC(C.Structure):
@@ -136,6 +143,12 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_engine_sigma": (dbl, [vp]),
         "gempe_engine_run_single_iteration": (i32, [vp, C.POINTER(dbl), C.POINTER(dbl)]),
         "gempe_engine_run": (i32, [vp, C.POINTER(EmbedResultC)]),
+        "gempe_parse_edge_list": (i32, [C.c_char_p, u64, C.POINTER(GraphC), C.POINTER(u64)]),
+        "gempe_parse_graph_snapshot": (i32, [C.c_char_p, u64, C.POINTER(GraphC)]),
+        "gempe_load_graph_file": (i32, [C.c_char_p, C.POINTER(GraphC), C.POINTER(u64)]),
+        "gempe_write_graph_snapshot": (i32, [C.c_char_p, u32, u64, vp, vp]),
+        "gempe_graph_free": (None, [C.POINTER(GraphC)]),
+        "gempe_write_embedding_tsv": (i32, [C.c_char_p, u32, u32, vp, vp, vp]),
     }
     assert sorted(sig) == sorted(SYMBOLS)
     for name, (res, args) in sig.items():

@@ -445,3 +445,78 @@ def random_relabel(n: int, seed: int) -> np.ndarray:
 
 def mix_seed(seed: int, component: int) -> int:
     return _capi.load().gempe_host_mix_seed(seed, component)
+
+
+# ---- graph ingest / embedding export (host side) -------------------------------------------------------
+class ParseError(DataError):
+    """parse_error: malformed input text; `line` is the 1-based offending line (errors.hpp:10-19)."""
+
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
+def _take_graph(L, gc):
+    try:
+        src = np.ctypeslib.as_array(gc.src, (gc.m,)).copy()
+        dst = np.ctypeslib.as_array(gc.dst, (gc.m,)).copy()
+        labels = np.ctypeslib.as_array(gc.raw_labels, (gc.n,)).copy() if gc.raw_labels else None
+        return Graph(gc.n, src, dst), labels
+    finally:
+        L.gempe_graph_free(C.byref(gc))
+
+
+def _raise_io(L, rc, line):
+    msg = L.gempe_last_error(None).decode(errors="replace")
+    if rc == _capi.ERR_DATA and line:
+        raise ParseError(msg, line)
+    _raise(rc, msg)
+
+
+def load_edge_list(text) -> tuple:
+    """load_edge_list (graph.cpp:75-133).  Returns (Graph, raw_labels)."""
+    L = _capi.load()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    gc, line = _capi.GraphC(), C.c_uint64()
+    rc = L.gempe_parse_edge_list(data, len(data), C.byref(gc), C.byref(line))
+    if rc != _capi.OK:
+        _raise_io(L, rc, line.value)
+    return _take_graph(L, gc)
+
+
+def load_graph_snapshot(data: bytes) -> Graph:
+    L = _capi.load()
+    gc = _capi.GraphC()
+    rc = L.gempe_parse_graph_snapshot(bytes(data), len(data), C.byref(gc))
+    if rc != _capi.OK:
+        _raise_io(L, rc, 0)
+    return _take_graph(L, gc)[0]
+
+
+def load_graph_file(path: str) -> tuple:
+    L = _capi.load()
+    gc, line = _capi.GraphC(), C.c_uint64()
+    rc = L.gempe_load_graph_file(path.encode(), C.byref(gc), C.byref(line))
+    if rc != _capi.OK:
+        _raise_io(L, rc, line.value)
+    return _take_graph(L, gc)
+
+
+def save_graph_snapshot(path: str, g: Graph):
+    L = _capi.load()
+    rc = L.gempe_write_graph_snapshot(path.encode(), g.n, g.edge_count(), _capi.ptr(g.src), _capi.ptr(g.dst))
+    if rc != _capi.OK:
+        _raise_io(L, rc, 0)
+
+
+def write_embedding_tsv(path: str, coords: np.ndarray, labels=None, perm_forward=None):
+    """write_embedding_tsv (io.cpp:17-46)."""
+    L = _capi.load()
+    x = np.ascontiguousarray(coords, np.float32)
+    lab = None if labels is None else np.ascontiguousarray(labels, np.uint64)
+    perm = None if perm_forward is None else np.ascontiguousarray(perm_forward, np.uint32)
+    if lab is not None and lab.size != x.shape[0]:
+        raise DataError("label count does not match embedding rows")
+    rc = L.gempe_write_embedding_tsv(path.encode(), x.shape[0], x.shape[1], _capi.ptr(x), _capi.ptr(lab), _capi.ptr(perm))
+    if rc != _capi.OK:
+        _raise_io(L, rc, 0)

@@ -175,6 +175,47 @@ def main():
                      "embedding": [repr(float(v)) for v in res["embedding"].ravel()]})
     dump("embed_runs.json", runs)
 
+    # ---- text formats: edge-list canonicalisation, snapshot bytes, TSV export ------------------------------
+    import base64
+    fm = {"edge_lists": [], "tsv": [], "snapshots": []}
+    texts = ["0 1\n1 2\n", "0 0\n0 1\n1 0\n", "5 9\n9 7\n", "# header\n% more\n\n   \n0 1\n", "0 1\n2 x\n", "0 1 2\n",
+             "7\n", "-1 2\n", "3 3\n", "# only comments\n", "5 9\n9 7\n7 5\n1 5\n", "10\t20\r\n20 30\r\n30   10", "",
+             "18446744073709551615 1\n18446744073709551616 2\n", "1 2\n\n\n2 1\n3 1 \n  4\t3\n", "1 2\n 3 4 x\n",
+             "9 8\n8 9\n9 9\n7 8", "0 1\x00\n", "4 5\n#6 7\n %8 9\n6 7 \v\f\n"]
+    soup = Stream(1, 99)
+    for _ in range(40):
+        ln = int(soup.below(1, 120)[0])
+        texts.append(bytes(int(v) for v in soup.below(ln, 256)).decode("latin1"))
+    for _ in range(40):  # digit-rich soup that often parses
+        ln = int(soup.below(1, 80)[0])
+        alphabet = "0123456789  \n\n\t#%x"
+        texts.append("".join(alphabet[int(v)] for v in soup.below(ln, len(alphabet))))
+    for t in texts:
+        raw = t.encode("latin1")
+        r = ref.load_edge_list(raw)
+        entry = {"text_b64": base64.b64encode(raw).decode(), "rc": r["rc"]}
+        if r["rc"] == 0:
+            entry.update(n=r["n"], src=[int(v) for v in r["src"]], dst=[int(v) for v in r["dst"]],
+                         labels=[str(int(v)) for v in r["labels"]])
+        else:
+            entry.update(line=r.get("line", 0), error=r["error"])
+        fm["edge_lists"].append(entry)
+    emb = ref.init_embedding(3, 2, 5)
+    fm["tsv"].append({"n": 3, "dim": 2, "bits": [int(v) for v in emb.view(np.uint32).ravel()], "labels": ["42", "7", "100"],
+                      "perm": None, "text": ref.write_embedding_tsv(emb, [42, 7, 100]).decode()})
+    emb = ref.init_embedding(4, 1, 9)
+    fm["tsv"].append({"n": 4, "dim": 1, "bits": [int(v) for v in emb.view(np.uint32).ravel()], "labels": None,
+                      "perm": [2, 3, 0, 1], "text": ref.write_embedding_tsv(emb, None, [2, 3, 0, 1]).decode()})
+    emb = (ref.init_embedding(6, 5, 77) - 0.5) * np.float32(1e4)
+    emb[0, 0], emb[1, 1], emb[2, 2] = 0.0, 1e-7, -123456789.0
+    fm["tsv"].append({"n": 6, "dim": 5, "bits": [int(v) for v in emb.view(np.uint32).ravel()],
+                      "labels": ["9", "3", "1000000000000", "0", "5", "4"], "perm": [5, 4, 3, 2, 1, 0],
+                      "text": ref.write_embedding_tsv(emb, [9, 3, 10**12, 0, 5, 4], [5, 4, 3, 2, 1, 0]).decode()})
+    n_, s_, d_ = er_graph(20, 40, 3)
+    fm["snapshots"].append({"n": n_, "src": [int(v) for v in s_], "dst": [int(v) for v in d_],
+                            "bytes_b64": base64.b64encode(ref.save_graph_snapshot(n_, s_, d_)).decode()})
+    dump("formats.json", fm)
+
 
 if __name__ == "__main__":
     main()
