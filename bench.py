@@ -269,17 +269,17 @@ def main():
         ctx.get_coords(x_np)
         steps_e2e = max(1, args.e2e_steps)
         t_e2e = []
+        x_out_host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+        bufs = [x_np, x_out_host.numpy()]
         for s in range(steps_e2e + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            ctx.set_coords(x_np)
-            ctx.iterate(mu, sigma, eng.iter + s)
-            ctx.get_coords(x_np)
+            ctx.step_host(bufs[s % 2], bufs[(s + 1) % 2], mu, sigma, eng.iter + s)
             t_e2e.append(time.perf_counter() - t0)
         e2e_s = float(np.median(t_e2e[1:]))
         line["e2e"] = {"value": pair_terms / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * dim * 4),
                        "d2h_bytes_per_step": int(n * dim * 4 + 2 * 512 * 8), "ms_per_step": e2e_s * 1e3,
-                       "call": "gempe_set_coords + gempe_iterate + gempe_get_coords (pinned host buffers)"}
+                       "call": "gempe_step_host: X_t in, round, X_{t+1} + tallies out (pinned host buffers, copies overlapped)"}
         if not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_reference_arm(n, src, dst, dim, args.cpu_seconds)

@@ -112,6 +112,13 @@ int gempe_relabel(gempe_ctx* ctx, uint64_t relabel_seed);
 int gempe_iterate(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index,
                   uint64_t* hist_edge, uint64_t* hist_nonedge);
 
+/* The round as a pure function on HOST buffers (what a caller that keeps the coordinates on the host pays):
+ * x_in (X_t, n*dim, WORK indexing, ideally pinned) is copied in while the sampling passes run, the gradient/update
+ * kernel runs in slices, and each finished slice of X_{t+1} is copied to x_out while the next slice is computed.
+ * Equivalent to gempe_set_coords + gempe_iterate + gempe_get_coords.  Unsharded contexts only. */
+int gempe_step_host(gempe_ctx* ctx, const float* x_in, float* x_out, double mu, double sigma, uint64_t iter_index,
+                    uint64_t* hist_edge, uint64_t* hist_nonedge);
+
 /* Same round, enqueue-only: no host synchronisation.  gempe_sync waits, checks the status word and
  * returns the tallies of the LAST round. */
 int gempe_iterate_async(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index);
@@ -217,6 +224,8 @@ typedef struct gempe_iteration_config { /* IterationConfig, engine.hpp:29-38 */
   uint32_t negatives;
   int32_t device;
   int32_t host_sigma;         /* 1 = run the sigma search on the host (hostmath.cpp) instead of the device kernel */
+  int32_t deterministic;      /* 1 = sorted sample buckets: byte-identical results run to run (README.md:41-44 of the
+                                 reference promises this for fixed input, seed, workers and lanes) */
 } gempe_iteration_config;
 
 typedef struct gempe_embed_result { /* EmbedResult, engine.hpp:98-107 */

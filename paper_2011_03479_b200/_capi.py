@@ -24,7 +24,7 @@ SYMBOLS = [
     "gempe_default_options", "gempe_create", "gempe_destroy", "gempe_last_error", "gempe_is_degenerate",
     "gempe_hash_bits", "gempe_sample_slots", "gempe_pair_terms", "gempe_algorithmic_bytes",
     "gempe_get_work_graph", "gempe_set_coords", "gempe_get_coords", "gempe_init_coords", "gempe_relabel",
-    "gempe_iterate", "gempe_iterate_async", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
+    "gempe_iterate", "gempe_step_host", "gempe_iterate_async", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
     "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_probe",
     "gempe_sample", "gempe_set_stream", "gempe_device_coords", "gempe_row_stride", "gempe_padded_rows",
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_gather_chunk", "gempe_end_round", "gempe_elapsed_ms",
@@ -50,7 +50,7 @@ class IterationConfigC(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("lane_width", C.c_uint32), ("workers", C.c_uint32),
                 ("convergence_tol", C.c_double), ("convergence_window", C.c_int32), ("relabel_period", C.c_int32),
                 ("fast_math", C.c_int32), ("hash_bits", C.c_int32), ("neg_mode", C.c_int32),
-                ("negatives", C.c_uint32), ("device", C.c_int32), ("host_sigma", C.c_int32)]
+                ("negatives", C.c_uint32), ("device", C.c_int32), ("host_sigma", C.c_int32), ("deterministic", C.c_int32)]
 
 
 class GraphC(C.Structure):
@@ -104,6 +104,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_init_coords": (i32, [vp, i32, u64, dbl]),
         "gempe_relabel": (i32, [vp, u64]),
         "gempe_iterate": (i32, [vp, dbl, dbl, u64, vp, vp]),
+        "gempe_step_host": (i32, [vp, vp, vp, dbl, dbl, u64, vp, vp]),
         "gempe_iterate_async": (i32, [vp, dbl, dbl, u64]),
         "gempe_sync": (i32, [vp, vp, vp]),
         "gempe_set_sigma": (i32, [vp, dbl, dbl]),

@@ -141,6 +141,21 @@ void build_structures(gempe_ctx* c) {
     }
   }
   c->chunk_item_off[c->comm_chunks] = static_cast<std::uint32_t>(items.size());
+  // slices for the host-buffer pipeline: ~equal item counts, cut at vertex boundaries (a hub's slices stay together)
+  c->step_item_off.assign(1, 0);
+  c->step_vertex_off.assign(1, 0);
+  if (world == 1 && !items.empty()) {
+    constexpr std::uint32_t kSlices = 8;
+    for (std::uint32_t k = 1; k < kSlices; ++k) {
+      std::uint64_t at = static_cast<std::uint64_t>(items.size()) * k / kSlices;
+      while (at < items.size() && items[at].w != 0) ++at;  // first item of a vertex
+      if (at >= items.size() || at <= c->step_item_off.back()) continue;
+      c->step_item_off.push_back(static_cast<std::uint32_t>(at));
+      c->step_vertex_off.push_back(items[at].x);
+    }
+    c->step_item_off.push_back(static_cast<std::uint32_t>(items.size()));
+    c->step_vertex_off.push_back(n);
+  }
 
   c->rowptr.upload(rowptr);
   c->nbr.upload(nbr);
@@ -332,6 +347,8 @@ using namespace gempe;
 gempe_ctx::~gempe_ctx() {
   for (cudaEvent_t e : events) cudaEventDestroy(e);
   if (pinned) cudaFreeHost(pinned);
+  for (cudaEvent_t e : step_events) cudaEventDestroy(e);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 
@@ -624,6 +641,50 @@ int gempe_iterate_auto(gempe_ctx* c, std::uint64_t iter_index, double* sigma, do
 }
 
 void* gempe_device_tallies(gempe_ctx* c) { return c->hist.get(); }
+
+int gempe_step_host(gempe_ctx* c, const float* x_in, float* x_out, double mu, double sigma, std::uint64_t iter_index,
+                    std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (c->opt.world != 1) throw config_error("gempe_step_host needs an unsharded context");
+    if (!x_in || !x_out) throw config_error("null coordinates");
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    if (!c->copy_stream) cuda_check(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+    const std::size_t slices = c->step_item_off.size() - 1;
+    while (c->step_events.size() < slices + 2) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      c->step_events.push_back(e);
+    }
+    set_round_math(c, mu, sigma);
+    c->round_iter = iter_index;
+    const std::size_t host_pitch = c->dim * sizeof(float), dev_pitch = c->ld * sizeof(float);
+    // X_t in on the copy stream while the (X-independent) sampling passes run on the compute stream
+    cuda_check(cudaEventRecord(c->step_events[slices], c->stream), "event");  // orders after earlier work on X
+    cuda_check(cudaStreamWaitEvent(c->copy_stream, c->step_events[slices], 0), "wait");
+    cuda_check(cudaMemcpy2DAsync(c->x[c->cur].get(), dev_pitch, x_in, host_pitch, host_pitch, c->n, cudaMemcpyHostToDevice,
+                                 c->copy_stream), "X in");
+    cuda_check(cudaEventRecord(c->step_events[slices + 1], c->copy_stream), "event");
+    sampling_passes(c, iter_index);
+    cuda_check(cudaStreamWaitEvent(c->stream, c->step_events[slices + 1], 0), "wait");
+    // gradient + update slice by slice; a finished slice's rows leave while the next slice is computed
+    float* x_next = c->x[c->cur ^ 1].get();
+    for (std::size_t k = 0; k < slices; ++k) {
+      gather_items(c, c->step_item_off[k], c->step_item_off[k + 1]);
+      cuda_check(cudaEventRecord(c->step_events[k], c->stream), "event");
+      cuda_check(cudaStreamWaitEvent(c->copy_stream, c->step_events[k], 0), "wait");
+      const std::uint32_t v0 = c->step_vertex_off[k], v1 = c->step_vertex_off[k + 1];
+      if (v1 > v0) {
+        cuda_check(cudaMemcpy2DAsync(x_out + static_cast<std::size_t>(v0) * c->dim, host_pitch,
+                                     x_next + static_cast<std::size_t>(v0) * c->ld, dev_pitch, host_pitch, v1 - v0,
+                                     cudaMemcpyDeviceToHost, c->copy_stream), "X out");
+      }
+    }
+    c->cur ^= 1;
+    fetch_status(c, hist_edge, hist_nonedge);  // waits for the compute stream and checks the status word
+    cuda_check(cudaStreamSynchronize(c->copy_stream), "X out");
+  });
+}
 
 int gempe_elapsed_ms(gempe_ctx* c, float out3[3]) {
   return guarded(c, [&] {

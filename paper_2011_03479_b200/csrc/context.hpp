@@ -87,6 +87,11 @@ struct gempe_ctx {
   gempe::DeviceBuffer<uint2> records;
   gempe::DeviceBuffer<uint4> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
+  // gempe_step_host pipeline: item / vertex boundaries of the slices whose rows are copied out while later
+  // slices are still being computed (world == 1 only)
+  std::vector<std::uint32_t> step_item_off, step_vertex_off;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> step_events;
   gempe::DeviceBuffer<std::uint32_t> hub_first, hub_items, hub_arrived;
   gempe::DeviceBuffer<double> part_y, part_z;
   gempe::DeviceBuffer<unsigned long long> hist;

@@ -139,6 +139,7 @@ void gempe_default_iteration_config(gempe_iteration_config* cfg) {
   cfg->negatives = 0;
   cfg->device = 0;
   cfg->host_sigma = 0;
+  cfg->deterministic = 0;
 }
 
 int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
@@ -165,6 +166,7 @@ int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, co
   opt.negatives = cfg->negatives;
   opt.math = cfg->fast_math ? GEMPE_MATH_TABLES : GEMPE_MATH_EXACT;
   opt.device = cfg->device;
+  opt.deterministic = cfg->deterministic;
   int rc = GEMPE_ERR_CONFIG;
   if (!bad) rc = gempe_create(&e->ctx, n, m, src, dst, &opt);
   if (bad) set_create_error(bad);

@@ -87,6 +87,7 @@ class IterationConfig:
     negatives: int = 0
     device: int = 0
     host_sigma: bool = False  # True: sigma search on the host instead of the device kernel
+    deterministic: bool = False  # True: sorted sample buckets, byte-identical results run to run
 
 
 @dataclass
@@ -218,6 +219,17 @@ class Context:
         self._check(self._L.gempe_iterate(self._h, mu, sigma, iter_index, _capi.ptr(he), _capi.ptr(hn)))
         return he, hn
 
+    def step_host(self, x_in: np.ndarray, x_out: np.ndarray, mu: float, sigma: float, iter_index: int):
+        """The round on host buffers (X_t in, X_{t+1} out), copies overlapped with the kernels."""
+        if x_in.dtype != np.float32 or x_out.dtype != np.float32 or x_in.shape != (self.n, self.dim) \
+                or x_out.shape != (self.n, self.dim) or not x_in.flags.c_contiguous or not x_out.flags.c_contiguous:
+            raise ConfigError(f"coordinates must be C-contiguous float32 {self.n}x{self.dim}")
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        self._check(self._L.gempe_step_host(self._h, _capi.ptr(x_in), _capi.ptr(x_out), mu, sigma, iter_index,
+                                            _capi.ptr(he), _capi.ptr(hn)))
+        return he, hn
+
     def iterate_async(self, mu: float, sigma: float, iter_index: int):
         self._check(self._L.gempe_iterate_async(self._h, mu, sigma, iter_index))
 
@@ -319,6 +331,7 @@ class EmbeddingEngine:
             raise ConfigError("hash table bits must be in [1,31]")
         c.neg_mode, c.negatives, c.device = cfg.neg_mode, cfg.negatives, cfg.device
         c.host_sigma = int(cfg.host_sigma)
+        c.deterministic = int(cfg.deterministic)
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         self._pe_trace = []
         rc = self._L.gempe_engine_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,

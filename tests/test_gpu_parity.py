@@ -175,7 +175,8 @@ def test_golden_embed_runs(G):
 
 # ------------------------------------------------------------------------------------- per-round parity
 
-KERNELS = {"batched": dict(), "batched_precise": dict(precise_distance=True), "rowwise": dict(kernel_variant=1)}
+KERNELS = {"batched": dict(), "batched_precise": dict(precise_distance=True), "rowwise": dict(kernel_variant=1),
+           "cp_async": dict(kernel_variant=10)}  # variant 10 only differs from the default for 16 < ld <= 128
 
 
 @pytest.mark.parametrize("kernel", list(KERNELS))
@@ -449,9 +450,43 @@ def test_engine_host_and_device_sigma_paths_agree(G):
     n, src, dst = er_graph(500, 2500, 12)
     runs = []
     for host in (False, True):
-        eng = G.EmbeddingEngine(G.Graph(n, src, dst), 2, G.IterationConfig(host_sigma=host), 3)
+        eng = G.EmbeddingEngine(G.Graph(n, src, dst), 2, G.IterationConfig(host_sigma=host, deterministic=True), 3)
         trace = [eng.run_single_iteration() for _ in range(6)]
         runs.append(([t.sigma for t in trace], [t.pe_estimate for t in trace], eng.work_coords()))
         eng.close()
     assert np.allclose(runs[0][0], runs[1][0], rtol=1e-6) and np.allclose(runs[0][1], runs[1][1], rtol=1e-6)
     assert rel_l2(runs[0][2], runs[1][2]) <= 1e-4
+
+
+@pytest.mark.parametrize("dim,mode,k", [(2, 0, 0), (100, 1, 4), (128, 1, 6)])
+def test_step_host_equals_set_iterate_get(G, dim, mode, k):
+    """gempe_step_host (copies overlapped with the sliced kernel) is the same function as set_coords + iterate +
+    get_coords: bit-identical with sorted buckets, hubs included."""
+    n, src, dst = star_plus_ring(3000, hubs=3)
+    a = G.Context(G.Graph(n, src, dst), dim, 7, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+    b = G.Context(G.Graph(n, src, dst), dim, 7, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+    x = a.get_coords()
+    out = np.empty_like(x)
+    for it in range(3):
+        b.set_coords(x)
+        he_b, hn_b = b.iterate(1.5, 1.0 + 0.2 * it, it)
+        want = b.get_coords()
+        he_a, hn_a = a.step_host(x, out, 1.5, 1.0 + 0.2 * it, it)
+        assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(he_a, he_b) and np.array_equal(hn_a, hn_b)
+        x = out.copy()
+    a.close()
+    b.close()
+
+
+def test_engine_is_byte_deterministic_when_asked(G):
+    """The reference promises byte-identical output for a fixed (input, seed, workers, lanes); with sorted sample
+    buckets the GPU engine gives the same guarantee."""
+    n, src, dst = er_graph(700, 3000, 2)
+    outs = []
+    for _ in range(3):
+        res = G.embed(G.Graph(n, src, dst), 3, G.IterationConfig(max_iters=15, deterministic=True), 8)
+        outs.append((res.embedding, res.pe_trace, res.final_sigma, res.iterations))
+    for o in outs[1:]:
+        assert np.array_equal(o[0].view(np.uint32), outs[0][0].view(np.uint32))
+        assert np.array_equal(o[1], outs[0][1]) and o[2] == outs[0][2] and o[3] == outs[0][3]
