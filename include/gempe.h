@@ -61,7 +61,7 @@ typedef struct gempe_options {
                              (src/engine.cpp:161-163); 0 = ids are used as work ids */
   int32_t device;         /* CUDA device ordinal */
   int32_t rank, world;    /* vertex sharding, one process per GPU; world = 1 for a single GPU */
-  int32_t comm_chunks;    /* all-gather pipeline depth (>= 1; forced to 1 when world == 1) */
+  int32_t comm_chunks;    /* all-gather pipeline depth (>= 1): ownership blocks per rank */
   uint32_t chunk_entries; /* hub split: max adjacency entries per work item (0 = default) */
   int32_t deterministic;  /* 1 = sort incoming-sample buckets so the fp32 sums are run-to-run identical */
   int32_t precise_distance; /* 1 = pair_distance exactly as src/engine.cpp:45-52 (double differences); 0 = fp32

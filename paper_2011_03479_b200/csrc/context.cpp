@@ -390,7 +390,6 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->dim = opt->dim;
     c->ld = row_stride_for(opt->dim);
     c->degenerate = n <= 1 || m == 0;  // engine.cpp:159
-    if (c->opt.world == 1) c->opt.comm_chunks = 1;
     c->comm_chunks = static_cast<std::uint32_t>(c->opt.comm_chunks);
     const std::uint64_t blocks = static_cast<std::uint64_t>(c->opt.world) * c->comm_chunks;
     c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);

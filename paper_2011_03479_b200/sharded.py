@@ -92,9 +92,12 @@ class ShardedEngine:
     """Drives rounds over a process group.  `ops` needs x_next(), begin_round, gather_chunk, end_round,
     tallies(); `stream` (optional) is the CUDA stream the ops launch on."""
 
-    def __init__(self, ops, n: int, m: int, world: int, rank: int, comm_chunks: int, group=None, stream=None):
+    def __init__(self, ops, n: int, m: int, world: int, rank: int, comm_chunks: int, group=None, stream=None,
+                 force_collectives: bool = False):
         self.ops, self.n, self.m, self.world, self.rank, self.chunks = ops, n, m, world, rank, comm_chunks
         self.group, self.stream = group, stream
+        # issue the collectives even for a single rank (exercises the NCCL plumbing on one GPU)
+        self.collective = world > 1 or force_collectives
         self.block_rows, self.rows = block_layout(n, world, comm_chunks)
         self.mu, self.sigma, self.iter = 1.5, 1.0, 0
         self.pe_trace: List[float] = []
@@ -117,7 +120,7 @@ class ShardedEngine:
             span = self.world * self.block_rows
             for c in range(self.chunks):
                 self.ops.gather_chunk(c)
-                if self.world > 1:
+                if self.collective:
                     region = x_next[c * span:(c + 1) * span]
                     mine = region[self.rank * self.block_rows:(self.rank + 1) * self.block_rows]
                     self._pending.append(dist.all_gather_into_tensor(region, mine, group=self.group, async_op=True))
@@ -129,7 +132,7 @@ class ShardedEngine:
         with ctx:
             self._wait_pending()
             t = self.ops.tallies()
-            if self.world > 1:
+            if self.collective:
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         t = t.cpu().numpy().astype(np.uint64)
         return t[:HIST], t[HIST:]
@@ -146,7 +149,7 @@ class ShardedEngine:
             ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
             with ctx:
                 self._wait_pending()
-                if self.world > 1:
+                if self.collective:
                     dist.all_reduce(self.ops.tallies_tensor(), op=dist.ReduceOp.SUM, group=self.group)
                 self.ops.sigma_update()
             self.sigma, pe, _ = self.ops.sigma_state()
@@ -174,11 +177,12 @@ class _Null:
 
 
 def make_cuda_engine(g: Graph, dim: int, seed: int, *, comm_chunks: int = 4, group=None, device: Optional[int] = None,
-                     **ctx_kw) -> ShardedEngine:
+                     force_collectives: bool = False, **ctx_kw) -> ShardedEngine:
     """One rank of a sharded engine over the default (NCCL) process group; world 1 without a group."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     device = torch.cuda.current_device() if device is None else device
-    chunks = comm_chunks if world > 1 else 1
+    chunks = comm_chunks if (world > 1 or force_collectives) else 1
     ops = CudaShardOps(g, dim, seed, rank, world, chunks, device, **ctx_kw)
-    return ShardedEngine(ops, g.n, g.edge_count(), world, rank, chunks, group=group, stream=ops.stream)
+    return ShardedEngine(ops, g.n, g.edge_count(), world, rank, chunks, group=group, stream=ops.stream,
+                         force_collectives=force_collectives)

@@ -57,3 +57,43 @@ def test_rank_contexts_reproduce_the_single_gpu_round(world, chunks, mode, k, bu
             sigma *= 1.3
         for c in ranks + [single]:
             c.close()
+
+
+def test_nccl_plumbing_on_a_single_rank_group():
+    """Real NCCL on one GPU: a 1-rank process group with the collectives forced on, three comm chunks.  Exercises
+    the device-pointer tensor views, the in-place all_gather_into_tensor per chunk, the device-side tally all-reduce
+    and the device sigma search; the result must equal the plain engine bit for bit."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import paper_2011_03479_b200 as G
+    from paper_2011_03479_b200 import sharded
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, src, dst = er_graph(2003, 12000, 4)
+        g = G.Graph(n, src, dst)
+        eng = sharded.make_cuda_engine(g, 64, 5, comm_chunks=3, device=0, force_collectives=True, neg_mode=1,
+                                       negatives=6, deterministic=True)
+        assert eng.chunks == 3 and eng.collective
+        plain = G.Context(g, 64, 5, neg_mode=1, negatives=6, deterministic=True)
+        plain.set_sigma(1.5, 1.0)
+        for it in range(3):
+            pe, sigma = eng.run_single_iteration()
+            s_want, pe_want, _, _, _ = plain.iterate_auto(it)
+            assert sigma == s_want and pe == pe_want
+        assert np.array_equal(eng.ops.ctx.get_coords().view(np.uint32), plain.get_coords().view(np.uint32))
+        # host-sigma path of the driver as well (tallies() + all_reduce + host search)
+        eng.round_async(1.5, eng.sigma, eng.iter)
+        he, hn = eng.finish_round()
+        he_w, hn_w = plain.iterate(1.5, eng.sigma, eng.iter)
+        assert np.array_equal(he, he_w) and np.array_equal(hn, hn_w)
+    finally:
+        dist.destroy_process_group()
