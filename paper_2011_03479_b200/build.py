@@ -23,7 +23,7 @@ CXX_SOURCES = ["hostmath.cpp", "context.cpp", "engine.cpp", "formats.cpp"]
 HEADERS = ["kernels.hpp", "context.hpp", "hostmath.hpp", "device_fns.cuh", os.path.join(ROOT, "include", "gempe.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+              "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"] + os.environ.get("GEMPE_NVCC_EXTRA", "").split()
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", f"-I{CUDA_HOME}/include"]
 
 

@@ -828,7 +828,16 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 // FULL            : ld == LPR*NV*VEC, no column predicates.
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+#ifndef GEMPE_PREFETCH_LEVEL
+#define GEMPE_PREFETCH_LEVEL 2
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+#if GEMPE_PREFETCH_LEVEL == 1
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
+}
 
 
 template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
@@ -1893,11 +1902,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   if (variant >= 10 && ld > 16 && ld <= 128) {  // cp.async pipeline (experimental: register pressure caps it at 8 warps/SM)
     if (ld <= 32) gather_async_go<8, 4>(a, lo, hi, precise, stream);
     else if (ld <= 64) gather_async_go<16, 8>(a, lo, hi, precise, stream);
-    else if (variant == 10) gather_async_go<32, 16, 4, 2>(a, lo, hi, precise, stream);
-    else if (variant == 11) gather_async_go<32, 16, 5, 2>(a, lo, hi, precise, stream);
-    else if (variant == 12) gather_async_go<32, 16, 6, 2>(a, lo, hi, precise, stream);
-    else if (variant == 13) gather_async_go<32, 16, 2, 6>(a, lo, hi, precise, stream);
-    else gather_async_go<32, 16, 4, 3>(a, lo, hi, precise, stream);
+    else gather_async_go<32, 16, 4, 2>(a, lo, hi, precise, stream);  // 8 warps/SM: 204 registers
     return 1;
   }
   //                          LPR NV VEC TB U
@@ -1907,20 +1912,8 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 4>(a, lo, hi, precise, stream);
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
-  else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1>(a, lo, hi, precise, stream);
-  else if (ld <= 128) {
-    switch (variant) {  // experimental launch shapes for the d=128 row (tools/profile_round.py --variant)
-      case 2: gather_batched_go<32, 1, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream); break;
-      case 3: gather_batched_go<32, 1, 4, 8, 1, 128, 5>(a, lo, hi, precise, stream); break;
-      case 4: gather_batched_go<32, 1, 4, 16, 1, 256, 1>(a, lo, hi, precise, stream); break;
-      case 5: gather_batched_go<32, 1, 4, 16, 1, 128, 3>(a, lo, hi, precise, stream); break;
-      case 6: gather_batched_go<32, 1, 4, 4, 1, 128, 6>(a, lo, hi, precise, stream); break;
-      case 7: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream); break;
-      case 8: gather_batched_go<32, 1, 4, 8, 1>(a, lo, hi, precise, stream); break;
-      case 9:  // register-resident batched kernel (the pre-pipeline default)
-      default: gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
-    }
-  }
+  else if (ld <= 64) gather_batched_go<16, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);  // 16 rows/warp, 16 warps/SM
   else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);

@@ -26,8 +26,11 @@ import torch  # noqa: E402
 n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config, device=torch.device('cuda', 0))
 torch.cuda.empty_cache()
 mode = P.NEG_PER_VERTEX_K if a.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
+import time  # noqa: E402
+_t0 = time.perf_counter()
 ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode == P.NEG_PER_VERTEX_K else 0,
                 precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries, bucket_mode=a.bucket_mode)
+print(f'context construction {time.perf_counter() - _t0:.2f} s (n={n}, m={len(src)})')
 ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
 sigma = a.sigma
 for it in range(2):
