@@ -394,7 +394,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     const std::uint64_t blocks = static_cast<std::uint64_t>(c->opt.world) * c->comm_chunks;
     c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);
     c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
-    c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : std::max(128u, 4096u / lanes_per_row(c->ld));
+    // hub split: d <= 4 runs one thread per item (64 list positions bound the divergence), wider rows one warp per item
+    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 64u : std::max(128u, 4096u / lanes_per_row(c->ld));
+    c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : default_chunk;
     cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned), (4 + 2 * kBins) * sizeof(unsigned long long),

@@ -1199,6 +1199,169 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   }
 }
 
+// ---------------------------------------------------------------------------------- gather, one thread per work item
+//
+// d <= 4 (graph drawing): a row is one 4..16-byte vector, so a whole work item fits one thread -- 32 different
+// vertices per warp keep 4 x 32 independent row gathers in flight, and there is no warp-serial latency chain per
+// item.  Same arithmetic and the same hub protocol as gather_batched_kernel; items are capped at 64 list
+// positions (context.cpp) to bound divergence on hubs.
+template <int VEC, bool PRECISE>
+__global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArgs a, std::uint32_t item_lo,
+                                                                 std::uint32_t item_hi) {
+  constexpr int kInflight = 4;
+  __shared__ unsigned int sh_hist[2 * kBins];
+  using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
+  __shared__ tab_t sh_tab;
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
+  for (int i = threadIdx.x; i < 65; i += kThreads) {
+    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
+    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
+  }
+  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;
+  const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
+                      static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
+  __syncthreads();
+
+  const std::uint32_t item = item_lo + blockIdx.x * kThreads + threadIdx.x;
+  if (item < item_hi) {
+    const uint4 it = __ldg(a.items + item);
+    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
+    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
+    const bool first = begin == row_lo;
+    const std::uint32_t lenA = min(begin + a.chunk_entries, row_hi) - begin;
+    std::uint32_t offB = begin, lenB = lenA;
+    if (a.neg_mode != 0) {
+      offB = u * a.k;
+      lenB = first ? a.k : 0u;
+    }
+    std::uint32_t offC = 0, lenC = 0;
+    if (first) {
+      offC = __ldg(a.in_off + u);
+      lenC = __ldg(a.in_off + u + 1) - offC;
+    }
+    const std::uint32_t endB = lenA + lenB, total = endB + lenC;
+    const std::uint32_t ld = a.ld;
+
+    float xu[VEC], y[VEC];
+    load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld, xu);
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) y[c] = 0.0f;
+    float zacc = 0.0f;
+
+    for (std::uint32_t base = 0; base < total; base += kInflight) {
+      std::uint32_t other[kInflight];
+      float xv[kInflight][VEC];
+#pragma unroll
+      for (int q = 0; q < kInflight; ++q) {
+        const std::uint32_t e = base + q;
+        other[q] = u;
+        if (e < total) {
+          other[q] = __ldg(e < lenA ? a.nbr + begin + e : (e < endB ? a.neg_own + offB + (e - lenA) : a.in_anchor + offC + (e - endB)));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kInflight; ++q) load_row<VEC>(a.x_cur + static_cast<std::size_t>(other[q]) * ld, xv[q]);
+#pragma unroll
+      for (int q = 0; q < kInflight; ++q) {
+        const std::uint32_t e = base + q;
+        if (e >= total) break;
+        const bool is_edge = e < lenA;
+        const bool tally = is_edge ? u < other[q] : e < endB;
+        float diff[VEC];
+        double exact2 = 0.0;
+        float d2 = 0.0f;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          diff[c] = xu[c] - xv[q][c];
+          d2 = fmaf(diff[c], diff[c], d2);
+          const double dd = static_cast<double>(xu[c]) - static_cast<double>(xv[q][c]);
+          exact2 = fma(dd, dd, exact2);  // pair_distance (engine.cpp:45-52); dead code in the fast path unless needed below
+        }
+        float wf = 0.0f, sf = 0.0f;
+        int bin;
+        if constexpr (PRECISE) {
+          const double delta = sqrt(exact2);
+          bin = static_cast<int>(delta / 12.0 * 512.0);
+          pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
+        } else {
+          float delta = sqrtf(d2);
+          const float pos = delta * (512.0f / 12.0f);
+          const float frac = pos - floorf(pos);
+          const float tol = 4e-6f * pos + 1e-9f;
+          bin = static_cast<int>(pos);
+          if (tally && pos < 513.0f && (frac < tol || frac > 1.0f - tol)) {  // exact tally near a bin edge
+            const double ex = sqrt(exact2);
+            bin = static_cast<int>(ex / 12.0 * 512.0);
+            delta = static_cast<float>(ex);
+          }
+          pair_terms_f(delta, is_edge, mf, rm.exact, sh_tab, wf, sf);
+        }
+        if (tally) {
+          bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
+          atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + bin], 1u);
+        }
+        zacc += wf;
+        const float coef = wf * (sf - 1.0f);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) y[c] = fmaf(coef, diff[c], y[c]);
+      }
+    }
+
+    double zs = static_cast<double>(zacc);
+    double ys[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) ys[c] = fma(zs, static_cast<double>(xu[c]), static_cast<double>(y[c]));
+    bool finalize = true;
+    if (hub != kNoHub) {
+      const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
+      const std::uint32_t slot = p0 + it.w;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + c] = ys[c];
+      a.part_z[slot] = zs;
+      __threadfence();
+      finalize = atomicAdd(a.hub_arrived + hub, 1u) == q - 1;
+      if (finalize) {  // last slice of the hub: consolidate the partials in slot order
+        __threadfence();
+        zs = 0.0;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) ys[c] = 0.0;
+        for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
+          zs += __ldcg(a.part_z + sl);
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) ys[c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + c);
+        }
+        a.hub_arrived[hub] = 0;
+      }
+    }
+    if (finalize) {
+      bool bad = false;
+      float out[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        out[c] = xu[c];
+        if (zs > 0.0) {
+          out[c] = static_cast<float>(ys[c] / zs);
+          bad |= !isfinite(out[c]);
+        }
+      }
+      store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld, out);
+      if (a.cap_y) {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c)
+          if (static_cast<std::uint32_t>(c) < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + c] = ys[c];
+      }
+      if (a.cap_z) a.cap_z[u] = zs;
+      if (bad) atomicOr(a.status + kStatNonFinite, 1u);
+    }
+  }
+
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
+    const unsigned int c = sh_hist[i];
+    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
+  }
+}
+
 // ---------------------------------------------------------------------------------- gather, cp.async pipeline
 //
 // The batched gather with the row loads decoupled from the arithmetic, for 16 < ld <= 128 (rows of 128..512
@@ -1903,6 +2066,20 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
     if (ld <= 32) gather_async_go<8, 4>(a, lo, hi, precise, stream);
     else if (ld <= 64) gather_async_go<16, 8>(a, lo, hi, precise, stream);
     else gather_async_go<32, 16, 4, 2>(a, lo, hi, precise, stream);  // 8 warps/SM: 204 registers
+    return 1;
+  }
+  if (ld <= 4 && variant != 2) {  // one thread per work item (variant 2 keeps the warp-per-item kernel for A/B runs)
+    const unsigned blocks = blocks_for(hi - lo, kThreads);
+    if (ld == 1) {
+      if (precise) gather_thread_kernel<1, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+      else gather_thread_kernel<1, false><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+    } else if (ld == 2) {
+      if (precise) gather_thread_kernel<2, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+      else gather_thread_kernel<2, false><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+    } else {
+      if (precise) gather_thread_kernel<4, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+      else gather_thread_kernel<4, false><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
+    }
     return 1;
   }
   //                          LPR NV VEC TB U
