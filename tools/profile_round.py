@@ -20,6 +20,7 @@ ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--chunk-entries", type=int, default=0)
 ap.add_argument("--sigma", type=float, default=1.0)
 ap.add_argument("--bucket-mode", type=int, default=0)
+ap.add_argument("--warm-iters", type=int, default=0, help="real iterations (device sigma feedback) before timing")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -33,6 +34,11 @@ ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode
 print(f'context construction {time.perf_counter() - _t0:.2f} s (n={n}, m={len(src)})')
 ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
 sigma = a.sigma
+if a.warm_iters:
+    ctx.set_sigma(1.5, sigma)
+    for it in range(a.warm_iters):
+        sigma = ctx.iterate_auto(it)[0]
+    print('sigma after warm iterations', sigma)
 for it in range(2):
     ctx.iterate_async(1.5, sigma, it)
 ctx.sync(); ctx.elapsed_ms()
