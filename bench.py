@@ -244,7 +244,10 @@ def main():
                             "traffic": traffic, "kernel": "gather_kernel", "algorithmic_bytes": int(b_alg),
                             "kernel_ms": gath_ms / args.steps, "sampling_passes_ms": samp_ms / args.steps,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
-                            "draws_per_sample": p_bar}
+                            "draws_per_sample": p_bar,
+                            # the same launch on ncu's DRAM byte count (hub rows re-read from L2 are not HBM traffic)
+                            "achieved_dram": (traffic / gather_s / 1e9) if traffic else None,
+                            "frac_dram": (traffic / gather_s / 1e9 / peak) if traffic else None}
 
         # whole iterations with the device-resident sigma feedback (round + sigma search + PE estimate, no host sync)
         ctx.set_sigma(mu, sigma)

@@ -870,7 +870,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   bool act[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) act[j] = FULL || static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
-  const float* x_lane = a.x_cur + r * VEC;  // this lane's column block of every row
+  // this lane's column block of every row, and the row pitch in bytes (a compile-time constant when FULL, so the row
+  // address is one shift-add; otherwise one 32x32->64 multiply-add)
+  const char* x_lane = reinterpret_cast<const char*>(a.x_cur + r * VEC);
+  const std::uint32_t row_bytes = FULL ? static_cast<std::uint32_t>(ROW_BYTES_MAX) : ld * 4u;
+  auto row_ptr = [&](std::uint32_t row, int j) {
+    return reinterpret_cast<const float*>(x_lane + static_cast<std::uint64_t>(row) * row_bytes + LPR * j * VEC * 4);
+  };
 
   // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
   // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
@@ -920,7 +926,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       for (int j = 0; j < NV; ++j) {
 #pragma unroll
         for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
-        if (act[j]) load_row<VEC>(x_lane + static_cast<std::size_t>(u) * ld + LPR * j * VEC, xu[j]);
+        if (act[j]) load_row<VEC>(row_ptr(u, j), xu[j]);
       }
       float zacc = 0.0f;
 
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
 #pragma unroll
                 for (int c = 0; c < VEC; ++c) xv[s][t][j][c] = 0.0f;
               }
-              if (act[j]) load_row<VEC>(x_lane + static_cast<std::size_t>(src_row) * ld + LPR * j * VEC, xv[s][t][j]);
+              if (act[j]) load_row<VEC>(row_ptr(src_row, j), xv[s][t][j]);
             }
           }
         }
@@ -954,7 +960,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             const int slot = i * 32 + lane;
             const std::uint32_t row = __shfl_sync(kFull, nxt[0], slot / LINES);
             if (base + E + slot / LINES < total) {
-              prefetch_l2(a.x_cur + static_cast<std::size_t>(row) * ld + (slot % LINES) * 32);
+              prefetch_l2(reinterpret_cast<const char*>(a.x_cur) + static_cast<std::uint64_t>(row) * row_bytes + (slot % LINES) * 128);
             }
           }
         }
@@ -1830,14 +1836,36 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
     }
     return block_sum(v, scratch);
   };
-  // coarse geometric scan of the unfloored cost, then bisection on dF/dsigma inside the best cell
+  // coarse geometric scan of the unfloored cost (all 17 candidates in ONE pass: 17 partial sums per thread, reduced
+  // together), then bisection on dF/dsigma inside the best cell
   constexpr int kGrid = 17;
-  double grid[kGrid], best_cost = 0.0;
+  __shared__ double grid_scratch[kBins / 32][kGrid];
+  double grid[kGrid], cost[kGrid], best_cost = 0.0;
   int best = 0;
+#pragma unroll 1
   for (int i = 0; i < kGrid; ++i) {
     grid[i] = 1e-3 * pow(16.0 / 1e-3, static_cast<double>(i) / (kGrid - 1));
-    const double cost = total(grid[i], 0);
-    if (i == 0 || cost < best_cost) best_cost = cost, best = i;
+    double v = 0.0;
+    if (ec != 0.0) v += ec * cost_tail(mid, mu, grid[i], true);
+    if (nc != 0.0) v += nw * nc * cost_tail(mid, mu, grid[i], false);
+    cost[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < kGrid; ++i) {
+    double v = cost[i];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    cost[i] = v;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < kGrid; ++i) grid_scratch[threadIdx.x >> 5][i] = cost[i];
+  }
+  __syncthreads();
+  for (int i = 0; i < kGrid; ++i) {
+    double t = 0.0;
+    for (int w = 0; w < kBins / 32; ++w) t += grid_scratch[w][i];
+    if (i == 0 || t < best_cost) best_cost = t, best = i;
   }
   double sigma_opt = grid[best];
   double lo = grid[best > 0 ? best - 1 : 0], hi = grid[best < kGrid - 1 ? best + 1 : kGrid - 1];
