@@ -491,3 +491,61 @@ def test_engine_is_byte_deterministic_when_asked(G):
     for o in outs[1:]:
         assert np.array_equal(o[0].view(np.uint32), outs[0][0].view(np.uint32))
         assert np.array_equal(o[1], outs[0][1]) and o[2] == outs[0][2] and o[3] == outs[0][3]
+
+
+# ------------------------------------------------------------------------------------- odd inputs
+
+def test_duplicate_edges_both_orientations_and_tiny_graphs(G, oracle, golden_fastmath):
+    """The reference treats whatever Graph it is handed literally: duplicated / reversed duplicates are separate
+    edges (two terms, two tallies).  Also the smallest live graphs."""
+    dup = (6, np.array([0, 1, 0, 2, 3], np.uint32), np.array([1, 0, 1, 3, 2], np.uint32))
+    check_round(G, oracle, golden_fastmath, dup, 2, seed=5, iters=2)
+    check_round(G, oracle, golden_fastmath, dup, 128, seed=5, iters=2, neg_mode=1, k=3)
+    two = (3, np.array([0], np.uint32), np.array([2], np.uint32))
+    check_round(G, oracle, golden_fastmath, two, 1, seed=1, iters=3)
+    check_round(G, oracle, golden_fastmath, two, 64, seed=1, iters=3)
+
+
+def test_unrelabelled_context_and_hash_bits_extremes(G, oracle, golden_fastmath):
+    n, src, dst = er_graph(200, 600, 3)
+    for bits in (1, 14, 24):
+        ctx = G.Context(G.Graph(n, src, dst), 4, 2, relabel=False, hash_bits=bits)
+        ws, wd, to_work = ctx.work_graph()
+        assert np.array_equal(ws, src) and np.array_equal(wd, dst) and np.array_equal(to_work, np.arange(n))
+        table = oracle.hash_build(n, ws, wd, bits)
+        x = ctx.get_coords()
+        if bits == 1:  # a 2-cell table rejects every candidate: the retry cap must fire exactly as in the reference
+            with pytest.raises(G.NearCompleteGraphError):
+                ctx.iterate(1.5, 1.0, 0)
+        else:
+            he, hn = ctx.iterate(1.5, 1.0, 0)
+            want = oracle.iterate(n, ws, wd, x, 0, 0, 2, 0, 1.5, 1.0, golden_fastmath, table)
+            assert np.array_equal(he, want["hist_edge"]) and np.array_equal(hn, want["hist_nonedge"])
+            assert rel_l2(ctx.get_coords(), want["x_next"]) <= TOL
+        ctx.close()
+
+
+def test_zero_negatives_per_vertex_and_large_k(G, oracle, golden_fastmath):
+    n, src, dst = er_graph(150, 500, 8)
+    ctx = G.Context(G.Graph(n, src, dst), 8, 2, neg_mode=1, negatives=0)
+    he, hn = ctx.iterate(1.5, 1.0, 0)
+    assert he.sum() == len(src) and hn.sum() == 0 and ctx.sample_slots == 0
+    ctx.close()
+    check_round(G, oracle, golden_fastmath, (n, src, dst), 8, seed=2, neg_mode=1, k=70, iters=1)  # buckets > 32 entries
+
+
+def test_many_rounds_async_then_sync_matches_stepwise(G):
+    n, src, dst = er_graph(2000, 9000, 4)
+    a = G.Context(G.Graph(n, src, dst), 32, 6, neg_mode=1, negatives=5, deterministic=True)
+    b = G.Context(G.Graph(n, src, dst), 32, 6, neg_mode=1, negatives=5, deterministic=True)
+    for it in range(12):
+        a.iterate_async(1.5, 1.0, it)
+        he_b, hn_b = b.iterate(1.5, 1.0, it)
+    he_a, hn_a = a.sync()
+    tot, samp, gath = a.elapsed_ms()
+    assert tot > 0 and samp > 0 and gath > 0
+    assert np.array_equal(he_a, he_b) and np.array_equal(hn_a, hn_b)
+    assert np.array_equal(a.get_coords().view(np.uint32), b.get_coords().view(np.uint32))
+    assert a.kernel_launches > 12 * 5
+    a.close()
+    b.close()
