@@ -6,6 +6,9 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 
 namespace gempe {
@@ -17,6 +20,18 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 namespace {
+
+// GEMPE_TRACE=1 prints the construction phases' wall time to stderr
+struct PhaseTimer {
+  bool on = std::getenv("GEMPE_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gempe] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
 
 thread_local std::string g_create_error;
 
@@ -87,32 +102,61 @@ void build_structures(gempe_ctx* c) {
   const auto& src = c->work_src;
   const auto& dst = c->work_dst;
 
-  // both-direction CSR in edge order; eid_role = 2*e + role keys the PER_EDGE_2 sample streams
-  std::vector<std::uint32_t> rowptr(static_cast<std::size_t>(n) + 1, 0);
-  for (std::uint64_t e = 0; e < m; ++e) {
-    ++rowptr[src[e] + 1];
-    ++rowptr[dst[e] + 1];
-  }
-  for (std::uint32_t v = 0; v < n; ++v) rowptr[v + 1] += rowptr[v];
-  std::vector<std::uint32_t> nbr(2 * m), cursor(rowptr.begin(), rowptr.end() - 1);
+  PhaseTimer timer;
   const bool per_edge = c->opt.neg_mode == GEMPE_NEG_PER_EDGE_2;
-  std::vector<std::uint32_t> eid_role, csr_src;
-  if (per_edge) {
-    eid_role.resize(2 * m);
-    csr_src.resize(2 * m);
+  // the work edge arrays on the device: they feed the CSR build and the hash-set build
+  if (c->tmp_src.size() != m || m == 0) {
+    c->tmp_src.upload(src);
+    c->tmp_dst.upload(dst);
   }
-  for (std::uint64_t e = 0; e < m; ++e) {
-    const std::uint32_t p0 = cursor[src[e]]++, p1 = cursor[dst[e]]++;
-    nbr[p0] = dst[e];
-    nbr[p1] = src[e];
-    if (per_edge) {
-      eid_role[p0] = static_cast<std::uint32_t>(2 * e);
-      eid_role[p1] = static_cast<std::uint32_t>(2 * e + 1);
-      csr_src[p0] = src[e];
-      csr_src[p1] = dst[e];
+  timer.lap("edge arrays -> device");
+  // both-direction CSR; eid_role = 2*e + role keys the PER_EDGE_2 sample streams.  Default: built on the device
+  // (degree count, scan, atomic fill; the order inside a row is the arrival order).  When a reproducible order is
+  // asked for (opt.deterministic) the rows are filled on the host in edge order instead.
+  std::vector<std::uint32_t> rowptr(static_cast<std::size_t>(n) + 1, 0);
+  if (!c->opt.deterministic) {
+    c->rowptr.allocate(static_cast<std::size_t>(n) + 1, true);
+    c->nbr.allocate(2 * m);
+    c->eid_role.allocate(per_edge ? 2 * m : 0);
+    c->csr_src.allocate(per_edge ? 2 * m : 0);
+    DeviceBuffer<std::uint32_t> deg, scratch;
+    deg.allocate(n);
+    scratch.allocate((n + 4095) / 4096 + 2);
+    c->launches += launch_csr_build(c->tmp_src.get(), c->tmp_dst.get(), m, n, deg.get(), c->rowptr.get(), scratch.get(),
+                                    c->nbr.get(), c->eid_role.get(), c->csr_src.get(), c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "csr build");
+    cuda_check(cudaMemcpy(rowptr.data(), c->rowptr.get(), rowptr.size() * sizeof(std::uint32_t), cudaMemcpyDeviceToHost),
+               "rowptr D2H");
+  } else {
+    for (std::uint64_t e = 0; e < m; ++e) {
+      ++rowptr[src[e] + 1];
+      ++rowptr[dst[e] + 1];
     }
+    for (std::uint32_t v = 0; v < n; ++v) rowptr[v + 1] += rowptr[v];
+    std::vector<std::uint32_t> nbr(2 * m), cursor(rowptr.begin(), rowptr.end() - 1);
+    std::vector<std::uint32_t> eid_role, csr_src;
+    if (per_edge) {
+      eid_role.resize(2 * m);
+      csr_src.resize(2 * m);
+    }
+    for (std::uint64_t e = 0; e < m; ++e) {
+      const std::uint32_t p0 = cursor[src[e]]++, p1 = cursor[dst[e]]++;
+      nbr[p0] = dst[e];
+      nbr[p1] = src[e];
+      if (per_edge) {
+        eid_role[p0] = static_cast<std::uint32_t>(2 * e);
+        eid_role[p1] = static_cast<std::uint32_t>(2 * e + 1);
+        csr_src[p0] = src[e];
+        csr_src[p1] = dst[e];
+      }
+    }
+    c->rowptr.upload(rowptr);
+    c->nbr.upload(nbr);
+    c->eid_role.upload(eid_role);
+    c->csr_src.upload(csr_src);
   }
 
+  timer.lap(c->opt.deterministic ? "csr (host, edge order)" : "csr (device)");
   // work items: one per owned vertex, hubs split every chunk_entries adjacency positions
   std::vector<uint4> items;
   std::vector<std::uint32_t> hub_first, hub_items;
@@ -157,10 +201,7 @@ void build_structures(gempe_ctx* c) {
     c->step_vertex_off.push_back(n);
   }
 
-  c->rowptr.upload(rowptr);
-  c->nbr.upload(nbr);
-  c->eid_role.upload(eid_role);
-  c->csr_src.upload(csr_src);
+  timer.lap("work items (host)");
   c->items.upload(items);
   c->hub_first.upload(hub_first);
   c->hub_items.upload(hub_items);
@@ -200,22 +241,37 @@ void build_structures(gempe_ctx* c) {
   c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
   c->scan_scratch.allocate((n + 4095) / 4096 + 2);
 
+  timer.lap("uploads + allocations");
   // edge hash set, bit-packed (hash_set.cpp:9-34)
   c->hash_bits = auto_hash_bits(m, c->opt.hash_bits);
   const std::uint64_t cells = 1ull << c->hash_bits;
   c->hash_words.allocate(std::max<std::uint64_t>(1, cells / 32), true);
-  {
-    DeviceBuffer<std::uint32_t> d_src, d_dst;
-    d_src.upload(src);
-    d_dst.upload(dst);
-    c->launches += launch_hash_build(d_src.get(), d_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
-                                     c->hash_words.get(), c->stream);
-    cuda_check(cudaStreamSynchronize(c->stream), "hash build");
-  }
+  c->launches += launch_hash_build(c->tmp_src.get(), c->tmp_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
+                                   c->hash_words.get(), c->stream);
+  cuda_check(cudaStreamSynchronize(c->stream), "hash build");
+  c->tmp_src.release();
+  c->tmp_dst.release();
+  timer.lap("hash set (device)");
   if (c->capture) {
     c->cap_y.allocate(static_cast<std::size_t>(n) * c->dim, true);
     c->cap_z.allocate(n, true);
   }
+}
+
+// random_relabel applied to the work graph (graph.cpp:199-204) on the device; the relabelled arrays come back to the
+// host copies and stay on the device for build_structures.
+void apply_relabel(gempe_ctx* c, const std::vector<std::uint32_t>& fwd) {
+  if (c->m) {
+    c->tmp_src.upload(c->work_src);
+    c->tmp_dst.upload(c->work_dst);
+    DeviceBuffer<std::uint32_t> d_fwd;
+    d_fwd.upload(fwd);
+    c->launches += launch_relabel_apply(c->tmp_src.get(), c->tmp_dst.get(), c->m, d_fwd.get(), c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "relabel");
+    cuda_check(cudaMemcpy(c->work_src.data(), c->tmp_src.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "relabel D2H");
+    cuda_check(cudaMemcpy(c->work_dst.data(), c->tmp_dst.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "relabel D2H");
+  }
+  for (auto& v : c->to_work) v = fwd[v];
 }
 
 SampleArgs sample_args(gempe_ctx* c, std::uint64_t iter) {
@@ -376,7 +432,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
   *out = nullptr;
   gempe_ctx* c = nullptr;
   const int rc = guarded(nullptr, [&] {
+    PhaseTimer timer;
     validate(n, m, src, dst, *opt);
+    timer.lap("validate");
     int device_count = 0;
     const cudaError_t probe = cudaGetDeviceCount(&device_count);
     if (probe != cudaSuccess || device_count == 0) {
@@ -412,13 +470,12 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->work_dst.assign(dst, dst + m);
     c->to_work.resize(n);
     for (std::uint32_t v = 0; v < n; ++v) c->to_work[v] = v;
+    timer.lap("device buffers + graph copy");
     if (!c->degenerate) {
       if (opt->relabel) {  // engine.cpp:161-163 -> graph.cpp:182-206
-        const auto fwd = random_relabel_forward(n, mix_seed(opt->seed, 0xA11BE11));
-        for (auto& v : c->work_src) v = fwd[v];
-        for (auto& v : c->work_dst) v = fwd[v];
-        c->to_work = fwd;
+        apply_relabel(c, random_relabel_forward(n, mix_seed(opt->seed, 0xA11BE11)));
       }
+      timer.lap("relabel (host)");
       build_structures(c);
     }
     c->launches += launch_init_coords(c->x[0].get(), n, c->dim, c->ld, GEMPE_INIT_REFERENCE, opt->seed, 0.0, c->stream);
@@ -495,9 +552,7 @@ int gempe_relabel(gempe_ctx* c, std::uint64_t relabel_seed) {
       std::memcpy(after.data() + static_cast<std::size_t>(fwd[v]) * c->dim,
                   before.data() + static_cast<std::size_t>(v) * c->dim, sizeof(float) * c->dim);
     }
-    for (auto& v : c->work_src) v = fwd[v];
-    for (auto& v : c->work_dst) v = fwd[v];
-    for (auto& v : c->to_work) v = fwd[v];
+    apply_relabel(c, fwd);
     build_structures(c);
     if (gempe_set_coords(c, after.data()) != GEMPE_OK) throw cuda_error(c->error);
   });

@@ -56,6 +56,49 @@ __global__ void probe_kernel(const std::uint32_t* __restrict__ words, std::uint3
   if (t < count) out[t] = hash_test(words, mask, n, i[t], j[t]) ? 1 : 0;
 }
 
+// ---------------------------------------------------------------------------------- construction on the device
+
+// random_relabel applied to the edge arrays (graph.cpp:199-204): ids -> forward[ids], in place
+__global__ void relabel_apply_kernel(std::uint32_t* __restrict__ src, std::uint32_t* __restrict__ dst, std::uint64_t m,
+                                     const std::uint32_t* __restrict__ forward) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    src[e] = __ldg(forward + src[e]);
+    dst[e] = __ldg(forward + dst[e]);
+  }
+}
+
+__global__ void degree_count_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst,
+                                    std::uint64_t m, std::uint32_t* __restrict__ deg) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    atomicAdd(deg + src[e], 1u);
+    atomicAdd(deg + dst[e], 1u);
+  }
+}
+
+// both-direction CSR fill; the order inside a row is whatever the atomics give (the host build is used when a
+// reproducible order is asked for)
+__global__ void csr_fill_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst, std::uint64_t m,
+                                const std::uint32_t* __restrict__ rowptr, std::uint32_t* __restrict__ cursor,
+                                std::uint32_t* __restrict__ nbr, std::uint32_t* __restrict__ eid_role,
+                                std::uint32_t* __restrict__ csr_src) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    const std::uint32_t a = src[e], b = dst[e];
+    const std::uint32_t p0 = rowptr[a] + atomicAdd(cursor + a, 1u);
+    const std::uint32_t p1 = rowptr[b] + atomicAdd(cursor + b, 1u);
+    nbr[p0] = b;
+    nbr[p1] = a;
+    if (eid_role) {
+      eid_role[p0] = static_cast<std::uint32_t>(2 * e);
+      eid_role[p1] = static_cast<std::uint32_t>(2 * e + 1);
+      csr_src[p0] = a;
+      csr_src[p1] = b;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------- sampler
 
 // One sample stream: replays expand_seed32(seed, iter, unit, draw) followed by the LCG "advance, then use" loop
@@ -1930,6 +1973,26 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
   if (count == 0) return 0;
   probe_kernel<<<blocks_for(count, kThreads), kThreads, 0, stream>>>(hash_words, hash_mask, n, i, j, count, out);
   return 1;
+}
+
+int launch_relabel_apply(std::uint32_t* src, std::uint32_t* dst, std::uint64_t m, const std::uint32_t* forward,
+                         cudaStream_t stream) {
+  if (m == 0) return 0;
+  relabel_apply_kernel<<<static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u)), kThreads, 0,
+                         stream>>>(src, dst, m, forward);
+  return 1;
+}
+
+int launch_csr_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                     std::uint32_t* deg, std::uint32_t* rowptr, std::uint32_t* scratch, std::uint32_t* nbr,
+                     std::uint32_t* eid_role, std::uint32_t* csr_src, cudaStream_t stream) {
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  cudaMemsetAsync(deg, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
+  degree_count_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, deg);
+  const int scans = launch_scan(deg, rowptr, n, scratch, stream);
+  cudaMemsetAsync(deg, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);  // reused as the row cursors
+  csr_fill_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, rowptr, deg, nbr, eid_role, csr_src);
+  return 2 + scans;
 }
 
 int launch_sample(const SampleArgs& a, cudaStream_t stream) {

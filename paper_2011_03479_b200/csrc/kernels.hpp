@@ -109,6 +109,12 @@ struct GatherArgs {
 // ---- launchers (all asynchronous on `stream`; return the number of kernels launched) ---------------
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                       std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream);
+// construction on the device: relabel application and the both-direction CSR (row order = atomic arrival order)
+int launch_relabel_apply(std::uint32_t* src, std::uint32_t* dst, std::uint64_t m, const std::uint32_t* forward,
+                         cudaStream_t stream);
+int launch_csr_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                     std::uint32_t* deg, std::uint32_t* rowptr, std::uint32_t* scratch, std::uint32_t* nbr,
+                     std::uint32_t* eid_role, std::uint32_t* csr_src, cudaStream_t stream);
 int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::uint32_t n,
                  const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out,
                  cudaStream_t stream);
