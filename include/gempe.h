@@ -71,6 +71,11 @@ typedef struct gempe_options {
                              10 = cp.async shared-memory pipeline (16 < row stride <= 128) */
   int32_t bucket_mode;    /* incoming-sample bucketing: 0 = auto, 1 = per-partner atomics + scan + scatter,
                              2 = two-level counting sort (streaming traffic only; auto for n >= 2^22) */
+  int32_t exchange;       /* sharded sampling: 0 = every rank enumerates all sample streams and keeps the partners it
+                             owns (no exchange step); 1 = a rank samples only the streams of its own anchors, packs
+                             (partner, anchor) records per destination rank and the ranks exchange them with one
+                             equal-split all-to-all per round (gempe_exchange_layout / gempe_bucket_received);
+                             2 = as 1, and a single rank (world = 1) also leaves the exchange to the caller */
 } gempe_options;
 
 /* Fills *opt with defaults (dim must still be set). */
@@ -162,6 +167,15 @@ uint32_t gempe_padded_rows(const gempe_ctx* ctx);                  /* world*comm
 uint32_t gempe_block_rows(const gempe_ctx* ctx);                   /* rows per (chunk, rank) ownership block */
 int gempe_begin_round(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index); /* sampling passes */
 int gempe_begin_round_auto(gempe_ctx* ctx, uint64_t iter_index); /* same, sigma taken from the device state */
+/* opt.exchange = 1 only.  gempe_begin_round[_auto] then samples the rank's own streams and fills the send side:
+ * `send_records` holds world regions of `capacity` records {uint32 partner, uint32 anchor}, region d destined for
+ * rank d, `send_counts[d]` its fill.  The caller moves region d / count d of every rank s into region s / count s of
+ * rank d's `recv_records` / `recv_counts` (an equal-split all-to-all on the context's stream), then calls
+ * gempe_bucket_received before the first gempe_gather_chunk.  With world = 1 and exchange = 1 the context is its
+ * own peer (recv aliases send) and bucketing happens inside gempe_begin_round / gempe_iterate*. */
+int gempe_exchange_layout(gempe_ctx* ctx, void** send_records, void** recv_records, uint32_t** send_counts,
+                          uint32_t** recv_counts, uint32_t* capacity);
+int gempe_bucket_received(gempe_ctx* ctx);
 int gempe_gather_chunk(gempe_ctx* ctx, int chunk);                 /* gradient+update for one comm chunk */
 int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t / X_{t+1} */
 /* Device time in ms of the last `rounds` enqueued through gempe_iterate_async since the previous call

@@ -240,6 +240,50 @@ void build_structures(gempe_ctx* c) {
   }
   c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
   c->scan_scratch.allocate((n + 4095) / 4096 + 2);
+  c->exchange = ExchangeArgs{};
+  if (c->opt.exchange) {
+    // own sample streams per rank: the anchors of block b = chunk * world + r belong to rank r.  Every rank derives the
+    // same per-(source, destination) capacity from the busiest rank, so the all-to-all is an equal split.
+    auto first_slot_of = [&](std::uint64_t v) { return per_edge ? static_cast<std::uint64_t>(rowptr[v]) : v * c->opt.negatives; };
+    std::vector<std::uint64_t> own_slots(world, 0), own_rows(world, 0), first(c->comm_chunks), prefix(c->comm_chunks + 1, 0);
+    for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
+      for (std::uint32_t r = 0; r < world; ++r) {
+        const std::uint64_t block = static_cast<std::uint64_t>(chunk) * world + r;
+        const std::uint64_t lo = std::min<std::uint64_t>(n, block * c->block_rows);
+        const std::uint64_t hi = std::min<std::uint64_t>(n, (block + 1) * c->block_rows);
+        own_slots[r] += first_slot_of(hi) - first_slot_of(lo);
+        own_rows[r] += hi - lo;
+        if (r == rank) {
+          first[chunk] = first_slot_of(lo);
+          prefix[chunk + 1] = prefix[chunk] + first_slot_of(hi) - first_slot_of(lo);
+        }
+      }
+    }
+    const std::uint64_t busiest = *std::max_element(own_slots.begin(), own_slots.end());
+    const double share = n ? static_cast<double>(*std::max_element(own_rows.begin(), own_rows.end())) / n : 1.0;
+    const double expect = 1.25 * static_cast<double>(busiest) * share;  // partners are ~uniform over vertices
+    const std::uint64_t cap = std::min<std::uint64_t>(busiest, static_cast<std::uint64_t>(expect + 8.0 * std::sqrt(expect)) + 1024);
+    if (cap * world > 0xffffffffull) throw config_error("exchange regions exceed 2^32 records; use more ranks");
+    c->ex_first_slot.upload(first);
+    c->ex_prefix.upload(prefix);
+    const bool external = world > 1 || c->opt.exchange == 2;
+    c->ex_send.allocate(static_cast<std::size_t>(cap) * world);
+    if (external) c->ex_recv.allocate(static_cast<std::size_t>(cap) * world); else c->ex_recv.release();
+    c->ex_send_count.allocate(world, true);
+    if (external) c->ex_recv_count.allocate(world, true); else c->ex_recv_count.release();
+    c->ex_rank.allocate(static_cast<std::size_t>(cap) * world);
+    if (c->in_cnt.size() == 0) c->in_cnt.allocate(n);
+    c->exchange.own_slots = prefix.back();
+    c->exchange.ranges = c->comm_chunks;
+    c->exchange.first_slot = c->ex_first_slot.get();
+    c->exchange.prefix = c->ex_prefix.get();
+    c->exchange.capacity = static_cast<std::uint32_t>(cap);
+    c->exchange.send = c->ex_send.get();
+    c->exchange.send_count = c->ex_send_count.get();
+    // a single rank is its own peer: what it packed is what it receives
+    c->exchange.recv = external ? c->ex_recv.get() : c->ex_send.get();
+    c->exchange.recv_count = external ? c->ex_recv_count.get() : c->ex_send_count.get();
+  }
 
   timer.lap("uploads + allocations");
   // edge hash set, bit-packed (hash_set.cpp:9-34)
@@ -299,10 +343,28 @@ void require_live(gempe_ctx* c) {
   if (c->degenerate) throw config_error("cannot iterate a degenerate graph");  // engine.cpp:279
 }
 
+// exchange path, second half: bucket the (partner, anchor) records received from all ranks by partner
+void bucket_received(gempe_ctx* c) {
+  if (!c->opt.exchange) throw config_error("context was created without opt.exchange");
+  if (!c->bucket_pending) throw config_error("gempe_bucket_received without a preceding gempe_begin_round");
+  c->launches += launch_bucket_records(c->exchange, static_cast<std::uint32_t>(c->opt.world), c->n, c->in_cnt.get(),
+                                       c->in_off.get(), c->ex_rank.get(), c->in_anchor.get(), c->scan_scratch.get(), c->stream);
+  if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
+  cuda_check(cudaGetLastError(), "bucket received records");
+  c->bucket_pending = false;
+}
+
 void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
   cuda_check(cudaMemsetAsync(c->status.get(), 0, 8 * sizeof(std::uint32_t), c->stream), "memset status");
   cuda_check(cudaMemsetAsync(c->hist.get(), 0, 2 * kBins * sizeof(unsigned long long), c->stream), "memset hist");
   const SampleArgs a = sample_args(c, iter);
+  if (c->opt.exchange) {
+    c->launches += launch_sample_pack(a, c->exchange, c->stream);
+    cuda_check(cudaGetLastError(), "sample + pack");
+    c->bucket_pending = true;
+    if (c->exchange.recv == c->exchange.send) bucket_received(c);  // own peer
+    return;
+  }
   if (c->partition.buckets) {
     c->launches += launch_sample_partition(a, c->partition, c->in_off.get(), c->in_anchor.get(), c->stream);
   } else {
@@ -316,6 +378,7 @@ void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
 }
 
 void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
+  if (c->bucket_pending) throw config_error("records are packed but not exchanged: call gempe_bucket_received first");
   GatherArgs g{};
   g.x_cur = c->x[c->cur].get();
   g.x_next = c->x[c->cur ^ 1].get();
@@ -371,6 +434,10 @@ void fetch_status(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_no
   if (st[kStatRetryCap]) {
     throw near_complete_graph_error("no non-edge partner found after 10^4 draws; graph is near-complete");
   }
+  if (st[kStatExchangeOverflow]) {
+    throw data_error("sample exchange region overflowed: partners are far from uniform over ranks for this graph; "
+                     "create the context with opt.exchange = 0");
+  }
   if (st[kStatNonFinite]) {
     throw divergence_error("non-finite coordinate after update", static_cast<int>(c->round_iter) + 1);
   }
@@ -381,6 +448,7 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
   if (o.dim < 1) throw config_error("dimension must be >= 1");
   if (row_stride_for(o.dim) > 1024) throw config_error("dimension above 1024 is not supported by the device layout");
   if (o.neg_mode != GEMPE_NEG_PER_EDGE_2 && o.neg_mode != GEMPE_NEG_PER_VERTEX_K) throw config_error("unknown neg_mode");
+  if (o.exchange < 0 || o.exchange > 2) throw config_error("unknown exchange mode");
   if (o.math != GEMPE_MATH_TABLES && o.math != GEMPE_MATH_EXACT) throw config_error("unknown math policy");
   if (o.rng != GEMPE_RNG_REFERENCE && o.rng != GEMPE_RNG_PHILOX) throw config_error("unknown rng mode");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw config_error("bad rank/world");
@@ -597,9 +665,29 @@ int gempe_begin_round_auto(gempe_ctx* c, std::uint64_t iter_index) {
   });
 }
 
+int gempe_bucket_received(gempe_ctx* c) {
+  return guarded(c, [&] {
+    require_live(c);
+    bucket_received(c);
+  });
+}
+
+int gempe_exchange_layout(gempe_ctx* c, void** send_records, void** recv_records, std::uint32_t** send_counts,
+                          std::uint32_t** recv_counts, std::uint32_t* capacity) {
+  return guarded(c, [&] {
+    if (!c->opt.exchange || c->degenerate) throw config_error("context has no exchange buffers (opt.exchange is off)");
+    if (send_records) *send_records = c->exchange.send;
+    if (recv_records) *recv_records = const_cast<uint2*>(c->exchange.recv);
+    if (send_counts) *send_counts = c->exchange.send_count;
+    if (recv_counts) *recv_counts = const_cast<std::uint32_t*>(c->exchange.recv_count);
+    if (capacity) *capacity = c->exchange.capacity;
+  });
+}
+
 int gempe_gather_chunk(gempe_ctx* c, int chunk) {
   return guarded(c, [&] {
     require_live(c);
+
     if (chunk < 0 || chunk >= static_cast<int>(c->comm_chunks)) throw config_error("chunk out of range");
     gather_items(c, c->chunk_item_off[chunk], c->chunk_item_off[chunk + 1]);
   });

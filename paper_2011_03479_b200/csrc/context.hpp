@@ -86,6 +86,12 @@ struct gempe_ctx {
   gempe::PartitionArgs partition{};
   gempe::DeviceBuffer<std::uint32_t> block_hist, bucket_off;
   gempe::DeviceBuffer<uint2> records;
+  // sharded sampling with an exchange step (opt.exchange): records packed by destination rank, see kernels.hpp
+  gempe::ExchangeArgs exchange{};
+  gempe::DeviceBuffer<std::uint64_t> ex_first_slot, ex_prefix;
+  gempe::DeviceBuffer<uint2> ex_send, ex_recv;
+  gempe::DeviceBuffer<std::uint32_t> ex_send_count, ex_recv_count, ex_rank;
+  bool bucket_pending = false;  // records packed, gempe_bucket_received not yet called
   gempe::DeviceBuffer<uint4> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
   // gempe_step_host pipeline: item / vertex boundaries of the slices whose rows are copied out while later

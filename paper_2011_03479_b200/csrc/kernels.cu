@@ -178,6 +178,68 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, c
   in_anchor[in_off[a.neg_own[t]] + rank] = anchor;
 }
 
+// ---- sharded sampling with an exchange step (world > 1): every rank samples ONLY the streams of the anchors it owns,
+// packs (partner, anchor) records by the partner's owner rank, the ranks exchange the packed regions (one equal-split
+// all-to-all over NVLink), and each rank buckets what it received.  Sampling work therefore scales with 1/world.
+__global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleArgs a, const ExchangeArgs x) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t draws = 0;
+  bool have = false;
+  std::uint32_t partner = 0, anchor = 0, dest = 0;
+  if (i < x.own_slots) {
+    // own slot i -> global slot: ranges[c] = first global slot of the c-th owned block, prefix[c] = own slots before it
+    std::uint32_t c = 0, hi = x.ranges;  // largest c with prefix[c] <= i
+    while (hi - c > 1) {
+      const std::uint32_t mid = (c + hi) >> 1;
+      if (__ldg(x.prefix + mid) <= i) c = mid; else hi = mid;
+    }
+    const std::uint64_t t = x.first_slot[c] + (i - x.prefix[c]);
+    partner = sample_slot(a, t, anchor, draws);
+    a.neg_own[t] = partner;
+    dest = (partner / a.own.block_rows) % a.own.world;
+    have = true;
+  }
+  add_draws(a, draws);
+  // one atomic per distinct destination rank and warp
+  const unsigned active = __ballot_sync(kFull, have);
+  if (have) {
+    const unsigned peers = __match_any_sync(active, dest);
+    const int leader = __ffs(peers) - 1;
+    std::uint32_t base = 0;
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(x.send_count + dest, static_cast<std::uint32_t>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    const std::uint32_t pos = base + __popc(peers & ((1u << (threadIdx.x & 31)) - 1));
+    if (pos < x.capacity) {
+      x.send[static_cast<std::size_t>(dest) * x.capacity + pos] = make_uint2(partner, anchor);
+    } else {
+      atomicOr(a.status + kStatExchangeOverflow, 1u);
+    }
+  }
+}
+
+// received records -> per-partner counts and arrival ranks
+__global__ void __launch_bounds__(kThreads) count_records_kernel(const ExchangeArgs x, std::uint32_t world,
+                                                                 std::uint32_t* __restrict__ in_cnt,
+                                                                 std::uint32_t* __restrict__ rec_rank) {
+  const std::uint64_t idx = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<std::uint64_t>(world) * x.capacity) return;
+  const std::uint32_t from = static_cast<std::uint32_t>(idx / x.capacity), j = static_cast<std::uint32_t>(idx % x.capacity);
+  if (j >= min(x.recv_count[from], x.capacity)) return;
+  rec_rank[idx] = atomicAdd(in_cnt + x.recv[idx].x, 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) scatter_records_kernel(const ExchangeArgs x, std::uint32_t world,
+                                                                   const std::uint32_t* __restrict__ rec_rank,
+                                                                   const std::uint32_t* __restrict__ in_off,
+                                                                   std::uint32_t* __restrict__ in_anchor) {
+  const std::uint64_t idx = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<std::uint64_t>(world) * x.capacity) return;
+  const std::uint32_t from = static_cast<std::uint32_t>(idx / x.capacity), j = static_cast<std::uint32_t>(idx % x.capacity);
+  if (j >= min(x.recv_count[from], x.capacity)) return;
+  const uint2 rec = x.recv[idx];
+  in_anchor[in_off[rec.x] + rec_rank[idx]] = rec.y;
+}
+
 // ---- bucketing by partner, method B (large n): two-level counting sort with streaming traffic only.
 //   1. sample_count_kernel: persistent blocks sample their slots (grid-stride tiles) and histogram the partners'
 //      COARSE buckets (partner >> shift, <= 8192 buckets) in shared memory; one histogram row per block.
@@ -1999,6 +2061,31 @@ int launch_sample(const SampleArgs& a, cudaStream_t stream) {
   if (a.slots == 0) return 0;
   sample_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a);
   return 1;
+}
+
+int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream) {
+  cudaMemsetAsync(x.send_count, 0, a.own.world * sizeof(std::uint32_t), stream);
+  if (x.own_slots == 0) return 0;
+  sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 0, stream>>>(a, x);
+  return 1;
+}
+
+int launch_bucket_records(const ExchangeArgs& x, std::uint32_t world, std::uint32_t n, std::uint32_t* in_cnt,
+                          std::uint32_t* in_off, std::uint32_t* rec_rank, std::uint32_t* in_anchor, std::uint32_t* scratch,
+                          cudaStream_t stream) {
+  const std::uint64_t total = static_cast<std::uint64_t>(world) * x.capacity;
+  cudaMemsetAsync(in_cnt, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
+  int launches = 0;
+  if (total) {
+    count_records_kernel<<<blocks_for(total, kThreads), kThreads, 0, stream>>>(x, world, in_cnt, rec_rank);
+    ++launches;
+  }
+  launches += launch_scan(in_cnt, in_off, n, scratch, stream);
+  if (total) {
+    scatter_records_kernel<<<blocks_for(total, kThreads), kThreads, 0, stream>>>(x, world, rec_rank, in_off, in_anchor);
+    ++launches;
+  }
+  return launches;
 }
 
 std::uint32_t partition_grid(std::uint64_t slots) {

@@ -12,7 +12,7 @@ constexpr std::uint32_t kNoHub = 0xffffffffu;
 constexpr std::uint32_t kNotLocal = 0xffffffffu;
 
 // status word layout (device u32[8])
-enum StatusSlot { kStatNonFinite = 0, kStatRetryCap = 1, kStatDrawsLo = 2, kStatDrawsHi = 3 };
+enum StatusSlot { kStatNonFinite = 0, kStatRetryCap = 1, kStatDrawsLo = 2, kStatDrawsHi = 3, kStatExchangeOverflow = 4 };
 
 // Per-round scalars of parabola_impl (sigmoid.hpp:88-101), folded on the host in double:
 //   u = (delta - mu) * inv_sqrt2_sigma,  w = A g^2 + sign B (delta-mu) g,  d = delta + sign C g / w.
@@ -68,6 +68,20 @@ struct SampleArgs {
   Ownership own;
 };
 
+// Sharded sampling with an exchange step: this rank samples the streams of the anchors it owns and packs
+// (partner, anchor) records by destination rank; after the all-to-all it buckets the records it received.
+struct ExchangeArgs {
+  std::uint64_t own_slots;           // sample streams anchored at vertices this rank owns
+  std::uint32_t ranges;              // owned blocks (comm chunks)
+  const std::uint64_t* first_slot;   // [ranges] global slot id of the first own slot of block c
+  const std::uint64_t* prefix;       // [ranges + 1] own slots before block c
+  std::uint32_t capacity;            // records per (source, destination) region
+  uint2* send;                       // [world][capacity]
+  std::uint32_t* send_count;         // [world]
+  const uint2* recv;                 // [world][capacity]
+  const std::uint32_t* recv_count;   // [world]
+};
+
 // Two-level counting sort of the accepted samples by partner (large n).
 struct PartitionArgs {
   std::uint32_t shift;          // coarse bucket = partner >> shift (2^shift vertices per bucket)
@@ -119,6 +133,10 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
                  const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out,
                  cudaStream_t stream);
 int launch_sample(const SampleArgs& a, cudaStream_t stream);
+int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream);
+int launch_bucket_records(const ExchangeArgs& x, std::uint32_t world, std::uint32_t n, std::uint32_t* in_cnt,
+                          std::uint32_t* in_off, std::uint32_t* rec_rank, std::uint32_t* in_anchor, std::uint32_t* scratch,
+                          cudaStream_t stream);
 std::uint32_t partition_grid(std::uint64_t slots);
 // sampling + bucketing by partner with streaming traffic only (fills neg_own, in_off[n+1], in_anchor)
 int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::uint32_t* in_off, std::uint32_t* in_anchor,

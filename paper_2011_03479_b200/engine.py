@@ -116,7 +116,8 @@ class Context:
 
     def __init__(self, g: Graph, dim: int, seed: int = 1, *, neg_mode=NEG_PER_EDGE_2, negatives=0,
                  math=MATH_TABLES, rng=RNG_REFERENCE, hash_bits=0, relabel=True, device=0, rank=0, world=1,
-                 comm_chunks=1, chunk_entries=0, deterministic=False, precise_distance=False, kernel_variant=0, bucket_mode=0):
+                 comm_chunks=1, chunk_entries=0, deterministic=False, precise_distance=False, kernel_variant=0, bucket_mode=0,
+                 exchange=False):
         self._L = _capi.load()
         self._h = C.c_void_p()
         opt = _capi.Options()
@@ -127,6 +128,7 @@ class Context:
         opt.chunk_entries, opt.deterministic = chunk_entries, int(deterministic)
         opt.precise_distance, opt.kernel_variant = int(precise_distance), kernel_variant
         opt.bucket_mode = bucket_mode
+        opt.exchange = int(exchange)  # 0 off, 1 on, 2 on with the exchange left to the caller even for one rank
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         rc = self._L.gempe_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), C.byref(opt))
         if rc != _capi.OK:
@@ -307,6 +309,16 @@ class Context:
 
     def begin_round_auto(self, iter_index):
         self._check(self._L.gempe_begin_round_auto(self._h, iter_index))
+
+    def exchange_layout(self):
+        """(send_records, recv_records, send_counts, recv_counts) device addresses and the per-region capacity."""
+        ptrs = [C.c_void_p() for _ in range(4)]
+        cap = C.c_uint32()
+        self._check(self._L.gempe_exchange_layout(self._h, *[C.byref(p) for p in ptrs], C.byref(cap)))
+        return tuple(p.value for p in ptrs) + (cap.value,)
+
+    def bucket_received(self):
+        self._check(self._L.gempe_bucket_received(self._h))
 
     def gather_chunk(self, chunk: int):
         self._check(self._L.gempe_gather_chunk(self._h, chunk))

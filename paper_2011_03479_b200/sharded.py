@@ -5,9 +5,11 @@ block-cyclically -- block b of `block_rows` rows belongs to rank b % world, comm
 updated rows of chunk c of all ranks form ONE contiguous region of X_{t+1}.  That makes the exchange an
 in-place ``all_gather_into_tensor`` per chunk, issued as soon as the chunk's gather kernel is enqueued and
 overlapped with the next chunk's kernel; the sampling passes of round t+1 do not read X and are enqueued
-before the wait on round t's last all-gather.  Partner-side sample terms need no exchange: each rank
-enumerates all sample streams (integer work) and keeps those whose partner it owns.  The 2x512 tallies are
-summed with one all_reduce.
+before the wait on round t's last all-gather.  Partner-side sample terms: each rank samples only the streams of
+the anchors it owns, packs (partner, anchor) records by the partner's owner and the ranks swap the packed regions
+with one equal-split all-to-all per round (8 bytes per sample; sampling work scales with 1/world).  With
+`exchange=False` every rank instead enumerates all sample streams and keeps the partners it owns (no exchange,
+replicated integer work).  The 2x512 tallies are summed with one all_reduce.
 
 The collective logic is backend-agnostic (`ops` supplies the compute); tests drive it with gloo on CPU
 tensors, the product with `CudaShardOps` over NCCL.
@@ -51,6 +53,20 @@ class CudaShardOps:
         self.stream = torch.cuda.Stream(device=self.device)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.rows, self.ld = self.ctx.padded_rows, self.ctx.row_stride
+        self._exchange = None
+        if kw.get("exchange"):
+            send, recv, send_cnt, recv_cnt, cap = self.ctx.exchange_layout()
+            if recv != send:  # a single-rank context with exchange=1 is its own peer and buckets inside begin_round
+                as_t = lambda ptr, shape: torch.as_tensor(_DeviceArray(ptr, shape, "<i4"), device=self.device)
+                self._exchange = (as_t(send, (world, cap, 2)), as_t(recv, (world, cap, 2)),
+                                  as_t(send_cnt, (world,)), as_t(recv_cnt, (world,)))
+
+    def exchange_tensors(self):
+        """(send_records[world,cap,2], recv_records, send_counts[world], recv_counts) or None."""
+        return self._exchange
+
+    def bucket_received(self):
+        self.ctx.bucket_received()
 
     def x_next(self) -> torch.Tensor:
         ptr = self.ctx.device_coords(1)
@@ -90,7 +106,8 @@ class CudaShardOps:
 
 class ShardedEngine:
     """Drives rounds over a process group.  `ops` needs x_next(), begin_round, gather_chunk, end_round,
-    tallies(); `stream` (optional) is the CUDA stream the ops launch on."""
+    tallies(), optionally exchange_tensors() + bucket_received(); `stream` (optional) is the CUDA stream the
+    ops launch on."""
 
     def __init__(self, ops, n: int, m: int, world: int, rank: int, comm_chunks: int, group=None, stream=None,
                  force_collectives: bool = False):
@@ -115,6 +132,13 @@ class ShardedEngine:
         ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
         with ctx:
             self.ops.begin_round(mu, sigma, it)  # X-independent: overlaps the previous round's last exchange
+            bufs = self.ops.exchange_tensors() if hasattr(self.ops, "exchange_tensors") else None
+            if bufs is not None:
+                # region d of every rank's send side lands in region <source rank> of rank d's receive side
+                send, recv, send_cnt, recv_cnt = bufs
+                dist.all_to_all_single(recv_cnt, send_cnt, group=self.group)
+                dist.all_to_all_single(recv, send, group=self.group)
+                self.ops.bucket_received()
             self._wait_pending()                 # X_t must be complete before the first gather reads it
             x_next = self.ops.x_next()
             span = self.world * self.block_rows
@@ -177,12 +201,17 @@ class _Null:
 
 
 def make_cuda_engine(g: Graph, dim: int, seed: int, *, comm_chunks: int = 4, group=None, device: Optional[int] = None,
-                     force_collectives: bool = False, **ctx_kw) -> ShardedEngine:
-    """One rank of a sharded engine over the default (NCCL) process group; world 1 without a group."""
+                     force_collectives: bool = False, exchange: Optional[bool] = None, **ctx_kw) -> ShardedEngine:
+    """One rank of a sharded engine over the default (NCCL) process group; world 1 without a group.
+    `exchange` (default: on when collectives are in use) selects sampling of own anchors + all-to-all."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     device = torch.cuda.current_device() if device is None else device
     chunks = comm_chunks if (world > 1 or force_collectives) else 1
+    if exchange is None:
+        exchange = world > 1 or force_collectives
+    if exchange:
+        ctx_kw["exchange"] = 2 if (world == 1 and force_collectives) else 1  # 2: external exchange even for one rank
     ops = CudaShardOps(g, dim, seed, rank, world, chunks, device, **ctx_kw)
     return ShardedEngine(ops, g.n, g.edge_count(), world, rank, chunks, group=group, stream=ops.stream,
                          force_collectives=force_collectives)

@@ -197,6 +197,27 @@ def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k, buck
                     exact=exact, iters=3, bucket_mode=bucket_mode)
 
 
+@pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5)])
+def test_round_parity_with_the_exchange_path(G, oracle, golden_fastmath, neg_mode, k):
+    """opt.exchange on a single rank (its own peer): sample + pack, bucket the packed records.  Same oracle bar, and the
+    sample hook still returns the reference's streams bit for bit."""
+    for dim in (2, 128):
+        check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, neg_mode=neg_mode, k=k,
+                    iters=3, exchange=1)
+    n, src, dst = er_graph(3000, 20000, 7)
+    a = G.Context(G.Graph(n, src, dst), 8, 3, neg_mode=neg_mode, negatives=k, deterministic=True)
+    b = G.Context(G.Graph(n, src, dst), 8, 3, neg_mode=neg_mode, negatives=k, deterministic=True, exchange=1)
+    for it in range(2):
+        pa, da = a.sample(it)
+        pb, db = b.sample(it)
+        assert np.array_equal(pa, pb) and da == db
+        ha, hb = a.iterate(1.5, 1.0, it), b.iterate(1.5, 1.0, it)
+        assert np.array_equal(ha[0], hb[0]) and np.array_equal(ha[1], hb[1])
+    assert np.array_equal(a.get_coords().view(np.uint32), b.get_coords().view(np.uint32))
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("n", [300, 5000, 70001])
 def test_counting_sort_buckets_equal_atomic_buckets(G, n):
     """Both bucketing methods must hand the gather the same multiset of incoming anchors per vertex: with

@@ -59,10 +59,78 @@ def test_rank_contexts_reproduce_the_single_gpu_round(world, chunks, mode, k, bu
             c.close()
 
 
-def test_nccl_plumbing_on_a_single_rank_group():
+def _exchange_views(ctx, world):
+    import torch
+    from paper_2011_03479_b200.sharded import _DeviceArray
+    send, recv, send_cnt, recv_cnt, cap = ctx.exchange_layout()
+    t = lambda ptr, shape: torch.as_tensor(_DeviceArray(ptr, shape, "<i4"), device="cuda:0")
+    return t(send, (world, cap, 2)), t(recv, (world, cap, 2)), t(send_cnt, (world,)), t(recv_cnt, (world,))
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (4, 2), (8, 4)])
+@pytest.mark.parametrize("mode,k", [(0, 0), (1, 6)])
+def test_rank_contexts_with_sample_exchange_reproduce_the_single_gpu_round(world, chunks, mode, k):
+    """opt.exchange: each rank samples only its own anchors' streams; the all-to-all is emulated by device copies
+    (region d of rank s -> region s of rank d).  Coordinates bit-identical to the single context, tallies and draw
+    counts sum to the single context's, and every rank does ~1/world of the sampling."""
+    import torch
+    import paper_2011_03479_b200 as G
+    for (n, src, dst), dim in ((er_graph(1003, 6000, 3), 64), (star_plus_ring(400, hubs=2), 2)):
+        g = G.Graph(n, src, dst)
+        single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+        ranks = [G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64, rank=r,
+                           world=world, comm_chunks=chunks, exchange=1) for r in range(world)]
+        views = [_exchange_views(c, world) for c in ranks]
+        block = ranks[0].block_rows
+        sigma = 1.0
+        for it in range(3):
+            he, hn = single.iterate(1.5, sigma, it)
+            want = single.get_coords()
+            for c in ranks:
+                c.begin_round(1.5, sigma, it)
+            torch.cuda.synchronize()
+            packed = 0
+            for s_rank in range(world):
+                packed += int(views[s_rank][2].sum())
+                for d in range(world):
+                    views[d][1][s_rank].copy_(views[s_rank][0][d])
+                    views[d][3][s_rank] = views[s_rank][2][d]
+            assert packed == single.sample_slots  # every stream sampled by exactly one rank
+            torch.cuda.synchronize()
+            tot_e, tot_n = np.zeros(512, np.uint64), np.zeros(512, np.uint64)
+            for c in ranks:
+                if it == 0 and c is ranks[0]:
+                    with pytest.raises(G.ConfigError):  # packed records must be exchanged and bucketed first
+                        c.gather_chunk(0)
+                c.bucket_received()
+                for ch in range(chunks):
+                    c.gather_chunk(ch)
+                e, nn = c.sync()
+                tot_e += e
+                tot_n += nn
+            assert np.array_equal(tot_e, he) and np.array_equal(tot_n, hn)
+            nxt = [_views(c, 1) for c in ranks]
+            for ch in range(chunks):
+                for r in range(world):
+                    lo = (ch * world + r) * block
+                    for other in range(world):
+                        if other != r:
+                            nxt[other][lo:lo + block].copy_(nxt[r][lo:lo + block])
+            torch.cuda.synchronize()
+            for c in ranks:
+                c.end_round()
+                assert np.array_equal(c.get_coords().view(np.uint32), want.view(np.uint32))
+            sigma *= 1.3
+        for c in ranks + [single]:
+            c.close()
+
+
+@pytest.mark.parametrize("exchange", [False, True])
+def test_nccl_plumbing_on_a_single_rank_group(exchange):
     """Real NCCL on one GPU: a 1-rank process group with the collectives forced on, three comm chunks.  Exercises
-    the device-pointer tensor views, the in-place all_gather_into_tensor per chunk, the device-side tally all-reduce
-    and the device sigma search; the result must equal the plain engine bit for bit."""
+    the device-pointer tensor views, the in-place all_gather_into_tensor per chunk, the device-side tally all-reduce,
+    the device sigma search and (exchange=True) the all_to_all_single of the packed sample records; the result must
+    equal the plain engine bit for bit."""
     import os
     import socket
     import torch
@@ -81,8 +149,9 @@ def test_nccl_plumbing_on_a_single_rank_group():
         n, src, dst = er_graph(2003, 12000, 4)
         g = G.Graph(n, src, dst)
         eng = sharded.make_cuda_engine(g, 64, 5, comm_chunks=3, device=0, force_collectives=True, neg_mode=1,
-                                       negatives=6, deterministic=True)
+                                       negatives=6, deterministic=True, exchange=exchange)
         assert eng.chunks == 3 and eng.collective
+        assert (eng.ops.exchange_tensors() is not None) == exchange
         plain = G.Context(g, 64, 5, neg_mode=1, negatives=6, deterministic=True)
         plain.set_sigma(1.5, 1.0)
         for it in range(3):
