@@ -146,11 +146,17 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
   return anchor + 1 < a.n ? anchor + 1 : 0;
 }
 
+// Total draw count (test hook / p-bar of the roofline formula).  Called by every thread of the block: one global
+// atomic per block -- per-warp atomics on this single address serialise in L2 and dominated the sampling kernel.
 __device__ __forceinline__ void add_draws(const SampleArgs& a, std::uint32_t draws) {
-  // total draw count (test hook / p-bar of the roofline formula)
+  __shared__ std::uint32_t block_draws;
+  if (threadIdx.x == 0) block_draws = 0;
+  __syncthreads();
   for (int off = 16; off > 0; off >>= 1) draws += __shfl_xor_sync(kFull, draws, off);
-  if ((threadIdx.x & 31) == 0 && draws) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.status + kStatDrawsLo), static_cast<unsigned long long>(draws));
+  if ((threadIdx.x & 31) == 0 && draws) atomicAdd(&block_draws, draws);
+  __syncthreads();
+  if (threadIdx.x == 0 && block_draws) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.status + kStatDrawsLo), static_cast<unsigned long long>(block_draws));
   }
 }
 
@@ -200,15 +206,21 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
     have = true;
   }
   add_draws(a, draws);
-  // one atomic per distinct destination rank and warp
-  const unsigned active = __ballot_sync(kFull, have);
+  // one global atomic per destination rank and BLOCK: ranks within the block come from shared counters
+  extern __shared__ std::uint32_t sh_pack[];  // [world] counts, then [world] bases
+  std::uint32_t* sh_cnt = sh_pack;
+  std::uint32_t* sh_base = sh_pack + a.own.world;
+  for (std::uint32_t d = threadIdx.x; d < a.own.world; d += blockDim.x) sh_cnt[d] = 0;
+  __syncthreads();
+  std::uint32_t local = 0;
+  if (have) local = atomicAdd(sh_cnt + dest, 1u);
+  __syncthreads();
+  for (std::uint32_t d = threadIdx.x; d < a.own.world; d += blockDim.x) {
+    sh_base[d] = sh_cnt[d] ? atomicAdd(x.send_count + d, sh_cnt[d]) : 0u;
+  }
+  __syncthreads();
   if (have) {
-    const unsigned peers = __match_any_sync(active, dest);
-    const int leader = __ffs(peers) - 1;
-    std::uint32_t base = 0;
-    if ((threadIdx.x & 31) == leader) base = atomicAdd(x.send_count + dest, static_cast<std::uint32_t>(__popc(peers)));
-    base = __shfl_sync(peers, base, leader);
-    const std::uint32_t pos = base + __popc(peers & ((1u << (threadIdx.x & 31)) - 1));
+    const std::uint32_t pos = sh_base[dest] + local;
     if (pos < x.capacity) {
       x.send[static_cast<std::size_t>(dest) * x.capacity + pos] = make_uint2(partner, anchor);
     } else {
@@ -2066,7 +2078,7 @@ int launch_sample(const SampleArgs& a, cudaStream_t stream) {
 int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream) {
   cudaMemsetAsync(x.send_count, 0, a.own.world * sizeof(std::uint32_t), stream);
   if (x.own_slots == 0) return 0;
-  sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 0, stream>>>(a, x);
+  sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 2 * a.own.world * sizeof(std::uint32_t), stream>>>(a, x);
   return 1;
 }
 
@@ -2182,9 +2194,10 @@ void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t 
 template <int LPR, int NV, int VEC, int TB, int U, int THREADS = 256, int MINB = 2>
 void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
   const bool full = a.ld == static_cast<std::uint32_t>(LPR * NV * VEC);
-  if (precise) {
-    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, true, true, THREADS, MINB>(a, lo, hi, stream);
-    else gather_batched_launch<LPR, NV, VEC, TB, U, true, false, THREADS, MINB>(a, lo, hi, stream);
+  if (precise) {  // the double chain needs the registers: never more than 4 blocks per SM
+    constexpr int kMinB = MINB > 4 ? 4 : MINB;
+    if (full) gather_batched_launch<LPR, NV, VEC, TB, U, true, true, THREADS, kMinB>(a, lo, hi, stream);
+    else gather_batched_launch<LPR, NV, VEC, TB, U, true, false, THREADS, kMinB>(a, lo, hi, stream);
   } else {
     if (full) gather_batched_launch<LPR, NV, VEC, TB, U, false, true, THREADS, MINB>(a, lo, hi, stream);
     else gather_batched_launch<LPR, NV, VEC, TB, U, false, false, THREADS, MINB>(a, lo, hi, stream);
@@ -2268,7 +2281,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
   else if (ld <= 64) gather_batched_go<16, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
-  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);  // 16 rows/warp, 16 warps/SM
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);  // 16 rows/warp, 20 warps/SM (96 regs)
   else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);
