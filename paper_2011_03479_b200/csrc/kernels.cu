@@ -994,6 +994,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   auto row_ptr = [&](std::uint32_t row, int j) {
     return reinterpret_cast<const float*>(x_lane + static_cast<std::uint64_t>(row) * row_bytes + LPR * j * VEC * 4);
   };
+  const char* pf_lane = reinterpret_cast<const char*>(a.x_cur) + (lane % LINES) * 128;  // this lane's line of a prefetched row
 
   // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
   // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
@@ -1026,14 +1027,17 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       // one list entry (vertex id) per lane and sub-batch.  Validity and kind (0 edge, 1 sample tallied here, 2
       // incoming sample) follow from the entry's position alone, so nothing has to wait on these loads until the
       // ids are needed as addresses two batches later.
+      // entry e of the virtual list lives at index e + d of its array (wrapping 32-bit arithmetic)
+      const std::uint32_t dA = begin, dB = offB - lenA, dC = offC - endB;
       auto fetch = [&](std::uint32_t base, std::uint32_t (&ent)[U]) {
 #pragma unroll
         for (int s = 0; s < U; ++s) {
           const std::uint32_t e = base + s * E + lane;
+          const bool in_a = e < lenA, in_b = e < endB;
+          const std::uint32_t idx = e + (in_a ? dA : (in_b ? dB : dC));
+          const std::uint32_t* arr = in_a ? a.nbr : (in_b ? a.neg_own : a.in_anchor);
           ent[s] = u;
-          if ((E == 32 || lane < E) && e < total) {
-            ent[s] = __ldg(e < lenA ? a.nbr + begin + e : (e < endB ? a.neg_own + offB + (e - lenA) : a.in_anchor + offC + (e - endB)));
-          }
+          if ((E == 32 || lane < E) && e < total) ent[s] = __ldg(arr + idx);
         }
       };
 
@@ -1073,12 +1077,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         // after that -> registers
         if constexpr (kPrefetch) {
 #pragma unroll
-          for (int i = 0; i < E * LINES / 32; ++i) {
-            const int slot = i * 32 + lane;
-            const std::uint32_t row = __shfl_sync(kFull, nxt[0], slot / LINES);
-            if (base + E + slot / LINES < total) {
-              prefetch_l2(reinterpret_cast<const char*>(a.x_cur) + static_cast<std::uint64_t>(row) * row_bytes + (slot % LINES) * 128);
-            }
+          for (int i = 0; i < E * LINES / 32; ++i) {  // lane -> line (lane % LINES) of row i * 32 / LINES + lane / LINES
+            const std::uint32_t slot_row = i * (32 / LINES) + lane / LINES;
+            const std::uint32_t row = __shfl_sync(kFull, nxt[0], slot_row);
+            if (base + E + slot_row < total) prefetch_l2(pf_lane + static_cast<std::uint64_t>(row) * row_bytes);
           }
         }
         std::uint32_t nn[U];
