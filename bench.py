@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline budget on rank 0")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--peer-broadcast", default="auto", choices=["auto", "off"],
+                   help="N > 1: gather kernel stores updated rows into the peers' buffers (auto) or NCCL all-gather (off)")
     return p.parse_args()
 
 
@@ -116,7 +118,7 @@ def cpu_reference_arm(n, src, dst, dim, budget_s, steps=None, warmup=1):
     return {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
             "sample": f"first {m_use} of {len(src)} edges on all {n} vertices, reference sampling (2 draws/edge, "
                       f"3m pair-terms), lane_width={lanes}, {rounds} timed rounds, median {sec:.3f} s/round",
-            "host_cores": cores}
+            "host_cores": cores, "sample_ms_per_round": sec * 1e3}
 
 
 def main():
@@ -141,8 +143,8 @@ def main():
         n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config, device=gen_device())
         base = cpu_reference_arm(n, src, dst, dim, max(args.cpu_seconds, 30.0), steps=args.steps, warmup=args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["sample_ms_per_round"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": {"workload": workload_name(args.config), "n": n, "m": int(len(src))},
                 "cpu_baseline": base,
                 "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -154,19 +156,57 @@ def main():
     import paper_2011_03479_b200 as P
     from paper_2011_03479_b200 import sharded
 
+    # test hook: GEMPE_BENCH_TEST_BACKEND=gloo runs the N > 1 control flow with every rank time-sliced on cuda:0 (no
+    # kernel waits on another rank; sample exchange off because gloo has no CUDA all-to-all) -- never a bench number
+    test_backend = os.environ.get("GEMPE_BENCH_TEST_BACKEND")
+    if test_backend:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if test_backend:
+            dist.init_process_group(test_backend)
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     n, src, dst, dim, k, _, init, std = graphgen.make_config(args.config, device=gen_device())
     torch.cuda.empty_cache()
     g = P.Graph(n, src, dst)
     neg_mode = P.NEG_PER_VERTEX_K if args.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
-    eng = sharded.make_cuda_engine(g, dim, 1, comm_chunks=args.comm_chunks, device=local_rank, neg_mode=neg_mode,
-                                   negatives=k if neg_mode == P.NEG_PER_VERTEX_K else 0,
-                                   chunk_entries=args.chunk_entries, bucket_mode=args.bucket_mode)
+    def build_engine(peer_broadcast):
+        e = sharded.make_cuda_engine(g, dim, 1, comm_chunks=args.comm_chunks, device=local_rank, neg_mode=neg_mode,
+                                     negatives=k if neg_mode == P.NEG_PER_VERTEX_K else 0,
+                                     chunk_entries=args.chunk_entries, bucket_mode=args.bucket_mode,
+                                     peer_broadcast=peer_broadcast, exchange=False if test_backend else None)
+        e.ops.ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
+        return e
+
+    # N > 1: fused update + broadcast into the peers' buffers when every rank can open them AND the replicas agree
+    # after two trial rounds; otherwise the NCCL all-gather per comm chunk
+    exchange_path = "none"
+    if world > 1:
+        exchange_path = "nccl all-gather per chunk"
+        if args.peer_broadcast != "off":
+            try:
+                eng = build_engine(True)
+                for _ in range(2):
+                    eng.run_single_iteration()
+                torch.cuda.synchronize()
+                dist.barrier()
+                if sharded.replicas_agree(eng.ops.x_next(), None) and sharded.replicas_agree(
+                        torch.as_tensor(sharded._DeviceArray(eng.ops.ctx.device_coords(0), (eng.ops.rows, eng.ops.ld)),
+                                        device=eng.ops.device), None):
+                    exchange_path = "peer stores from the gather kernel (CUDA IPC)"
+                else:
+                    raise RuntimeError("replicas differ")
+            except Exception as e:  # noqa: BLE001
+                if rank == 0:
+                    print(f"[bench] peer broadcast unavailable ({e}); using the all-gather path", file=sys.stderr)
+                eng = None
+        if exchange_path.startswith("nccl"):
+            eng = build_engine(False)
+    else:
+        eng = build_engine(False)
     ctx = eng.ops.ctx
-    ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
     stream = eng.ops.stream
 
     def barrier():
@@ -217,7 +257,10 @@ def main():
                        "pair_terms_per_iteration": int(pair_terms), "sigma": sigma,
                        "l2": "inputs larger than L2 (X %.0f MB + lists)" % (n * dim * 4 / 1e6) if n * dim * 4 > 126e6
                              else "working set fits L2 (reported as is)",
-                       "parallelism": f"vertex-sharded x{world}, all-gather chunks={eng.chunks}" if world > 1 else "1 GPU"},
+                       "parallelism": f"vertex-sharded x{world}, samples: "
+                                      f"{'own anchors + all-to-all' if eng.ops.exchange_tensors() is not None else 'replicated enumeration'}"
+                                      f", coordinates: {exchange_path}"
+                                      if world > 1 else "1 GPU"},
             "clocks": clocks, "gpu_launches": int(launches)}
 
     if rank == 0 and world == 1:

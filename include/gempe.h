@@ -177,6 +177,24 @@ int gempe_exchange_layout(gempe_ctx* ctx, void** send_records, void** recv_recor
                           uint32_t** recv_counts, uint32_t* capacity);
 int gempe_bucket_received(gempe_ctx* ctx);
 int gempe_gather_chunk(gempe_ctx* ctx, int chunk);                 /* gradient+update for one comm chunk */
+
+/* Fused update + broadcast (replaces the all-gather of gempe_gather_chunk's rows): once peers are registered, every
+ * row this rank updates is stored by the gather kernel into the X_{t+1} buffer of each peer as well (peer device
+ * memory over NVLink / NVSwitch), so after all ranks have finished round t every rank holds the full X_{t+1} without
+ * a collective on the coordinates.  The ranks only need a barrier between consecutive rounds (a rank must not start
+ * round t+1's gather while a peer still reads or writes round t's buffers); the tally all-reduce is one.
+ *   gempe_coords_ipc_handles : this rank's two coordinate buffers as CUDA IPC handles (2 x 64 bytes, parity 0 and 1)
+ *   gempe_open_peer          : registers a peer from the handles it published (another process, any GPU with P2P)
+ *   gempe_add_peer_pointers  : registers a peer living in THIS process (buffers of parity 0 and 1)
+ *   gempe_device_coords_parity / gempe_coords_parity : the buffer of a given parity / the parity holding X_t now
+ * All ranks must run their rounds in lock step (same parity).  */
+#define GEMPE_IPC_HANDLE_BYTES 64
+int gempe_coords_ipc_handles(gempe_ctx* ctx, void* out_2x64_bytes);
+int gempe_open_peer(gempe_ctx* ctx, const void* handles_2x64_bytes);
+int gempe_add_peer_pointers(gempe_ctx* ctx, void* x_parity0, void* x_parity1);
+int gempe_clear_peers(gempe_ctx* ctx);
+void* gempe_device_coords_parity(gempe_ctx* ctx, int parity);
+int gempe_coords_parity(const gempe_ctx* ctx);
 int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t / X_{t+1} */
 /* Device time in ms of the last `rounds` enqueued through gempe_iterate_async since the previous call
  * (CUDA events on the context's stream), split as {total, sampling passes, gather+update}. */

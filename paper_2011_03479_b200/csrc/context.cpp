@@ -382,6 +382,8 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   GatherArgs g{};
   g.x_cur = c->x[c->cur].get();
   g.x_next = c->x[c->cur ^ 1].get();
+  g.n_peers = static_cast<int>(c->peers.size());
+  for (int p = 0; p < g.n_peers; ++p) g.peer_next[p] = c->peers[p].x[c->cur ^ 1];
   g.n = c->n;
   g.dim = c->dim;
   g.ld = c->ld;
@@ -469,6 +471,11 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
 using namespace gempe;
 
 gempe_ctx::~gempe_ctx() {
+  for (const Peer& p : peers) {
+    if (!p.ipc) continue;
+    cudaIpcCloseMemHandle(p.x[0]);
+    cudaIpcCloseMemHandle(p.x[1]);
+  }
   for (cudaEvent_t e : events) cudaEventDestroy(e);
   if (pinned) cudaFreeHost(pinned);
   for (cudaEvent_t e : step_events) cudaEventDestroy(e);
@@ -894,6 +901,61 @@ int gempe_set_stream(gempe_ctx* c, void* cuda_stream) {
   c->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c->own_stream;
   return GEMPE_OK;
 }
+// ---- fused update + broadcast over peer memory -------------------------------------------------------
+int gempe_coords_ipc_handles(gempe_ctx* c, void* out) {
+  return guarded(c, [&] {
+    if (c->degenerate) throw config_error("degenerate graph: no coordinates on the device");
+    cudaIpcMemHandle_t h[2];
+    static_assert(sizeof h == 2 * GEMPE_IPC_HANDLE_BYTES, "handle size");
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    for (int i = 0; i < 2; ++i) cuda_check(cudaIpcGetMemHandle(&h[i], c->x[i].get()), "cudaIpcGetMemHandle");
+    std::memcpy(out, h, sizeof h);
+  });
+}
+
+int gempe_open_peer(gempe_ctx* c, const void* handles) {
+  return guarded(c, [&] {
+    if (static_cast<int>(c->peers.size()) >= kMaxPeers) throw config_error("too many peers (world <= 16)");
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, handles, sizeof h);
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    gempe_ctx::Peer p;
+    p.ipc = true;
+    for (int i = 0; i < 2; ++i) {
+      void* ptr = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&ptr, h[i], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      p.x[i] = static_cast<float*>(ptr);
+    }
+    c->peers.push_back(p);
+  });
+}
+
+int gempe_add_peer_pointers(gempe_ctx* c, void* x0, void* x1) {
+  return guarded(c, [&] {
+    if (static_cast<int>(c->peers.size()) >= kMaxPeers) throw config_error("too many peers (world <= 16)");
+    if (!x0 || !x1) throw config_error("null peer buffer");
+    gempe_ctx::Peer p;
+    p.x[0] = static_cast<float*>(x0);
+    p.x[1] = static_cast<float*>(x1);
+    c->peers.push_back(p);
+  });
+}
+
+int gempe_clear_peers(gempe_ctx* c) {
+  return guarded(c, [&] {
+    cuda_check(cudaStreamSynchronize(c->stream), "clear peers");
+    for (const gempe_ctx::Peer& p : c->peers) {
+      if (!p.ipc) continue;
+      cudaIpcCloseMemHandle(p.x[0]);
+      cudaIpcCloseMemHandle(p.x[1]);
+    }
+    c->peers.clear();
+  });
+}
+
+void* gempe_device_coords_parity(gempe_ctx* c, int parity) { return c->x[parity & 1].get(); }
+int gempe_coords_parity(const gempe_ctx* c) { return c->cur; }
+
 void* gempe_device_coords(gempe_ctx* c, int which) { return c->x[which ? c->cur ^ 1 : c->cur].get(); }
 std::uint32_t gempe_row_stride(const gempe_ctx* c) { return c->ld; }
 std::uint32_t gempe_padded_rows(const gempe_ctx* c) { return c->n_pad; }

@@ -92,6 +92,12 @@ struct gempe_ctx {
   gempe::DeviceBuffer<uint2> ex_send, ex_recv;
   gempe::DeviceBuffer<std::uint32_t> ex_send_count, ex_recv_count, ex_rank;
   bool bucket_pending = false;  // records packed, gempe_bucket_received not yet called
+  // fused update + broadcast: X buffers (both parities, indexed like x[]) of the other ranks, in this rank's address space
+  struct Peer {
+    float* x[2] = {nullptr, nullptr};
+    bool ipc = false;  // opened with cudaIpcOpenMemHandle (closed on destroy)
+  };
+  std::vector<Peer> peers;
   gempe::DeviceBuffer<uint4> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
   // gempe_step_host pipeline: item / vertex boundaries of the slices whose rows are copied out while later

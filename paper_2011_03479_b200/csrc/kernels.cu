@@ -715,6 +715,13 @@ __device__ __forceinline__ void store_row(float* __restrict__ p, const float (&v
   }
 }
 
+// the updated row goes to this rank's X_{t+1} and to every peer's (GatherArgs::peer_next)
+template <int VEC>
+__device__ __forceinline__ void store_row_everywhere(const GatherArgs& a, std::size_t offset, const float (&v)[VEC]) {
+  store_row<VEC>(a.x_next + offset, v);
+  for (int p = 0; p < a.n_peers; ++p) store_row<VEC>(a.peer_next[p] + offset, v);
+}
+
 __device__ __forceinline__ double shfl_xor_f64(double v, int off) {
   return __shfl_xor_sync(kFull, v, off);
 }
@@ -902,7 +909,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
           }
         }
         const std::uint32_t col = (r + LPR * j) * VEC;
-        store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+        store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld + col, out);
         if (a.cap_y) {
 #pragma unroll
           for (int c = 0; c < VEC; ++c)
@@ -919,6 +926,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
+  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
 }
 
 
@@ -1304,7 +1312,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             }
           }
           const std::uint32_t col = (r + LPR * j) * VEC;
-          store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+          store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld + col, out);
           if (a.cap_y) {
 #pragma unroll
             for (int c = 0; c < VEC; ++c)
@@ -1322,6 +1330,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
+  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
 }
 
 // ---------------------------------------------------------------------------------- gather, one thread per work item
@@ -1469,7 +1478,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
           bad |= !isfinite(out[c]);
         }
       }
-      store_row<VEC>(a.x_next + static_cast<std::size_t>(u) * ld, out);
+      store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld, out);
       if (a.cap_y) {
 #pragma unroll
         for (int c = 0; c < VEC; ++c)
@@ -1485,6 +1494,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
+  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
 }
 
 // ---------------------------------------------------------------------------------- gather, cp.async pipeline
@@ -1850,7 +1860,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
           }
         }
         const std::uint32_t col = r * 4;
-        store_row<4>(a.x_next + static_cast<std::size_t>(u) * ld + col, out);
+        store_row_everywhere<4>(a, static_cast<std::size_t>(u) * ld + col, out);
         if (a.cap_y) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
@@ -1880,6 +1890,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const Ga
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
+  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
 }
 
 // ---------------------------------------------------------------------------------- sigma search on the device

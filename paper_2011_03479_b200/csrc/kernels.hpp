@@ -92,9 +92,15 @@ struct PartitionArgs {
   uint2* records;               // [S] (partner, anchor), grouped by coarse bucket
 };
 
+constexpr int kMaxPeers = 15;  // other ranks whose X_{t+1} copy this rank writes directly (world <= 16)
+
 struct GatherArgs {
   const float* x_cur;
   float* x_next;
+  // fused update + broadcast: every updated row is also stored into the X_{t+1} buffer of each peer rank (peer
+  // device memory over NVLink, opened through CUDA IPC), so no all-gather follows the kernel
+  int n_peers;
+  float* peer_next[kMaxPeers];
   std::uint32_t n, dim, ld;
   const std::uint32_t* rowptr;     // n+1
   const std::uint32_t* nbr;        // 2m, both directions

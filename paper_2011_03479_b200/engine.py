@@ -320,6 +320,28 @@ class Context:
     def bucket_received(self):
         self._check(self._L.gempe_bucket_received(self._h))
 
+    # fused update + broadcast over peer memory
+    def coords_ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        self._check(self._L.gempe_coords_ipc_handles(self._h, buf))
+        return buf.raw
+
+    def open_peer(self, handles: bytes):
+        self._check(self._L.gempe_open_peer(self._h, C.c_char_p(handles)))
+
+    def add_peer_pointers(self, x_parity0: int, x_parity1: int):
+        self._check(self._L.gempe_add_peer_pointers(self._h, C.c_void_p(x_parity0), C.c_void_p(x_parity1)))
+
+    def clear_peers(self):
+        self._check(self._L.gempe_clear_peers(self._h))
+
+    def device_coords_parity(self, parity: int) -> int:
+        return self._L.gempe_device_coords_parity(self._h, parity)
+
+    @property
+    def coords_parity(self) -> int:
+        return self._L.gempe_coords_parity(self._h)
+
     def gather_chunk(self, chunk: int):
         self._check(self._L.gempe_gather_chunk(self._h, chunk))
 

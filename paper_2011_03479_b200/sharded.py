@@ -11,6 +11,11 @@ with one equal-split all-to-all per round (8 bytes per sample; sampling work sca
 `exchange=False` every rank instead enumerates all sample streams and keeps the partners it owns (no exchange,
 replicated integer work).  The 2x512 tallies are summed with one all_reduce.
 
+`peer_broadcast=True` removes the all-gather altogether: the ranks open each other's coordinate buffers (CUDA IPC,
+peer memory over NVLink / NVSwitch) and the gather kernel stores every row it updates into all ranks' X_{t+1}
+directly -- the update and its broadcast are one kernel, the transfer rides under the remaining rows' compute.
+Between consecutive rounds the ranks pass a barrier (a one-element all_reduce, or the tally all_reduce).
+
 The collective logic is backend-agnostic (`ops` supplies the compute); tests drive it with gloo on CPU
 tensors, the product with `CudaShardOps` over NCCL.
 """
@@ -61,6 +66,18 @@ class CudaShardOps:
                 self._exchange = (as_t(send, (world, cap, 2)), as_t(recv, (world, cap, 2)),
                                   as_t(send_cnt, (world,)), as_t(recv_cnt, (world,)))
 
+    def connect_peers(self, group=None):
+        """Opens every other rank's coordinate buffers in this process (handles travel over the process group)."""
+        world = dist.get_world_size(group)
+        if world == 1:
+            return
+        mine = self.ctx.coords_ipc_handles()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        for r in range(world):
+            if r != dist.get_rank(group):
+                self.ctx.open_peer(handles[r])
+
     def exchange_tensors(self):
         """(send_records[world,cap,2], recv_records, send_counts[world], recv_counts) or None."""
         return self._exchange
@@ -110,9 +127,13 @@ class ShardedEngine:
     ops launch on."""
 
     def __init__(self, ops, n: int, m: int, world: int, rank: int, comm_chunks: int, group=None, stream=None,
-                 force_collectives: bool = False):
+                 force_collectives: bool = False, peer_broadcast: bool = False):
         self.ops, self.n, self.m, self.world, self.rank, self.chunks = ops, n, m, world, rank, comm_chunks
         self.group, self.stream = group, stream
+        # True: the compute backend stores updated rows into every rank's X_{t+1} itself (peer memory); the driver
+        # only separates consecutive rounds with a barrier
+        self.peer_broadcast = peer_broadcast and world > 1
+        self._flag = None
         # issue the collectives even for a single rank (exercises the NCCL plumbing on one GPU)
         self.collective = world > 1 or force_collectives
         self.block_rows, self.rows = block_layout(n, world, comm_chunks)
@@ -144,11 +165,24 @@ class ShardedEngine:
             span = self.world * self.block_rows
             for c in range(self.chunks):
                 self.ops.gather_chunk(c)
-                if self.collective:
+                if self.collective and not self.peer_broadcast:
                     region = x_next[c * span:(c + 1) * span]
                     mine = region[self.rank * self.block_rows:(self.rank + 1) * self.block_rows]
                     self._pending.append(dist.all_gather_into_tensor(region, mine, group=self.group, async_op=True))
             self.ops.end_round()
+            if self.peer_broadcast:
+                self._round_barrier()
+
+    def _round_barrier(self):
+        """No rank may start the next gather before every rank has finished this one (it reads what the peers wrote
+        and overwrites what they were reading)."""
+        if dist.get_backend(self.group) == "nccl":
+            if self._flag is None:
+                self._flag = torch.zeros(1, device="cuda")
+            self._pending.append(dist.all_reduce(self._flag, group=self.group, async_op=True))  # stream-ordered
+        else:  # host-side backend (gloo): drain the stream, then meet
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
 
     def finish_round(self):
         """Waits for the exchange and returns the job-wide tallies (edge[512], nonedge[512])."""
@@ -157,6 +191,8 @@ class ShardedEngine:
             self._wait_pending()
             t = self.ops.tallies()
             if self.collective:
+                if t.is_cuda and dist.get_backend(self.group) != "nccl":
+                    t = t.cpu()  # host-side backend
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         t = t.cpu().numpy().astype(np.uint64)
         return t[:HIST], t[HIST:]
@@ -192,6 +228,17 @@ class ShardedEngine:
         return pe, self.sigma
 
 
+def replicas_agree(x: torch.Tensor, group=None) -> bool:
+    """True when every rank holds bit-identical coordinates (all ranks keep the full X)."""
+    h = x.contiguous().view(torch.int32).to(torch.int64)
+    idx = torch.arange(h.numel(), device=h.device, dtype=torch.int64).view_as(h)
+    digest = torch.stack([h.sum(), (h * (idx % 8191 + 1)).sum()])
+    lo, hi = digest.clone(), digest.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    return bool(torch.equal(lo, hi))
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -201,17 +248,31 @@ class _Null:
 
 
 def make_cuda_engine(g: Graph, dim: int, seed: int, *, comm_chunks: int = 4, group=None, device: Optional[int] = None,
-                     force_collectives: bool = False, exchange: Optional[bool] = None, **ctx_kw) -> ShardedEngine:
+                     force_collectives: bool = False, exchange: Optional[bool] = None, peer_broadcast: bool = False,
+                     **ctx_kw) -> ShardedEngine:
     """One rank of a sharded engine over the default (NCCL) process group; world 1 without a group.
-    `exchange` (default: on when collectives are in use) selects sampling of own anchors + all-to-all."""
+    `exchange` (default: on when collectives are in use) selects sampling of own anchors + all-to-all;
+    `peer_broadcast` replaces the per-chunk all-gather by direct stores into the peers' buffers (one comm chunk)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     device = torch.cuda.current_device() if device is None else device
     chunks = comm_chunks if (world > 1 or force_collectives) else 1
+    if peer_broadcast and world > 1:
+        chunks = 1  # nothing to pipeline: the rows travel while the kernel runs
     if exchange is None:
         exchange = world > 1 or force_collectives
     if exchange:
         ctx_kw["exchange"] = 2 if (world == 1 and force_collectives) else 1  # 2: external exchange even for one rank
     ops = CudaShardOps(g, dim, seed, rank, world, chunks, device, **ctx_kw)
+    if peer_broadcast and world > 1:
+        # every rank must succeed (P2P-capable topology, IPC allowed) or none uses the path
+        ok = torch.ones(1, device=ops.device)
+        try:
+            ops.connect_peers(group)
+        except Exception:  # noqa: BLE001 - reported through the agreed flag
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() < 1:
+            raise RuntimeError("peer_broadcast: a rank could not open its peers' coordinate buffers (CUDA IPC / P2P)")
     return ShardedEngine(ops, g.n, g.edge_count(), world, rank, chunks, group=group, stream=ops.stream,
-                         force_collectives=force_collectives)
+                         force_collectives=force_collectives, peer_broadcast=peer_broadcast)

@@ -125,6 +125,106 @@ def test_rank_contexts_with_sample_exchange_reproduce_the_single_gpu_round(world
             c.close()
 
 
+@pytest.mark.parametrize("world,chunks,exchange", [(2, 1, 0), (4, 1, 1), (8, 2, 1), (16, 1, 0)])
+@pytest.mark.parametrize("mode,k", [(0, 0), (1, 6)])
+def test_fused_update_and_broadcast_into_peer_buffers(world, chunks, exchange, mode, k):
+    """Peer broadcast: the rank contexts of one process register each other's coordinate buffers and every gather
+    kernel stores the rows it updates into all of them -- no copy stands in for an all-gather here.  Ranks are stepped
+    one after another; after the last one every rank must hold the single-GPU X_{t+1} bit for bit."""
+    import torch
+    import paper_2011_03479_b200 as G
+    for (n, src, dst), dim in ((er_graph(1003, 6000, 3), 64), (er_graph(1003, 6000, 3), 128),
+                               (star_plus_ring(400, hubs=2), 2)):
+        g = G.Graph(n, src, dst)
+        single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
+        ranks = [G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64, rank=r,
+                           world=world, comm_chunks=chunks, exchange=exchange) for r in range(world)]
+        for a in ranks:
+            for b in ranks:
+                if a is not b:
+                    a.add_peer_pointers(b.device_coords_parity(0), b.device_coords_parity(1))
+        views = [_exchange_views(c, world) for c in ranks] if exchange else None
+        sigma = 1.0
+        for it in range(3):
+            he, hn = single.iterate(1.5, sigma, it)
+            want = single.get_coords()
+            for c in ranks:
+                c.begin_round(1.5, sigma, it)
+            if exchange:
+                torch.cuda.synchronize()
+                for s_rank in range(world):
+                    for d in range(world):
+                        views[d][1][s_rank].copy_(views[s_rank][0][d])
+                        views[d][3][s_rank] = views[s_rank][2][d]
+                torch.cuda.synchronize()
+            tot_e, tot_n = np.zeros(512, np.uint64), np.zeros(512, np.uint64)
+            for c in ranks:
+                assert c.coords_parity == it % 2
+                if exchange:
+                    c.bucket_received()
+                for ch in range(chunks):
+                    c.gather_chunk(ch)
+                e, nn = c.sync()
+                tot_e += e
+                tot_n += nn
+            assert np.array_equal(tot_e, he) and np.array_equal(tot_n, hn)
+            for c in ranks:
+                c.end_round()
+                assert np.array_equal(c.get_coords().view(np.uint32), want.view(np.uint32))
+            sigma *= 1.3
+        for c in ranks:
+            c.clear_peers()
+        for c in ranks + [single]:
+            c.close()
+
+
+def _ipc_worker(rank, world, port, results):
+    """One process per rank, all on cuda:0 (time-sliced; no kernel waits on another process): gloo carries the IPC
+    handles, the tallies and the barriers, the coordinates travel only through the peer stores of the gather kernel."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2011_03479_b200 as G
+        from paper_2011_03479_b200 import sharded
+        torch.cuda.set_device(0)
+        n, src, dst = er_graph(2003, 12000, 4)
+        g = G.Graph(n, src, dst)
+        eng = sharded.make_cuda_engine(g, 64, 5, device=0, neg_mode=1, negatives=6, deterministic=True,
+                                       exchange=False, peer_broadcast=True)
+        assert eng.peer_broadcast and eng.chunks == 1
+        plain = G.Context(g, 64, 5, neg_mode=1, negatives=6, deterministic=True)
+        ok = True
+        sigma = 1.0
+        for it in range(4):
+            eng.round_async(1.5, sigma, it)
+            he, hn = eng.finish_round()
+            he_w, hn_w = plain.iterate(1.5, sigma, it)
+            ok = ok and np.array_equal(he, he_w) and np.array_equal(hn, hn_w)
+            dist.barrier()
+            ok = ok and np.array_equal(eng.ops.ctx.get_coords().view(np.uint32), plain.get_coords().view(np.uint32))
+            dist.barrier()
+            sigma *= 1.2
+        eng.ops.ctx.clear_peers()
+        results[rank] = bool(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_broadcast_across_processes_over_cuda_ipc():
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_ipc_worker, args=(2, port, results), nprocs=2, join=True)
+    assert dict(results) == {0: True, 1: True}
+
+
 @pytest.mark.parametrize("exchange", [False, True])
 def test_nccl_plumbing_on_a_single_rank_group(exchange):
     """Real NCCL on one GPU: a 1-rank process group with the collectives forced on, three comm chunks.  Exercises

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--chunks", type=int, default=4)
     ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--peers", action="store_true",
+                    help="also time the fused update + broadcast with world-1 stand-in peer buffers in LOCAL memory "
+                         "(instruction and store-issue overhead only; NVLink is not involved on one GPU)")
     args = ap.parse_args()
     n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config, device="cuda:0")
     g = G.Graph(n, src, dst)
@@ -40,12 +43,18 @@ def main():
     stream = torch.cuda.Stream()
     rows = []
     for world in [int(w) for w in args.worlds.split(",")]:
-        for exchange in ([0] if world == 1 else [0, 1]):
-            chunks = 1 if world == 1 else args.chunks
+        for exchange, peers in ([(0, 0)] if world == 1 else [(0, 0), (1, 0)] + ([(1, 1)] if args.peers else [])):
+            chunks = 1 if (world == 1 or peers) else args.chunks
             ctx = G.Context(g, dim, 1, neg_mode=mode, negatives=k, rank=0, world=world, comm_chunks=chunks,
                             exchange=exchange)
             ctx.set_stream(stream.cuda_stream)
             ctx.init_coords(G.INIT_NORMAL, 1, 0.01)
+            dummies = []
+            if peers:
+                for _ in range(world - 1):
+                    dummies.append((torch.empty(ctx.padded_rows * ctx.row_stride, device="cuda:0"),
+                                    torch.empty(ctx.padded_rows * ctx.row_stride, device="cuda:0")))
+                    ctx.add_peer_pointers(dummies[-1][0].data_ptr(), dummies[-1][1].data_ptr())
             views = None
             if exchange:
                 send, recv, sc, rc, cap = ctx.exchange_layout()
@@ -68,14 +77,16 @@ def main():
                     cur = (ts + tb + tg, ts, tb, tg)
                     if it >= 2 and (best is None or cur[0] < best[0]):
                         best = cur
-            row = dict(config=args.config, world=world, exchange=exchange, chunks=chunks, total_ms=round(best[0], 3),
+            row = dict(config=args.config, world=world, exchange=exchange, peer_stores=peers, chunks=chunks, total_ms=round(best[0], 3),
                        sample_ms=round(best[1], 3), bucket_ms=round(best[2], 3), gather_ms=round(best[3], 3),
                        allgather_bytes_per_rank=int(ctx.padded_rows * ctx.row_stride * 4 * (world - 1) / world),
                        alltoall_bytes_per_rank=int(views[0].numel() * 4 * (world - 1) / world) if exchange else 0)
             print(json.dumps(row), flush=True)
             rows.append(row)
+            if peers:
+                ctx.clear_peers()
             ctx.close()
-            del ctx, views
+            del ctx, views, dummies
 
 
 if __name__ == "__main__":
