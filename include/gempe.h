@@ -70,7 +70,9 @@ typedef struct gempe_options {
                              A/B variants kept under test: 1 = row-at-a-time, 2 = warp per item also for d <= 4,
                              10 = cp.async shared-memory pipeline (16 < row stride <= 128) */
   int32_t bucket_mode;    /* incoming-sample bucketing: 0 = auto, 1 = per-partner atomics + scan + scatter,
-                             2 = two-level counting sort (streaming traffic only; auto for n >= 2^22) */
+                             2 = two-level counting sort (streaming traffic only),
+                             3 = one radix pass by contiguous vertex range, then per-partner atomics range by range
+                                 (auto for n >= 2^22 on one rank) */
   int32_t exchange;       /* sharded sampling: 0 = every rank enumerates all sample streams and keeps the partners it
                              owns (no exchange step); 1 = a rank samples only the streams of its own anchors, packs
                              (partner, anchor) records per destination rank and the ranks exchange them with one

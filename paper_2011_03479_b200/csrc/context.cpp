@@ -212,13 +212,14 @@ void build_structures(gempe_ctx* c) {
   c->slots = per_edge ? 2 * m : static_cast<std::uint64_t>(n) * c->opt.negatives;
   c->neg_own.allocate(c->slots);
   c->in_anchor.allocate(c->slots);
-  // bucketing method: per-partner atomics while the per-vertex counters fit L2 comfortably, else the two-level
-  // counting sort (opt.bucket_mode: 0 auto, 1 atomics, 2 counting sort)
+  // bucketing method (opt.bucket_mode): 1 = per-partner atomics (auto while the per-vertex counters fit L2
+  // comfortably), 3 = radix pass by vertex range + atomics range by range (auto for n >= 2^22 on one rank),
+  // 2 = two-level counting sort (kept for A/B runs)
   c->partition = PartitionArgs{};
   std::uint32_t shift = 8;
   while ((static_cast<std::uint64_t>(n) + (1ull << shift) - 1) >> shift > 4096) ++shift;
   const bool can_partition = shift <= 15 && c->slots > 0;
-  const bool want_partition = c->opt.bucket_mode == 2 || (c->opt.bucket_mode == 0 && n >= (1u << 22));
+  const bool want_partition = c->opt.bucket_mode == 2;
   if (can_partition && want_partition) {
     c->partition.shift = shift;
     c->partition.buckets = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) + (1ull << shift) - 1) >> shift);
@@ -241,7 +242,12 @@ void build_structures(gempe_ctx* c) {
   c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
   c->scan_scratch.allocate((n + 4095) / 4096 + 2);
   c->exchange = ExchangeArgs{};
-  if (c->opt.exchange) {
+  // bucket_mode 3 (one rank): the pack / bucket kernels of the exchange path with contiguous vertex ranges as the
+  // destinations -- one radix pass by range, then per-partner atomics whose counters stay L2-resident range by range
+  const bool region_mode = (c->opt.bucket_mode == 3 || (c->opt.bucket_mode == 0 && n >= (1u << 22))) && world == 1 &&
+                           !c->opt.exchange && c->slots > 0;
+  c->pack_path = c->opt.exchange != 0 || region_mode;
+  if (c->pack_path) {
     // own sample streams per rank: the anchors of block b = chunk * world + r belong to rank r.  Every rank derives the
     // same per-(source, destination) capacity from the busiest rank, so the all-to-all is an equal split.
     auto first_slot_of = [&](std::uint64_t v) { return per_edge ? static_cast<std::uint64_t>(rowptr[v]) : v * c->opt.negatives; };
@@ -259,24 +265,36 @@ void build_structures(gempe_ctx* c) {
         }
       }
     }
+    std::uint32_t regions = world, region_rows = 0;
+    double share = n ? static_cast<double>(*std::max_element(own_rows.begin(), own_rows.end())) / n : 1.0;
+    if (region_mode) {
+      std::uint64_t range_bytes = 4u << 20;  // counters per range (c5: 16.6 ms at 4 MB, 18.0 at 2, 20.9 at 8, 27 at 32)
+      if (const char* e = std::getenv("GEMPE_REGION_MB")) range_bytes = std::max(1, std::atoi(e)) * (1ull << 20);
+      regions = static_cast<std::uint32_t>(std::min<std::uint64_t>(256, std::max<std::uint64_t>(1, (4ull * n + range_bytes - 1) / range_bytes)));
+      region_rows = (n + regions - 1) / regions;
+      regions = (n + region_rows - 1) / region_rows;
+      share = static_cast<double>(region_rows) / n;
+    }
     const std::uint64_t busiest = *std::max_element(own_slots.begin(), own_slots.end());
-    const double share = n ? static_cast<double>(*std::max_element(own_rows.begin(), own_rows.end())) / n : 1.0;
     const double expect = 1.25 * static_cast<double>(busiest) * share;  // partners are ~uniform over vertices
     const std::uint64_t cap = std::min<std::uint64_t>(busiest, static_cast<std::uint64_t>(expect + 8.0 * std::sqrt(expect)) + 1024);
-    if (cap * world > 0xffffffffull) throw config_error("exchange regions exceed 2^32 records; use more ranks");
+    if (cap * regions > 0xffffffffull) throw config_error("exchange regions exceed 2^32 records; use more ranks");
     c->ex_first_slot.upload(first);
     c->ex_prefix.upload(prefix);
-    const bool external = world > 1 || c->opt.exchange == 2;
-    c->ex_send.allocate(static_cast<std::size_t>(cap) * world);
-    if (external) c->ex_recv.allocate(static_cast<std::size_t>(cap) * world); else c->ex_recv.release();
-    c->ex_send_count.allocate(world, true);
-    if (external) c->ex_recv_count.allocate(world, true); else c->ex_recv_count.release();
-    c->ex_rank.allocate(static_cast<std::size_t>(cap) * world);
+    const bool external = !region_mode && (world > 1 || c->opt.exchange == 2);
+    c->ex_send.allocate(static_cast<std::size_t>(cap) * regions);
+    if (external) c->ex_recv.allocate(static_cast<std::size_t>(cap) * regions); else c->ex_recv.release();
+    c->ex_send_count.allocate(regions, true);
+    if (external) c->ex_recv_count.allocate(regions, true); else c->ex_recv_count.release();
+    c->ex_rank.allocate(static_cast<std::size_t>(cap) * regions);
     if (c->in_cnt.size() == 0) c->in_cnt.allocate(n);
+    c->in_rank.release();  // arrival ranks live beside the records here
     c->exchange.own_slots = prefix.back();
     c->exchange.ranges = c->comm_chunks;
     c->exchange.first_slot = c->ex_first_slot.get();
     c->exchange.prefix = c->ex_prefix.get();
+    c->exchange.regions = regions;
+    c->exchange.region_rows = region_rows;
     c->exchange.capacity = static_cast<std::uint32_t>(cap);
     c->exchange.send = c->ex_send.get();
     c->exchange.send_count = c->ex_send_count.get();
@@ -345,9 +363,9 @@ void require_live(gempe_ctx* c) {
 
 // exchange path, second half: bucket the (partner, anchor) records received from all ranks by partner
 void bucket_received(gempe_ctx* c) {
-  if (!c->opt.exchange) throw config_error("context was created without opt.exchange");
+  if (!c->pack_path) throw config_error("context was created without opt.exchange");
   if (!c->bucket_pending) throw config_error("gempe_bucket_received without a preceding gempe_begin_round");
-  c->launches += launch_bucket_records(c->exchange, static_cast<std::uint32_t>(c->opt.world), c->n, c->in_cnt.get(),
+  c->launches += launch_bucket_records(c->exchange, c->exchange.regions, c->n, c->in_cnt.get(),
                                        c->in_off.get(), c->ex_rank.get(), c->in_anchor.get(), c->scan_scratch.get(), c->stream);
   if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
   cuda_check(cudaGetLastError(), "bucket received records");
@@ -358,7 +376,7 @@ void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
   cuda_check(cudaMemsetAsync(c->status.get(), 0, 8 * sizeof(std::uint32_t), c->stream), "memset status");
   cuda_check(cudaMemsetAsync(c->hist.get(), 0, 2 * kBins * sizeof(unsigned long long), c->stream), "memset hist");
   const SampleArgs a = sample_args(c, iter);
-  if (c->opt.exchange) {
+  if (c->pack_path) {
     c->launches += launch_sample_pack(a, c->exchange, c->stream);
     cuda_check(cudaGetLastError(), "sample + pack");
     c->bucket_pending = true;

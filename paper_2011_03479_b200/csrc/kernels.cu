@@ -202,20 +202,20 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
     const std::uint64_t t = x.first_slot[c] + (i - x.prefix[c]);
     partner = sample_slot(a, t, anchor, draws);
     a.neg_own[t] = partner;
-    dest = (partner / a.own.block_rows) % a.own.world;
+    dest = x.region_rows ? partner / x.region_rows : (partner / a.own.block_rows) % a.own.world;
     have = true;
   }
   add_draws(a, draws);
   // one global atomic per destination rank and BLOCK: ranks within the block come from shared counters
-  extern __shared__ std::uint32_t sh_pack[];  // [world] counts, then [world] bases
+  extern __shared__ std::uint32_t sh_pack[];  // [regions] counts, then [regions] bases
   std::uint32_t* sh_cnt = sh_pack;
-  std::uint32_t* sh_base = sh_pack + a.own.world;
-  for (std::uint32_t d = threadIdx.x; d < a.own.world; d += blockDim.x) sh_cnt[d] = 0;
+  std::uint32_t* sh_base = sh_pack + x.regions;
+  for (std::uint32_t d = threadIdx.x; d < x.regions; d += blockDim.x) sh_cnt[d] = 0;
   __syncthreads();
   std::uint32_t local = 0;
   if (have) local = atomicAdd(sh_cnt + dest, 1u);
   __syncthreads();
-  for (std::uint32_t d = threadIdx.x; d < a.own.world; d += blockDim.x) {
+  for (std::uint32_t d = threadIdx.x; d < x.regions; d += blockDim.x) {
     sh_base[d] = sh_cnt[d] ? atomicAdd(x.send_count + d, sh_cnt[d]) : 0u;
   }
   __syncthreads();
@@ -229,25 +229,23 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
   }
 }
 
-// received records -> per-partner counts and arrival ranks
-__global__ void __launch_bounds__(kThreads) count_records_kernel(const ExchangeArgs x, std::uint32_t world,
-                                                                 std::uint32_t* __restrict__ in_cnt,
+// received records -> per-partner counts and arrival ranks.  blockIdx.y = source region: the regions are walked one
+// after another, so with contiguous vertex ranges the counters touched at any time are one range's (L2-resident).
+__global__ void __launch_bounds__(kThreads) count_records_kernel(const ExchangeArgs x, std::uint32_t* __restrict__ in_cnt,
                                                                  std::uint32_t* __restrict__ rec_rank) {
-  const std::uint64_t idx = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<std::uint64_t>(world) * x.capacity) return;
-  const std::uint32_t from = static_cast<std::uint32_t>(idx / x.capacity), j = static_cast<std::uint32_t>(idx % x.capacity);
+  const std::uint32_t from = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= min(x.recv_count[from], x.capacity)) return;
+  const std::size_t idx = static_cast<std::size_t>(from) * x.capacity + j;
   rec_rank[idx] = atomicAdd(in_cnt + x.recv[idx].x, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads) scatter_records_kernel(const ExchangeArgs x, std::uint32_t world,
+__global__ void __launch_bounds__(kThreads) scatter_records_kernel(const ExchangeArgs x,
                                                                    const std::uint32_t* __restrict__ rec_rank,
                                                                    const std::uint32_t* __restrict__ in_off,
                                                                    std::uint32_t* __restrict__ in_anchor) {
-  const std::uint64_t idx = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<std::uint64_t>(world) * x.capacity) return;
-  const std::uint32_t from = static_cast<std::uint32_t>(idx / x.capacity), j = static_cast<std::uint32_t>(idx % x.capacity);
+  const std::uint32_t from = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= min(x.recv_count[from], x.capacity)) return;
+  const std::size_t idx = static_cast<std::size_t>(from) * x.capacity + j;
   const uint2 rec = x.recv[idx];
   in_anchor[in_off[rec.x] + rec_rank[idx]] = rec.y;
 }
@@ -2089,25 +2087,25 @@ int launch_sample(const SampleArgs& a, cudaStream_t stream) {
 }
 
 int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream) {
-  cudaMemsetAsync(x.send_count, 0, a.own.world * sizeof(std::uint32_t), stream);
+  cudaMemsetAsync(x.send_count, 0, x.regions * sizeof(std::uint32_t), stream);
   if (x.own_slots == 0) return 0;
-  sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 2 * a.own.world * sizeof(std::uint32_t), stream>>>(a, x);
+  sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 2 * x.regions * sizeof(std::uint32_t), stream>>>(a, x);
   return 1;
 }
 
-int launch_bucket_records(const ExchangeArgs& x, std::uint32_t world, std::uint32_t n, std::uint32_t* in_cnt,
+int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uint32_t n, std::uint32_t* in_cnt,
                           std::uint32_t* in_off, std::uint32_t* rec_rank, std::uint32_t* in_anchor, std::uint32_t* scratch,
                           cudaStream_t stream) {
-  const std::uint64_t total = static_cast<std::uint64_t>(world) * x.capacity;
   cudaMemsetAsync(in_cnt, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
   int launches = 0;
-  if (total) {
-    count_records_kernel<<<blocks_for(total, kThreads), kThreads, 0, stream>>>(x, world, in_cnt, rec_rank);
+  const dim3 grid(blocks_for(x.capacity, kThreads), sources);
+  if (x.capacity) {
+    count_records_kernel<<<grid, kThreads, 0, stream>>>(x, in_cnt, rec_rank);
     ++launches;
   }
   launches += launch_scan(in_cnt, in_off, n, scratch, stream);
-  if (total) {
-    scatter_records_kernel<<<blocks_for(total, kThreads), kThreads, 0, stream>>>(x, world, rec_rank, in_off, in_anchor);
+  if (x.capacity) {
+    scatter_records_kernel<<<grid, kThreads, 0, stream>>>(x, rec_rank, in_off, in_anchor);
     ++launches;
   }
   return launches;

@@ -75,6 +75,8 @@ struct ExchangeArgs {
   std::uint32_t ranges;              // owned blocks (comm chunks)
   const std::uint64_t* first_slot;   // [ranges] global slot id of the first own slot of block c
   const std::uint64_t* prefix;       // [ranges + 1] own slots before block c
+  std::uint32_t regions;             // destinations: the ranks (exchange), or contiguous vertex ranges of one rank
+  std::uint32_t region_rows;         // 0: destination = owner rank of the partner; else destination = partner / region_rows
   std::uint32_t capacity;            // records per (source, destination) region
   uint2* send;                       // [world][capacity]
   std::uint32_t* send_count;         // [world]
@@ -140,7 +142,7 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
                  cudaStream_t stream);
 int launch_sample(const SampleArgs& a, cudaStream_t stream);
 int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream);
-int launch_bucket_records(const ExchangeArgs& x, std::uint32_t world, std::uint32_t n, std::uint32_t* in_cnt,
+int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uint32_t n, std::uint32_t* in_cnt,
                           std::uint32_t* in_off, std::uint32_t* rec_rank, std::uint32_t* in_anchor, std::uint32_t* scratch,
                           cudaStream_t stream);
 std::uint32_t partition_grid(std::uint64_t slots);

@@ -188,13 +188,30 @@ def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim, kernel)
                 **KERNELS[kernel])
 
 
-@pytest.mark.parametrize("bucket_mode", [1, 2])
+@pytest.mark.parametrize("bucket_mode", [1, 2, 3])
 @pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5), (1, 20)])
 def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k, bucket_mode):
     for dim in (2, 64, 128):
         check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, neg_mode=neg_mode, k=k,
                     exact=exact, iters=3, bucket_mode=bucket_mode)
+
+
+def test_range_bucketing_with_several_ranges(G, monkeypatch):
+    """bucket_mode 3 with more than one vertex range (1 MB of counters per range here): same buckets as the atomics."""
+    monkeypatch.setenv("GEMPE_REGION_MB", "1")
+    n = 700_001  # 2.8 MB of counters -> 3 ranges, the last one short
+    _, src, dst = er_graph(n, 2 * n, 13)
+    outs = []
+    for mode in (1, 3):
+        ctx = G.Context(G.Graph(n, src, dst), 4, 3, neg_mode=1, negatives=3, deterministic=True, bucket_mode=mode)
+        partners, draws = ctx.sample(1)
+        he, hn = ctx.iterate(1.5, 1.0, 1)
+        outs.append((ctx.get_coords(), he, hn, partners, draws))
+        ctx.close()
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+    assert np.array_equal(outs[0][3], outs[1][3]) and outs[0][4] == outs[1][4]
 
 
 @pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5)])
@@ -220,18 +237,19 @@ def test_round_parity_with_the_exchange_path(G, oracle, golden_fastmath, neg_mod
 
 @pytest.mark.parametrize("n", [300, 5000, 70001])
 def test_counting_sort_buckets_equal_atomic_buckets(G, n):
-    """Both bucketing methods must hand the gather the same multiset of incoming anchors per vertex: with
+    """All bucketing methods must hand the gather the same multiset of incoming anchors per vertex: with
     sorted buckets (deterministic mode) the rounds are bit-identical."""
     _, src, dst = er_graph(n, 4 * n, 11)
     outs = []
-    for mode in (1, 2):
+    for mode in (1, 2, 3):
         ctx = G.Context(G.Graph(n, src, dst), 8, 3, neg_mode=1, negatives=9, deterministic=True, bucket_mode=mode)
         for it in range(2):
             he, hn = ctx.iterate(1.5, 1.0, it)
         outs.append((ctx.get_coords(), he, hn))
         ctx.close()
-    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
-    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+    for other in outs[1:]:
+        assert np.array_equal(outs[0][0].view(np.uint32), other[0].view(np.uint32))
+        assert np.array_equal(outs[0][1], other[1]) and np.array_equal(outs[0][2], other[2])
 
 
 @pytest.mark.parametrize("dim", [2, 64, 128])
