@@ -308,8 +308,12 @@ void build_structures(gempe_ctx* c) {
   c->hash_bits = auto_hash_bits(m, c->opt.hash_bits);
   const std::uint64_t cells = 1ull << c->hash_bits;
   c->hash_words.allocate(std::max<std::uint64_t>(1, cells / 32), true);
+  // a sparse table beyond what L2 keeps (c4: 128 MB, 3 % of the cells set) gets a 4x smaller "any cell of the group
+  // set" summary in front of it; dense or small tables do not
+  const bool summarise = cells / 8 > (64ull << 20) && 2 * m <= cells / 16;
+  if (summarise) c->hash_summary.allocate(cells >> (5 + kHashSummaryShift), true); else c->hash_summary.release();
   c->launches += launch_hash_build(c->tmp_src.get(), c->tmp_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
-                                   c->hash_words.get(), c->stream);
+                                   c->hash_words.get(), summarise ? c->hash_summary.get() : nullptr, c->stream);
   cuda_check(cudaStreamSynchronize(c->stream), "hash build");
   c->tmp_src.release();
   c->tmp_dst.release();
@@ -348,6 +352,7 @@ SampleArgs sample_args(gempe_ctx* c, std::uint64_t iter) {
   a.csr_src = c->csr_src.get();
   a.eid_role = c->eid_role.get();
   a.hash_words = c->hash_words.get();
+  a.hash_summary = c->hash_summary.size() ? c->hash_summary.get() : nullptr;
   a.hash_mask = static_cast<std::uint32_t>((1ull << c->hash_bits) - 1);
   a.neg_own = c->neg_own.get();
   a.in_cnt = c->in_cnt.get();

@@ -80,7 +80,7 @@ struct gempe_ctx {
   int cur = 0;
   gempe::DeviceBuffer<std::uint32_t> rowptr, nbr, eid_role, csr_src;
   gempe::DeviceBuffer<std::uint32_t> tmp_src, tmp_dst;  // work edge arrays on the device during construction only
-  gempe::DeviceBuffer<std::uint32_t> hash_words;
+  gempe::DeviceBuffer<std::uint32_t> hash_words, hash_summary;
   gempe::DeviceBuffer<std::uint32_t> neg_own, in_cnt, in_off, in_rank, in_anchor, scan_scratch;
   // large-n bucketing (two-level counting sort); partition.buckets == 0 selects the atomic method
   gempe::PartitionArgs partition{};

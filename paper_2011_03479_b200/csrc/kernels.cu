@@ -35,17 +35,36 @@ __device__ __forceinline__ bool hash_test(const std::uint32_t* __restrict__ word
   return (__ldg(words + (h >> 5)) >> (h & 31u)) & 1u;
 }
 
+// Same answer through the summary bitmap (bit g = "some cell of group g is set", kSummaryGroup cells per group): a
+// sparse table that does not fit L2 is consulted only for the minority of probes whose group is occupied.
+constexpr int kSummaryShift = kHashSummaryShift;
+__device__ __forceinline__ bool hash_test(const std::uint32_t* __restrict__ words,
+                                          const std::uint32_t* __restrict__ summary, std::uint32_t mask,
+                                          std::uint32_t n, std::uint32_t i, std::uint32_t j) {
+  const std::uint32_t h = pair_hash(i, j, n, mask);
+  if (summary) {
+    const std::uint32_t g = h >> kSummaryShift;
+    if (!((__ldg(summary + (g >> 5)) >> (g & 31u)) & 1u)) return false;
+  }
+  return (__ldg(words + (h >> 5)) >> (h & 31u)) & 1u;
+}
+
 // ---------------------------------------------------------------------------------- hash set
 
 __global__ void hash_build_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst,
                                   std::uint64_t m, std::uint32_t n, std::uint32_t mask,
-                                  std::uint32_t* __restrict__ words) {
+                                  std::uint32_t* __restrict__ words, std::uint32_t* __restrict__ summary) {
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
   for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
     const std::uint32_t i = src[e], j = dst[e];
     const std::uint32_t h0 = pair_hash(i, j, n, mask), h1 = pair_hash(j, i, n, mask);
     atomicOr(words + (h0 >> 5), 1u << (h0 & 31u));
     atomicOr(words + (h1 >> 5), 1u << (h1 & 31u));
+    if (summary) {
+      const std::uint32_t g0 = h0 >> kSummaryShift, g1 = h1 >> kSummaryShift;
+      atomicOr(summary + (g0 >> 5), 1u << (g0 & 31u));
+      atomicOr(summary + (g1 >> 5), 1u << (g1 & 31u));
+    }
   }
 }
 
@@ -123,7 +142,7 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
       ++draws;
       const std::uint32_t g = uniform_index(s, a.n);
       if (g == anchor) continue;
-      if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
+      if (hash_test(a.hash_words, a.hash_summary, a.hash_mask, a.n, anchor, g)) continue;
       return g;
     }
   } else {
@@ -136,7 +155,7 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
         ++draws;
         const std::uint32_t g = static_cast<std::uint32_t>((static_cast<std::uint64_t>(ctr[q]) * a.n) >> 32);
         if (g == anchor) continue;
-        if (hash_test(a.hash_words, a.hash_mask, a.n, anchor, g)) continue;
+        if (hash_test(a.hash_words, a.hash_summary, a.hash_mask, a.n, anchor, g)) continue;
         return g;
       }
     }
@@ -2046,10 +2065,10 @@ inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
 // ---------------------------------------------------------------------------------- launchers
 
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
-                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream) {
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream) {
   if (m == 0) return 0;
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
-  hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words);
+  hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words, hash_summary);
   return 1;
 }
 

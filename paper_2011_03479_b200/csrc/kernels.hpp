@@ -60,6 +60,7 @@ struct SampleArgs {
   const std::uint32_t* csr_src;   // PER_EDGE_2: anchor of each CSR position
   const std::uint32_t* eid_role;  // PER_EDGE_2: 2*edge + role (role 0: anchor is src[e], 1: dst[e])
   const std::uint32_t* hash_words;  // bit-packed direct-mapped table, 2^bits bits
+  const std::uint32_t* hash_summary;  // optional: one bit per 4 cells ("any set"), null when the table itself fits L2
   std::uint32_t hash_mask;        // 2^bits - 1
   std::uint32_t* neg_own;         // out: accepted partner per slot
   std::uint32_t* in_cnt;          // in/out: per-vertex count of incoming samples (zeroed before)
@@ -130,7 +131,8 @@ struct GatherArgs {
 
 // ---- launchers (all asynchronous on `stream`; return the number of kernels launched) ---------------
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
-                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream);
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream);
+constexpr int kHashSummaryShift = 2;  // cells per summary bit = 4 (kernels.cu: kSummaryShift)
 // construction on the device: relabel application and the both-direction CSR (row order = atomic arrival order)
 int launch_relabel_apply(std::uint32_t* src, std::uint32_t* dst, std::uint64_t m, const std::uint32_t* forward,
                          cudaStream_t stream);

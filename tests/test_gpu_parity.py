@@ -564,6 +564,25 @@ def test_unrelabelled_context_and_hash_bits_extremes(G, oracle, golden_fastmath)
         ctx.close()
 
 
+def test_large_sparse_table_goes_through_the_summary_bitmap(G, oracle, golden_fastmath):
+    """A 2^30-cell table (128 MB bit-packed, far from full) is fronted by the "any cell of the group set" summary in
+    the sampler; the streams and draw counts must still be the reference's bit for bit.  A dense complete-bipartite
+    block makes real rejections (and table collisions) frequent."""
+    n = 3000
+    a, b = np.meshgrid(np.arange(0, 600, dtype=np.uint32), np.arange(600, 1500, dtype=np.uint32))
+    src, dst = a.ravel(), b.ravel()  # 540 000 edges, vertices 0..599 adjacent to 30 % of the graph
+    ctx = G.Context(G.Graph(n, src, dst), 2, 11, hash_bits=30)
+    ws, wd, _ = ctx.work_graph()
+    table = oracle.hash_build(n, ws, wd, 30)
+    x = ctx.get_coords()
+    for it in (0, 3):
+        got, draws = ctx.sample(it)
+        want = oracle.iterate(n, ws, wd, x, 0, 0, 11, it, 1.5, 1.0, golden_fastmath, table)
+        assert np.array_equal(got, want["partners"]) and draws == want["draws"]
+        assert draws > 1.15 * len(got)  # rejections did happen
+    ctx.close()
+
+
 def test_zero_negatives_per_vertex_and_large_k(G, oracle, golden_fastmath):
     n, src, dst = er_graph(150, 500, 8)
     ctx = G.Context(G.Graph(n, src, dst), 8, 2, neg_mode=1, negatives=0)
