@@ -39,7 +39,8 @@ def parse():
     p.add_argument("--chunk-entries", type=int, default=0)
     p.add_argument("--bucket-mode", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=3)
-    p.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline budget on rank 0")
+    p.add_argument("--cpu-seconds", type=float, default=None,
+                   help="CPU budget on rank 0 (default: 20 s for the cpu_baseline leg, 30 s for --impl reference)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--peer-broadcast", default="auto", choices=["auto", "off"],
                    help="N > 1: gather kernel stores updated rows into the peers' buffers (auto) or NCCL all-gather (off)")
@@ -141,7 +142,7 @@ def main():
         if rank != 0:
             return
         n, src, dst, dim, k, _, _, _ = graphgen.make_config(args.config, device=gen_device())
-        base = cpu_reference_arm(n, src, dst, dim, max(args.cpu_seconds, 30.0), steps=args.steps, warmup=args.warmup)
+        base = cpu_reference_arm(n, src, dst, dim, args.cpu_seconds or 30.0, steps=args.steps, warmup=args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["sample_ms_per_round"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -328,7 +329,7 @@ def main():
                        "call": "gempe_step_host: X_t in, round, X_{t+1} + tallies out (pinned host buffers, copies overlapped)"}
         if not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_reference_arm(n, src, dst, dim, args.cpu_seconds)
+                line["cpu_baseline"] = cpu_reference_arm(n, src, dst, dim, args.cpu_seconds or 20.0)
             except Exception as e:  # the reference build is test infrastructure; its absence is reported, not fatal
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
