@@ -10,9 +10,11 @@
 //                             (engine.cpp:45-73, 253-276, sigmoid.hpp:88-101, histogram.hpp:24-29)
 #include "kernels.hpp"
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "device_fns.cuh"
@@ -2056,6 +2058,149 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
   }
 }
 
+// The same search on a cluster of 8 CTAs (8 SMs): one evaluation of the objective is bound by the FP64 throughput of
+// ONE SM, and the search is ~38 of them in a row.  Here every CTA owns all 512 bins and evaluates a DIFFERENT candidate:
+// the 17-point scan takes one round of <= 3 evaluations per CTA, and the bisection is walked speculatively, the 7 nodes
+// of the next three levels at once (each CTA derives its node's interval with the same arithmetic the sequential walk
+// uses, so every visited midpoint and therefore sigma is bit-identical to sigma_update_kernel).  Results travel
+// through distributed shared memory: thread 0 stores its block sum into every CTA's mailbox, cluster.sync() orders it.
+constexpr int kSigmaCtas = 8;
+__global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
+    sigma_update_cluster_kernel(const unsigned long long* __restrict__ hist, double mu, double pairs, double edges,
+                                int exact_math, SigmaState* __restrict__ state) {
+  using namespace sigma;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cta = static_cast<int>(cluster.block_rank());
+  __shared__ double scratch[kBins / 32];
+  __shared__ double mailbox[2][24];
+  const int b = threadIdx.x;
+  const double ec = static_cast<double>(hist[b]), nc = static_cast<double>(hist[kBins + b]);
+  const double mid = (b + 0.5) * 12.0 / kBins;
+  const double cap = state->sigma * 1.5;  // read before anybody writes the state (CTA 0, after the last sync)
+  const double samples = block_sum(nc, scratch);
+  const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;
+  auto total = [&](double s, int which) {
+    double v = 0.0;
+    if (which == 0) {
+      if (ec != 0.0) v += ec * cost_tail(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_tail(mid, mu, s, false);
+    } else if (which == 1) {
+      if (ec != 0.0) v += ec * cost_dsigma(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_dsigma(mid, mu, s, false);
+    } else {
+      if (ec != 0.0) v += ec * cost_floor(mid, mu, s, true);
+      if (nc != 0.0) v += nw * nc * cost_floor(mid, mu, s, false);
+    }
+    return block_sum(v, scratch);
+  };
+  int parity = 0;
+  auto post = [&](int slot, double v) {
+    if (b == 0) {
+      for (int r = 0; r < kSigmaCtas; ++r) *cluster.map_shared_rank(&mailbox[parity][slot], r) = v;
+    }
+  };
+
+  // round 0: coarse geometric scan
+  constexpr int kGrid = 17;
+  double grid[kGrid];
+#pragma unroll 1
+  for (int i = 0; i < kGrid; ++i) grid[i] = 1e-3 * pow(16.0 / 1e-3, static_cast<double>(i) / (kGrid - 1));
+#pragma unroll 1
+  for (int i = cta; i < kGrid; i += kSigmaCtas) post(i, total(grid[i], 0));
+  cluster.sync();
+  double best_cost = 0.0;
+  int best = 0;
+  for (int i = 0; i < kGrid; ++i) {
+    const double t = mailbox[parity][i];
+    if (i == 0 || t < best_cost) best_cost = t, best = i;
+  }
+  parity ^= 1;
+  double sigma_opt = grid[best];
+  double lo = grid[best > 0 ? best - 1 : 0], hi = grid[best < kGrid - 1 ? best + 1 : kGrid - 1];
+
+  // interval of heap node k (children of k: 2k+1 = left half, 2k+2 = right half) below (lo, hi)
+  auto node_mid = [&](int k) {
+    int path[3], depth = 0;
+    for (int q = k; q > 0; q = (q - 1) >> 1) path[depth++] = (q & 1) ? 0 : 1;
+    double nlo = lo, nhi = hi;
+    for (int d = depth - 1; d >= 0; --d) {
+      const double m = 0.5 * (nlo + nhi);
+      if (path[d]) nlo = m; else nhi = m;
+    }
+    return 0.5 * (nlo + nhi);
+  };
+  int steps = 0;
+  bool open = true;  // the bisection loop of optimize_sigma_detail is still running
+  // consumes up to `levels` levels of the posted tree (slots base .. base + 2^levels - 2)
+  auto walk = [&](int levels, int base) {
+    int k = 0;
+    for (int l = 0; l < levels && open; ++l) {
+      if (!(hi - lo > 1e-4 && steps < 60)) {
+        open = false;
+        break;
+      }
+      ++steps;
+      const double m = 0.5 * (lo + hi);
+      const double f_mid = mailbox[parity][base + k];
+      if (f_mid == 0.0) {
+        lo = hi = m;
+        open = false;
+        break;
+      }
+      if ((f_mid > 0.0) == false) {  // same sign as f_lo (< 0 throughout): move the lower end
+        lo = m;
+        k = 2 * k + 2;
+      } else {
+        hi = m;
+        k = 2 * k + 1;
+      }
+    }
+  };
+
+  // round 1: the derivative at both ends and the first two levels
+  if (cta == 0) post(0, total(lo, 1));
+  else if (cta == 1) post(1, total(hi, 1));
+  else if (cta < 5) post(cta, total(node_mid(cta - 2), 1));
+  cluster.sync();
+  const bool bisect = mailbox[parity][0] < 0.0 && mailbox[parity][1] > 0.0;
+  if (bisect) walk(2, 2); else open = false;
+  parity ^= 1;
+  while (open && hi - lo > 1e-4 && steps < 60) {
+    if (cta < 7) post(cta, total(node_mid(cta), 1));
+    cluster.sync();
+    walk(3, 0);
+    parity ^= 1;
+  }
+
+  // last round: acceptance test and the PE estimate of either outcome
+  const double refined = 0.5 * (lo + hi);
+  if (cta == 0) post(0, bisect ? total(refined, 0) : 0.0);
+  else if (cta == 1) post(1, total(fmin(refined, cap), 2));
+  else if (cta == 2) post(2, total(fmin(grid[best], cap), 2));
+  cluster.sync();
+  double pe_sum = mailbox[parity][2];
+  if (bisect && mailbox[parity][0] <= best_cost) {
+    sigma_opt = refined;
+    pe_sum = mailbox[parity][1];
+  }
+  const double sigma_new = fmin(sigma_opt, cap);  // growth cap, engine.cpp:302-307
+  if (cta == 0 && b == 0) {
+    const double c1 = 2.0 / (3.14159265358979323846264338327950288 * kLn2);
+    const double c2 = 1.0 / (2.50662827463100050241576528481 * kLn2);
+    state->sigma = sigma_new;
+    state->pe_estimate = pe_sum / pairs;
+    state->nonedge_weight = nw;
+    state->bisection_steps = steps;
+    state->math.mu = mu;
+    state->math.inv_sqrt2_sigma = 1.0 / (kSqrt2 * sigma_new);
+    state->math.A = c1 / (sigma_new * sigma_new);
+    state->math.B = c2 / (sigma_new * sigma_new * sigma_new);
+    state->math.C = c2 / sigma_new;
+    state->math.exact = exact_math;
+  }
+}
+
 inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
   return static_cast<unsigned>((work + per_block - 1) / per_block);
 }
@@ -2320,7 +2465,9 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
 
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
                         SigmaState* state, cudaStream_t stream) {
-  sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
+  const bool single_block = std::getenv("GEMPE_SIGMA_SINGLE_BLOCK") != nullptr;  // A/B switch, read per call
+  if (single_block) sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
+  else sigma_update_cluster_kernel<<<kSigmaCtas, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
   return 1;
 }
 
