@@ -464,6 +464,45 @@ def test_config4_size_properties(G):
     ctx.close()
 
 
+def test_config5_size_properties(G):
+    """BASELINE config 5 (R-MAT scale 24: n = 16.7 M, m = 260 M, d = 128, k = 20 -- the largest size): tallies count every
+    pair once, sampled partners are valid non-edges, and the round does not depend on the bucketing method (range
+    bucketing over 16 vertex ranges vs. plain per-partner atomics, sorted buckets: bit-identical coordinates)."""
+    import torch
+    from paper_2011_03479_b200 import graphgen
+    from paper_2011_03479_b200.sharded import _DeviceArray
+    if torch.cuda.mem_get_info()[1] < 150e9:
+        pytest.skip("needs a 180 GB part")
+    n, src, dst, dim, k, _, _, std = graphgen.make_config("c5", device=torch.device("cuda", 0))
+    torch.cuda.empty_cache()
+    g = G.Graph(n, src, dst)
+    sums = []
+    for mode in (0, 1):
+        ctx = G.Context(g, dim, 1, neg_mode=G.NEG_PER_VERTEX_K, negatives=k, deterministic=True, bucket_mode=mode)
+        ctx.init_coords(G.INIT_NORMAL, 1, std)
+        if mode == 0:
+            assert ctx.hash_bits == 31
+            partners, draws = ctx.sample(0)
+            anchors = np.repeat(np.arange(n, dtype=np.uint32), k)
+            assert (partners != anchors).all() and (partners < n).all()
+            pick = np.random.default_rng(0).integers(0, partners.size, 4_000_000)
+            assert not ctx.probe(anchors[pick], partners[pick]).any()
+            # i * n wraps for i >= 2^8 at n = 2^24 (32-bit pair_hash, reproduced on purpose), so many edges alias:
+            # ~7 % of the probes are rejected, not the 24 % that 2m distinct cells would give
+            assert 1.03 < draws / partners.size < 1.3
+            del partners, anchors
+        he, hn = ctx.iterate(1.5, 1.0, 0)
+        assert he.sum() == len(src) and hn.sum() == n * k
+        x = torch.as_tensor(_DeviceArray(ctx.device_coords(0), (ctx.padded_rows, ctx.row_stride)), device="cuda:0")
+        assert bool(torch.isfinite(x).all())
+        bits = x.view(torch.int32).to(torch.int64)
+        sums.append((int(bits.sum()), int((bits[::7] * 3).sum()), he.tolist(), hn.tolist()))
+        del x, bits
+        ctx.close()
+        torch.cuda.empty_cache()
+    assert sums[0] == sums[1]
+
+
 def test_device_sigma_search_matches_host_search(G):
     """sigma_update_kernel (device) against hostmath.cpp (pinned to the reference by tests/test_host_numerics.py)
     on the tallies of real rounds, including the growth cap and the PE estimate."""
