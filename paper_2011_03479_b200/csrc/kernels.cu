@@ -2455,7 +2455,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 4>(a, lo, hi, precise, stream);
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
-  else if (ld <= 64) gather_batched_go<16, 1, 4, 16, 1, 128, 4>(a, lo, hi, precise, stream);
+  else if (ld <= 64) gather_batched_go<16, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);
   else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);  // 16 rows/warp, 20 warps/SM (96 regs)
   else if (ld <= 256) gather_batched_go<32, 2, 4, 4, 1>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 2, 1>(a, lo, hi, precise, stream);
