@@ -276,7 +276,11 @@ void build_structures(gempe_ctx* c) {
       share = static_cast<double>(region_rows) / n;
     }
     const std::uint64_t busiest = *std::max_element(own_slots.begin(), own_slots.end());
-    const double expect = 1.25 * static_cast<double>(busiest) * share;  // partners are ~uniform over vertices
+    double slack = 1.25;
+    if (const char* e = std::getenv("GEMPE_REGION_SLACK")) {  // test hook: undersized regions exercise the spill area
+      if (region_mode) slack = std::max(0.05, std::atof(e));
+    }
+    const double expect = slack * static_cast<double>(busiest) * share;  // partners are ~uniform over vertices
     const std::uint64_t cap = std::min<std::uint64_t>(busiest, static_cast<std::uint64_t>(expect + 8.0 * std::sqrt(expect)) + 1024);
     if (cap * regions > 0xffffffffull) throw config_error("exchange regions exceed 2^32 records; use more ranks");
     c->ex_first_slot.upload(first);
@@ -286,7 +290,15 @@ void build_structures(gempe_ctx* c) {
     if (external) c->ex_recv.allocate(static_cast<std::size_t>(cap) * regions); else c->ex_recv.release();
     c->ex_send_count.allocate(regions, true);
     if (external) c->ex_recv_count.allocate(regions, true); else c->ex_recv_count.release();
-    c->ex_rank.allocate(static_cast<std::size_t>(cap) * regions);
+    const std::uint64_t spill_cap = region_mode ? c->slots : 0;
+    c->ex_rank.allocate(static_cast<std::size_t>(cap) * regions + spill_cap);
+    if (region_mode) {
+      c->ex_spill.allocate(spill_cap);
+      c->ex_spill_count.allocate(1, true);
+    } else {
+      c->ex_spill.release();
+      c->ex_spill_count.release();
+    }
     if (c->in_cnt.size() == 0) c->in_cnt.allocate(n);
     c->in_rank.release();  // arrival ranks live beside the records here
     c->exchange.own_slots = prefix.back();
@@ -296,6 +308,9 @@ void build_structures(gempe_ctx* c) {
     c->exchange.regions = regions;
     c->exchange.region_rows = region_rows;
     c->exchange.capacity = static_cast<std::uint32_t>(cap);
+    c->exchange.spill = region_mode ? c->ex_spill.get() : nullptr;
+    c->exchange.spill_count = region_mode ? c->ex_spill_count.get() : nullptr;
+    c->exchange.spill_capacity = static_cast<std::uint32_t>(spill_cap);
     c->exchange.send = c->ex_send.get();
     c->exchange.send_count = c->ex_send_count.get();
     // a single rank is its own peer: what it packed is what it receives

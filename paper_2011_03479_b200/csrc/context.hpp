@@ -89,8 +89,8 @@ struct gempe_ctx {
   // sharded sampling with an exchange step (opt.exchange): records packed by destination rank, see kernels.hpp
   gempe::ExchangeArgs exchange{};
   gempe::DeviceBuffer<std::uint64_t> ex_first_slot, ex_prefix;
-  gempe::DeviceBuffer<uint2> ex_send, ex_recv;
-  gempe::DeviceBuffer<std::uint32_t> ex_send_count, ex_recv_count, ex_rank;
+  gempe::DeviceBuffer<uint2> ex_send, ex_recv, ex_spill;
+  gempe::DeviceBuffer<std::uint32_t> ex_send_count, ex_recv_count, ex_rank, ex_spill_count;
   bool pack_path = false;       // sampling goes through sample_pack + bucket_records (opt.exchange, or bucket_mode 3)
   bool bucket_pending = false;  // records packed, gempe_bucket_received not yet called
   // fused update + broadcast: X buffers (both parities, indexed like x[]) of the other ranks, in this rank's address space

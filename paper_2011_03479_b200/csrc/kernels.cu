@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
     if (pos < x.capacity) {
       x.send[static_cast<std::size_t>(dest) * x.capacity + pos] = make_uint2(partner, anchor);
     } else {
-      atomicOr(a.status + kStatExchangeOverflow, 1u);
+      const std::uint32_t at = x.spill ? atomicAdd(x.spill_count, 1u) : 0xffffffffu;
+      if (at < x.spill_capacity) x.spill[at] = make_uint2(partner, anchor);
+      else atomicOr(a.status + kStatExchangeOverflow, 1u);
     }
   }
 }
@@ -269,6 +271,25 @@ __global__ void __launch_bounds__(kThreads) scatter_records_kernel(const Exchang
   const std::size_t idx = static_cast<std::size_t>(from) * x.capacity + j;
   const uint2 rec = x.recv[idx];
   in_anchor[in_off[rec.x] + rec_rank[idx]] = rec.y;
+}
+
+// the spill area (see ExchangeArgs): same two steps, grid-stride, normally zero records
+__global__ void __launch_bounds__(kThreads) count_spill_kernel(const ExchangeArgs x, std::uint32_t* __restrict__ in_cnt,
+                                                               std::uint32_t* __restrict__ spill_rank) {
+  const std::uint32_t count = min(*x.spill_count, x.spill_capacity);
+  for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+    spill_rank[j] = atomicAdd(in_cnt + x.spill[j].x, 1u);
+  }
+}
+__global__ void __launch_bounds__(kThreads) scatter_spill_kernel(const ExchangeArgs x,
+                                                                 const std::uint32_t* __restrict__ spill_rank,
+                                                                 const std::uint32_t* __restrict__ in_off,
+                                                                 std::uint32_t* __restrict__ in_anchor) {
+  const std::uint32_t count = min(*x.spill_count, x.spill_capacity);
+  for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+    const uint2 rec = x.spill[j];
+    in_anchor[in_off[rec.x] + spill_rank[j]] = rec.y;
+  }
 }
 
 // ---- bucketing by partner, method B (large n): two-level counting sort with streaming traffic only.
@@ -2252,6 +2273,7 @@ int launch_sample(const SampleArgs& a, cudaStream_t stream) {
 
 int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream) {
   cudaMemsetAsync(x.send_count, 0, x.regions * sizeof(std::uint32_t), stream);
+  if (x.spill) cudaMemsetAsync(x.spill_count, 0, sizeof(std::uint32_t), stream);
   if (x.own_slots == 0) return 0;
   sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 2 * x.regions * sizeof(std::uint32_t), stream>>>(a, x);
   return 1;
@@ -2263,13 +2285,22 @@ int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uin
   cudaMemsetAsync(in_cnt, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
   int launches = 0;
   const dim3 grid(blocks_for(x.capacity, kThreads), sources);
+  std::uint32_t* spill_rank = rec_rank + static_cast<std::size_t>(sources) * x.capacity;
   if (x.capacity) {
     count_records_kernel<<<grid, kThreads, 0, stream>>>(x, in_cnt, rec_rank);
+    ++launches;
+  }
+  if (x.spill) {
+    count_spill_kernel<<<148 * 4, kThreads, 0, stream>>>(x, in_cnt, spill_rank);
     ++launches;
   }
   launches += launch_scan(in_cnt, in_off, n, scratch, stream);
   if (x.capacity) {
     scatter_records_kernel<<<grid, kThreads, 0, stream>>>(x, rec_rank, in_off, in_anchor);
+    ++launches;
+  }
+  if (x.spill) {
+    scatter_spill_kernel<<<148 * 4, kThreads, 0, stream>>>(x, spill_rank, in_off, in_anchor);
     ++launches;
   }
   return launches;

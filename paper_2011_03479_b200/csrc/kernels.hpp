@@ -83,6 +83,12 @@ struct ExchangeArgs {
   std::uint32_t* send_count;         // [world]
   const uint2* recv;                 // [world][capacity]
   const std::uint32_t* recv_count;   // [world]
+  // one rank, vertex ranges as destinations: records that do not fit their range's region (partners far from uniform
+  // over the ranges, e.g. structured ids without the random relabelling) go to a common spill area, bucketed after
+  // the regions -- correct for any input, only slower.  Null across ranks (a record must reach its owner).
+  uint2* spill;
+  std::uint32_t* spill_count;
+  std::uint32_t spill_capacity;
 };
 
 // Two-level counting sort of the accepted samples by partner (large n).

@@ -198,20 +198,24 @@ def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k, buck
 
 
 def test_range_bucketing_with_several_ranges(G, monkeypatch):
-    """bucket_mode 3 with more than one vertex range (1 MB of counters per range here): same buckets as the atomics."""
+    """bucket_mode 3 with more than one vertex range (1 MB of counters per range here): same buckets as the atomics,
+    also when the ranges' regions are too small and records spill to the common area."""
     monkeypatch.setenv("GEMPE_REGION_MB", "1")
     n = 700_001  # 2.8 MB of counters -> 3 ranges, the last one short
     _, src, dst = er_graph(n, 2 * n, 13)
     outs = []
-    for mode in (1, 3):
+    for mode, slack in ((1, None), (3, None), (3, "0.5")):  # slack 0.5: half of every range spills to the common area
+        if slack:
+            monkeypatch.setenv("GEMPE_REGION_SLACK", slack)
         ctx = G.Context(G.Graph(n, src, dst), 4, 3, neg_mode=1, negatives=3, deterministic=True, bucket_mode=mode)
         partners, draws = ctx.sample(1)
         he, hn = ctx.iterate(1.5, 1.0, 1)
         outs.append((ctx.get_coords(), he, hn, partners, draws))
         ctx.close()
-    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
-    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
-    assert np.array_equal(outs[0][3], outs[1][3]) and outs[0][4] == outs[1][4]
+    for other in outs[1:]:
+        assert np.array_equal(outs[0][0].view(np.uint32), other[0].view(np.uint32))
+        assert np.array_equal(outs[0][1], other[1]) and np.array_equal(outs[0][2], other[2])
+        assert np.array_equal(outs[0][3], other[3]) and outs[0][4] == other[4]
 
 
 @pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5)])
