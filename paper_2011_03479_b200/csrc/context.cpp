@@ -50,6 +50,9 @@ namespace {
 template <typename Fn>
 int guarded(gempe_ctx* ctx, Fn&& fn) {
   try {
+    // every entry point works on the context's own device, whatever the caller's current device is (several
+    // contexts on different GPUs may be driven from one thread)
+    if (ctx && cudaSetDevice(ctx->opt.device) != cudaSuccess) throw cuda_error("cudaSetDevice failed");
     fn();
     return GEMPE_OK;
   } catch (const std::exception& e) {
