@@ -98,21 +98,24 @@ void set_round_math(gempe_ctx* c, double mu, double sigma) {
   m.exact = c->opt.math == GEMPE_MATH_EXACT;
 }
 
-// Builds every graph-derived device structure from the current host work graph.
+// Host copies of the work edge arrays, downloaded on first use.
+void host_work_graph(gempe_ctx* c) {
+  if (c->work_src.size() == c->m && c->work_dst.size() == c->m) return;
+  c->work_src.resize(c->m);
+  c->work_dst.resize(c->m);
+  if (c->m == 0) return;
+  cuda_check(cudaMemcpy(c->work_src.data(), c->tmp_src.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "work graph D2H");
+  cuda_check(cudaMemcpy(c->work_dst.data(), c->tmp_dst.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "work graph D2H");
+}
+
+// Builds every graph-derived device structure from the work graph on the device.
 void build_structures(gempe_ctx* c) {
   const std::uint32_t n = c->n;
   const std::uint64_t m = c->m;
-  const auto& src = c->work_src;
-  const auto& dst = c->work_dst;
 
   PhaseTimer timer;
   const bool per_edge = c->opt.neg_mode == GEMPE_NEG_PER_EDGE_2;
-  // the work edge arrays on the device: they feed the CSR build and the hash-set build
-  if (c->tmp_src.size() != m || m == 0) {
-    c->tmp_src.upload(src);
-    c->tmp_dst.upload(dst);
-  }
-  timer.lap("edge arrays -> device");
+  // the work edge arrays are resident on the device (tmp_src / tmp_dst): they feed the CSR build and the hash-set build
   // both-direction CSR; eid_role = 2*e + role keys the PER_EDGE_2 sample streams.  Default: built on the device
   // (degree count, scan, atomic fill; the order inside a row is the arrival order).  When a reproducible order is
   // asked for (opt.deterministic) the rows are filled on the host in edge order instead.
@@ -131,6 +134,9 @@ void build_structures(gempe_ctx* c) {
     cuda_check(cudaMemcpy(rowptr.data(), c->rowptr.get(), rowptr.size() * sizeof(std::uint32_t), cudaMemcpyDeviceToHost),
                "rowptr D2H");
   } else {
+    host_work_graph(c);
+    const auto& src = c->work_src;
+    const auto& dst = c->work_dst;
     for (std::uint64_t e = 0; e < m; ++e) {
       ++rowptr[src[e] + 1];
       ++rowptr[dst[e] + 1];
@@ -164,6 +170,8 @@ void build_structures(gempe_ctx* c) {
   std::vector<uint4> items;
   std::vector<std::uint32_t> hub_first, hub_items;
   std::uint32_t parts = 0;
+  items.reserve(static_cast<std::size_t>(n) / static_cast<std::size_t>(c->opt.world) +
+                static_cast<std::size_t>(2 * m / std::max(1u, c->chunk_entries)) + 1024);
   c->chunk_item_off.assign(c->comm_chunks + 1, 0);
   const std::uint32_t world = static_cast<std::uint32_t>(c->opt.world), rank = static_cast<std::uint32_t>(c->opt.rank);
   for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
@@ -333,8 +341,6 @@ void build_structures(gempe_ctx* c) {
   c->launches += launch_hash_build(c->tmp_src.get(), c->tmp_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
                                    c->hash_words.get(), summarise ? c->hash_summary.get() : nullptr, c->stream);
   cuda_check(cudaStreamSynchronize(c->stream), "hash build");
-  c->tmp_src.release();
-  c->tmp_dst.release();
   timer.lap("hash set (device)");
   if (c->capture) {
     c->cap_y.allocate(static_cast<std::size_t>(n) * c->dim, true);
@@ -342,19 +348,16 @@ void build_structures(gempe_ctx* c) {
   }
 }
 
-// random_relabel applied to the work graph (graph.cpp:199-204) on the device; the relabelled arrays come back to the
-// host copies and stay on the device for build_structures.
+// random_relabel applied to the work graph (graph.cpp:199-204), in place on the device
 void apply_relabel(gempe_ctx* c, const std::vector<std::uint32_t>& fwd) {
   if (c->m) {
-    c->tmp_src.upload(c->work_src);
-    c->tmp_dst.upload(c->work_dst);
     DeviceBuffer<std::uint32_t> d_fwd;
     d_fwd.upload(fwd);
     c->launches += launch_relabel_apply(c->tmp_src.get(), c->tmp_dst.get(), c->m, d_fwd.get(), c->stream);
     cuda_check(cudaStreamSynchronize(c->stream), "relabel");
-    cuda_check(cudaMemcpy(c->work_src.data(), c->tmp_src.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "relabel D2H");
-    cuda_check(cudaMemcpy(c->work_dst.data(), c->tmp_dst.get(), c->m * sizeof(std::uint32_t), cudaMemcpyDeviceToHost), "relabel D2H");
   }
+  c->work_src.clear();  // stale host copies
+  c->work_dst.clear();
   for (auto& v : c->to_work) v = fwd[v];
 }
 
@@ -500,10 +503,7 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
   if (2 * m >= 0xffffffffull) throw config_error("edge count exceeds the 32-bit adjacency index");
   const std::uint64_t slots = o.neg_mode == GEMPE_NEG_PER_EDGE_2 ? 2 * m : static_cast<std::uint64_t>(n) * o.negatives;
   if (slots >= 0xffffffffull) throw config_error("sample count exceeds the 32-bit bucket index");
-  for (std::uint64_t e = 0; e < m; ++e) {
-    if (src[e] >= n || dst[e] >= n) throw data_error("edge endpoint out of range");
-    if (src[e] == dst[e]) throw data_error("self-loop in edge list (graphs must be canonical)");
-  }
+  (void)n;  // the edge arrays themselves are checked on the device once they are there (gempe_create)
 }
 
 }  // namespace
@@ -582,11 +582,22 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->hist.allocate(2 * kBins, true);
     for (auto& buf : c->x) buf.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
 
-    c->work_src.assign(src, src + m);
-    c->work_dst.assign(dst, dst + m);
+    timer.lap("device buffers");
+    // the edge list goes straight to the device; endpoints and self-loops are checked there
+    c->tmp_src.upload(src, m);
+    c->tmp_dst.upload(dst, m);
+    if (m) {
+      launch_validate_edges(c->tmp_src.get(), c->tmp_dst.get(), m, n, c->status.get(), c->stream);
+      std::uint32_t flags = 0;
+      cuda_check(cudaMemcpyAsync(&flags, c->status.get(), sizeof flags, cudaMemcpyDeviceToHost, c->stream), "validate D2H");
+      cuda_check(cudaStreamSynchronize(c->stream), "validate edges");
+      cuda_check(cudaMemsetAsync(c->status.get(), 0, sizeof flags, c->stream), "status reset");
+      if (flags & 1u) throw data_error("edge endpoint out of range");
+      if (flags & 2u) throw data_error("self-loop in edge list (graphs must be canonical)");
+    }
     c->to_work.resize(n);
     for (std::uint32_t v = 0; v < n; ++v) c->to_work[v] = v;
-    timer.lap("device buffers + graph copy");
+    timer.lap("edge list -> device, validation");
     if (!c->degenerate) {
       if (opt->relabel) {  // engine.cpp:161-163 -> graph.cpp:182-206
         apply_relabel(c, random_relabel_forward(n, mix_seed(opt->seed, 0xA11BE11)));
@@ -623,11 +634,14 @@ std::uint64_t gempe_algorithmic_bytes(const gempe_ctx* c) {
   return (2 * c->m + 2 * S) * R + 2ull * c->n * R + 8 * c->m + 8ull * c->n + 4 * S + S;
 }
 
-int gempe_get_work_graph(const gempe_ctx* c, std::uint32_t* src, std::uint32_t* dst, std::uint32_t* to_work) {
-  if (src) std::copy(c->work_src.begin(), c->work_src.end(), src);
-  if (dst) std::copy(c->work_dst.begin(), c->work_dst.end(), dst);
-  if (to_work) std::copy(c->to_work.begin(), c->to_work.end(), to_work);
-  return GEMPE_OK;
+int gempe_get_work_graph(const gempe_ctx* cc, std::uint32_t* src, std::uint32_t* dst, std::uint32_t* to_work) {
+  gempe_ctx* c = const_cast<gempe_ctx*>(cc);  // fills the host cache
+  return guarded(c, [&] {
+    if (src || dst) host_work_graph(c);
+    if (src) std::copy(c->work_src.begin(), c->work_src.end(), src);
+    if (dst) std::copy(c->work_dst.begin(), c->work_dst.end(), dst);
+    if (to_work) std::copy(c->to_work.begin(), c->to_work.end(), to_work);
+  });
 }
 
 int gempe_set_coords(gempe_ctx* c, const float* x_work) {

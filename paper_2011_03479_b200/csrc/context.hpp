@@ -35,10 +35,11 @@ class DeviceBuffer {
       cuda_check(cudaDeviceSynchronize(), "cudaMemset");
     }
   }
-  void upload(const std::vector<T>& host) {
-    allocate(host.size());
-    if (!host.empty()) {
-      cuda_check(cudaMemcpy(ptr_, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  void upload(const std::vector<T>& host) { upload(host.data(), host.size()); }
+  void upload(const T* host, std::size_t count) {
+    allocate(count);
+    if (count) {
+      cuda_check(cudaMemcpy(ptr_, host, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
       cuda_check(cudaDeviceSynchronize(), "upload");  // pageable H2D may still be in flight on return
     }
   }
@@ -72,14 +73,15 @@ struct gempe_ctx {
   std::uint32_t chunk_entries = 0;
   std::string error;
 
-  // host copies kept for the work-graph accessors and re-relabelling
+  // the work graph (edge list in work ids) lives on the device (tmp_src / tmp_dst); the host copies are filled on
+  // demand (work-graph accessor, deterministic CSR) and dropped when the graph is relabelled
   std::vector<std::uint32_t> work_src, work_dst, to_work;
 
   // device state
   gempe::DeviceBuffer<float> x[2];
   int cur = 0;
   gempe::DeviceBuffer<std::uint32_t> rowptr, nbr, eid_role, csr_src;
-  gempe::DeviceBuffer<std::uint32_t> tmp_src, tmp_dst;  // work edge arrays on the device during construction only
+  gempe::DeviceBuffer<std::uint32_t> tmp_src, tmp_dst;  // the work edge arrays (work ids, input edge order)
   gempe::DeviceBuffer<std::uint32_t> hash_words, hash_summary;
   gempe::DeviceBuffer<std::uint32_t> neg_own, in_cnt, in_off, in_rank, in_anchor, scan_scratch;
   // large-n bucketing (two-level counting sort); partition.buckets == 0 selects the atomic method

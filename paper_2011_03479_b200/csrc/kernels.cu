@@ -70,6 +70,18 @@ __global__ void hash_build_kernel(const std::uint32_t* __restrict__ src, const s
   }
 }
 
+__global__ void validate_edges_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst,
+                                      std::uint64_t m, std::uint32_t n, std::uint32_t* __restrict__ flags) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  std::uint32_t bad = 0;
+  for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+    const std::uint32_t i = src[e], j = dst[e];
+    if (i >= n || j >= n) bad |= 1u;
+    else if (i == j) bad |= 2u;
+  }
+  if (bad) atomicOr(flags, bad);
+}
+
 __global__ void probe_kernel(const std::uint32_t* __restrict__ words, std::uint32_t mask, std::uint32_t n,
                              const std::uint32_t* __restrict__ i, const std::uint32_t* __restrict__ j,
                              std::uint64_t count, std::uint8_t* __restrict__ out) {
@@ -2229,6 +2241,14 @@ inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
 }  // namespace
 
 // ---------------------------------------------------------------------------------- launchers
+
+int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                          std::uint32_t* flags, cudaStream_t stream) {
+  if (m == 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  validate_edges_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, flags);
+  return 1;
+}
 
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                       std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream) {

@@ -136,6 +136,9 @@ struct GatherArgs {
 };
 
 // ---- launchers (all asynchronous on `stream`; return the number of kernels launched) ---------------
+// flags |= 1 when an endpoint is >= n, |= 2 on a self-loop
+int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
+                          std::uint32_t* flags, cudaStream_t stream);
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                       std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream);
 constexpr int kHashSummaryShift = 2;  // cells per summary bit = 4 (kernels.cu: kSummaryShift)
