@@ -676,15 +676,16 @@ int gempe_relabel(gempe_ctx* c, std::uint64_t relabel_seed) {
   return guarded(c, [&] {
     require_live(c);
     const auto fwd = random_relabel_forward(c->n, relabel_seed);
-    std::vector<float> before(static_cast<std::size_t>(c->n) * c->dim), after(before.size());
-    if (gempe_get_coords(c, before.data()) != GEMPE_OK) throw cuda_error(c->error);
-    for (std::uint32_t v = 0; v < c->n; ++v) {  // engine.cpp:186-190
-      std::memcpy(after.data() + static_cast<std::size_t>(fwd[v]) * c->dim,
-                  before.data() + static_cast<std::size_t>(v) * c->dim, sizeof(float) * c->dim);
+    {  // coordinates follow their vertices (engine.cpp:186-190): row v moves to row fwd[v], into the other buffer
+      DeviceBuffer<std::uint32_t> d_fwd;
+      d_fwd.upload(fwd);
+      c->launches += launch_permute_rows(c->x[c->cur].get(), c->ld, c->x[c->cur ^ 1].get(), c->ld, c->ld, c->n,
+                                         d_fwd.get(), true, c->stream);
+      cuda_check(cudaStreamSynchronize(c->stream), "relabel coordinates");
+      c->cur ^= 1;
     }
     apply_relabel(c, fwd);
     build_structures(c);
-    if (gempe_set_coords(c, after.data()) != GEMPE_OK) throw cuda_error(c->error);
   });
 }
 

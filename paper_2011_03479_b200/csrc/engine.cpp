@@ -65,19 +65,18 @@ void rethrow(gempe_ctx* c, int rc) {
   }
 }
 
-// original-indexed export of a work-indexed device layout (engine.cpp:327-337)
+// original-indexed export of a work-indexed device layout (engine.cpp:327-337, 376-381): rows gathered on the
+// device, one transfer into the caller's buffer
 void map_back(gempe_engine* e, const float* x_dev, const std::vector<std::uint32_t>& to_work, float* out) {
   gempe_ctx* c = e->ctx;
-  std::vector<float> work(static_cast<std::size_t>(e->n) * e->dim);
-  if (e->n) {
-    cuda_check(cudaStreamSynchronize(c->stream), "map_back");
-    cuda_check(cudaMemcpy2D(work.data(), e->dim * sizeof(float), x_dev, c->ld * sizeof(float), e->dim * sizeof(float),
-                            e->n, cudaMemcpyDeviceToHost), "map_back D2H");
-  }
-  for (std::uint32_t v = 0; v < e->n; ++v) {
-    std::memcpy(out + static_cast<std::size_t>(v) * e->dim, work.data() + static_cast<std::size_t>(to_work[v]) * e->dim,
-                sizeof(float) * e->dim);
-  }
+  if (e->n == 0) return;
+  DeviceBuffer<std::uint32_t> d_map;
+  DeviceBuffer<float> packed;
+  d_map.upload(to_work);
+  packed.allocate(static_cast<std::size_t>(e->n) * e->dim);
+  c->launches += launch_permute_rows(x_dev, c->ld, packed.get(), e->dim, e->dim, e->n, d_map.get(), false, c->stream);
+  cuda_check(cudaStreamSynchronize(c->stream), "map_back");
+  cuda_check(cudaMemcpy(out, packed.get(), packed.size() * sizeof(float), cudaMemcpyDeviceToHost), "map_back D2H");
 }
 
 void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {

@@ -2234,6 +2234,21 @@ __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
   }
 }
 
+__global__ void __launch_bounds__(kThreads) permute_rows_kernel(const float* __restrict__ in, std::uint32_t in_ld,
+                                                                float* __restrict__ out, std::uint32_t out_ld,
+                                                                std::uint32_t dim, std::uint32_t n,
+                                                                const std::uint32_t* __restrict__ map, bool scatter) {
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * dim;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const std::uint32_t v = static_cast<std::uint32_t>(i / dim), col = static_cast<std::uint32_t>(i % dim);
+    const std::uint32_t w = __ldg(map + v);
+    const std::size_t from = static_cast<std::size_t>(scatter ? v : w) * in_ld + col;
+    const std::size_t to = static_cast<std::size_t>(scatter ? w : v) * out_ld + col;
+    out[to] = in[from];
+  }
+}
+
 inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
   return static_cast<unsigned>((work + per_block - 1) / per_block);
 }
@@ -2375,6 +2390,15 @@ int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32
 
 int launch_sort_buckets(const std::uint32_t* in_off, std::uint32_t* in_anchor, std::uint32_t n, cudaStream_t stream) {
   sort_buckets_kernel<<<blocks_for(static_cast<std::uint64_t>(n) * 32, kThreads), kThreads, 0, stream>>>(in_off, in_anchor, n);
+  return 1;
+}
+
+int launch_permute_rows(const float* in, std::uint32_t in_ld, float* out, std::uint32_t out_ld, std::uint32_t dim,
+                        std::uint32_t n, const std::uint32_t* map, bool scatter, cudaStream_t stream) {
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * dim;
+  if (total == 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(total, kThreads), 148u * 64u));
+  permute_rows_kernel<<<blocks, kThreads, 0, stream>>>(in, in_ld, out, out_ld, dim, n, map, scatter);
   return 1;
 }
 

@@ -169,6 +169,10 @@ int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32
 int launch_sort_buckets(const std::uint32_t* in_off, std::uint32_t* in_anchor, std::uint32_t n,
                         cudaStream_t stream);
 // reorders neg_own (CSR order) into reference slot order 2e+draw (test hook)
+// Row permutation of a coordinate matrix: gather (out[v] = in[map[v]]) or scatter (out[map[v]] = in[v]); dim floats
+// per row, row pitches in floats.
+int launch_permute_rows(const float* in, std::uint32_t in_ld, float* out, std::uint32_t out_ld, std::uint32_t dim,
+                        std::uint32_t n, const std::uint32_t* map, bool scatter, cudaStream_t stream);
 int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t* eid_role, std::uint64_t slots,
                               std::uint32_t* out, cudaStream_t stream);
 // variant 0: batched kernel (default), 1: v0 row-at-a-time kernel.  precise: reference-exact double pair_distance.
