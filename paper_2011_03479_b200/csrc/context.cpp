@@ -569,7 +569,7 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);
     c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
     // hub split: d <= 4 runs one thread per item (64 list positions bound the divergence), wider rows one warp per item
-    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 64u : std::max(128u, 4096u / lanes_per_row(c->ld));
+    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 64u : std::max(256u, 4096u / lanes_per_row(c->ld));  // c4 sweep: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41
     c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : default_chunk;
     cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
