@@ -472,7 +472,10 @@ __global__ void unpermute_kernel(const std::uint32_t* __restrict__ neg_own, cons
 
 // One warp per vertex: rank-sort of the (small, Poisson-sized) incoming bucket, in place via registers for
 // buckets up to 32*kSortRegs entries; larger buckets fall back to an O(len^2) global pass.
-constexpr int kGrab = 4;  // work items claimed per atomic by a persistent warp
+#ifndef GEMPE_GRAB
+#define GEMPE_GRAB 4
+#endif
+constexpr int kGrab = GEMPE_GRAB;  // work items claimed per atomic by a persistent warp
 constexpr int kSortRegs = 8;
 __global__ void __launch_bounds__(kThreads) sort_buckets_kernel(const std::uint32_t* __restrict__ in_off,
                                                                 std::uint32_t* __restrict__ in_anchor, std::uint32_t n) {
