@@ -196,10 +196,25 @@ void build_structures(gempe_ctx* c) {
     }
   }
   c->chunk_item_off[c->comm_chunks] = static_cast<std::uint32_t>(items.size());
+  // d <= 4 runs one THREAD per item: items of similar length are put next to each other (longest first) inside every
+  // chunk, so the 32 items of a warp finish together instead of waiting for the longest one
+  const bool sorted_items = c->ld <= 4 && c->opt.kernel_variant == 0 && std::getenv("GEMPE_NO_ITEM_SORT") == nullptr;
+  if (sorted_items) {
+    auto adjacency_len = [&](const uint4& it) {
+      return std::min(it.y + c->chunk_entries, rowptr[it.x + 1]) - it.y;
+    };
+    for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
+      std::stable_sort(items.begin() + c->chunk_item_off[chunk], items.begin() + c->chunk_item_off[chunk + 1],
+                       [&](const uint4& a, const uint4& b) { return adjacency_len(a) > adjacency_len(b); });
+    }
+  }
   // slices for the host-buffer pipeline: ~equal item counts, cut at vertex boundaries (a hub's slices stay together)
   c->step_item_off.assign(1, 0);
   c->step_vertex_off.assign(1, 0);
-  if (world == 1 && !items.empty()) {
+  if (world == 1 && !items.empty() && sorted_items) {  // vertex order is gone: one slice
+    c->step_item_off.push_back(static_cast<std::uint32_t>(items.size()));
+    c->step_vertex_off.push_back(n);
+  } else if (world == 1 && !items.empty()) {
     constexpr std::uint32_t kSlices = 8;
     for (std::uint32_t k = 1; k < kSlices; ++k) {
       std::uint64_t at = static_cast<std::uint64_t>(items.size()) * k / kSlices;
@@ -568,8 +583,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     const std::uint64_t blocks = static_cast<std::uint64_t>(c->opt.world) * c->comm_chunks;
     c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);
     c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
-    // hub split: d <= 4 runs one thread per item (64 list positions bound the divergence), wider rows one warp per item
-    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 64u : std::max(256u, 4096u / lanes_per_row(c->ld));  // c4 sweep: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41
+    // hub split: d <= 4 runs one thread per item (32 adjacency positions bound its serial latency chain), wider rows one warp per item
+    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 32u :  // c2 sweep: 16 -> 76 us, 32 -> 60, 64 -> 80, 128 -> 117
+                                                                                      std::max(256u, 4096u / lanes_per_row(c->ld));  // c4 sweep: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41
     c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : default_chunk;
     cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;

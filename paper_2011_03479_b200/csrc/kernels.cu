@@ -1392,7 +1392,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
 //
 // d <= 4 (graph drawing): a row is one 4..16-byte vector, so a whole work item fits one thread -- 32 different
 // vertices per warp keep 4 x 32 independent row gathers in flight, and there is no warp-serial latency chain per
-// item.  Same arithmetic and the same hub protocol as gather_batched_kernel; items are capped at 64 list
+// item.  Same arithmetic and the same hub protocol as gather_batched_kernel; items are capped at 32 adjacency
 // positions (context.cpp) to bound divergence on hubs.
 template <int VEC, bool PRECISE>
 __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArgs a, std::uint32_t item_lo,
