@@ -2252,6 +2252,51 @@ __global__ void __launch_bounds__(kThreads) permute_rows_kernel(const float* __r
   }
 }
 
+// exclusive scan of in[0..n) into out[0..n], out[n] = total: one 1024-thread block, 4 elements per thread and pass
+constexpr std::uint32_t kScanSingleBlockMax = 1u << 14;  // beyond that the three-kernel scan wins (c2, n = 1e5: 50 vs 82 us)
+__global__ void __launch_bounds__(1024) scan_single_block_kernel(const std::uint32_t* __restrict__ in,
+                                                                 std::uint32_t* __restrict__ out, std::uint32_t n) {
+  __shared__ std::uint32_t warp_tot[32];
+  __shared__ std::uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (std::uint32_t base = 0; base < n; base += 4096) {
+    const std::uint32_t i0 = base + threadIdx.x * 4;
+    std::uint32_t v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = i0 + q < n ? in[i0 + q] : 0u;
+    const std::uint32_t mine = v[0] + v[1] + v[2] + v[3];
+    std::uint32_t inc = mine;
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+      if (lane >= off) inc += o;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const std::uint32_t w = warp_tot[lane];
+      std::uint32_t winc = w;
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, winc, off);
+        if (lane >= off) winc += o;
+      }
+      warp_tot[lane] = winc - w;
+    }
+    __syncthreads();
+    std::uint32_t run = carry + warp_tot[warp] + inc - mine;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i0 + q < n) out[i0 + q] = run;
+      run += v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = run;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
 inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
   return static_cast<unsigned>((work + per_block - 1) / per_block);
 }
@@ -2378,6 +2423,10 @@ int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::ui
 
 int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
                 cudaStream_t stream) {
+  if (n <= kScanSingleBlockMax) {  // small graphs are launch-bound: one block walks the array with a running carry
+    scan_single_block_kernel<<<1, 1024, 0, stream>>>(in_cnt, in_off, n);
+    return 1;
+  }
   const unsigned tiles = blocks_for(n, kScanTile);
   scan_tile_sums_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch);
   scan_tile_offsets_kernel<<<1, 1024, 0, stream>>>(scratch, tiles);
