@@ -263,7 +263,7 @@ void build_structures(gempe_ctx* c) {
     c->bucket_off.release();
     c->records.release();
     c->in_rank.allocate(c->slots);
-    c->in_cnt.allocate(n);
+    c->in_cnt.allocate(n, true);
   }
   c->in_off.allocate(static_cast<std::size_t>(n) + 1, true);
   c->scan_scratch.allocate((n + 4095) / 4096 + 2);
@@ -325,7 +325,7 @@ void build_structures(gempe_ctx* c) {
       c->ex_spill.release();
       c->ex_spill_count.release();
     }
-    if (c->in_cnt.size() == 0) c->in_cnt.allocate(n);
+    if (c->in_cnt.size() == 0) c->in_cnt.allocate(n, true);
     c->in_rank.release();  // arrival ranks live beside the records here
     c->exchange.own_slots = prefix.back();
     c->exchange.ranges = c->comm_chunks;
@@ -414,8 +414,8 @@ void bucket_received(gempe_ctx* c) {
 }
 
 void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
-  cuda_check(cudaMemsetAsync(c->status.get(), 0, 8 * sizeof(std::uint32_t), c->stream), "memset status");
-  cuda_check(cudaMemsetAsync(c->hist.get(), 0, 2 * kBins * sizeof(unsigned long long), c->stream), "memset hist");
+  cuda_check(cudaMemsetAsync(c->round_state.get(), 0, (4 + 2 * kBins) * sizeof(unsigned long long), c->stream),
+             "memset status + tallies");
   const SampleArgs a = sample_args(c, iter);
   if (c->pack_path) {
     c->launches += launch_sample_pack(a, c->exchange, c->stream);
@@ -427,9 +427,9 @@ void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
   if (c->partition.buckets) {
     c->launches += launch_sample_partition(a, c->partition, c->in_off.get(), c->in_anchor.get(), c->stream);
   } else {
-    cuda_check(cudaMemsetAsync(c->in_cnt.get(), 0, c->n * sizeof(std::uint32_t), c->stream), "memset in_cnt");
+    // in_cnt is zero on entry: allocated zeroed, and the scan clears what it has read
     c->launches += launch_sample(a, c->stream);
-    c->launches += launch_scan(c->in_cnt.get(), c->in_off.get(), c->n, c->scan_scratch.get(), c->stream);
+    c->launches += launch_scan(c->in_cnt.get(), c->in_off.get(), c->n, c->scan_scratch.get(), c->stream, true);
     c->launches += launch_scatter(a, c->in_off.get(), c->in_anchor.get(), c->stream);
   }
   if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
@@ -482,10 +482,8 @@ cudaEvent_t next_event(gempe_ctx* c) {
 }
 
 void fetch_status(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
-  cuda_check(cudaMemcpyAsync(c->pinned, c->status.get(), 8 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream),
-             "status D2H");
-  cuda_check(cudaMemcpyAsync(c->pinned + 4, c->hist.get(), 2 * kBins * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, c->stream), "hist D2H");
+  cuda_check(cudaMemcpyAsync(c->pinned, c->round_state.get(), (4 + 2 * kBins) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c->stream), "status + tallies D2H");
   cuda_check(cudaStreamSynchronize(c->stream), "round");
   std::uint32_t st[8];
   std::memcpy(st, c->pinned, sizeof st);
@@ -592,10 +590,11 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned), (4 + 2 * kBins) * sizeof(unsigned long long),
                              cudaHostAllocDefault), "cudaHostAlloc");
     pack_tables(c->tables);
-    c->status.allocate(8, true);
+    c->round_state.allocate(4 + 2 * kBins, true);
+    c->status.p = reinterpret_cast<std::uint32_t*>(c->round_state.get());
+    c->hist.p = c->round_state.get() + 4;
     c->work_cursor.allocate(1, true);
     c->sigma_state.allocate(1, true);
-    c->hist.allocate(2 * kBins, true);
     for (auto& buf : c->x) buf.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
 
     timer.lap("device buffers");

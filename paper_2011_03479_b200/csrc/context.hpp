@@ -110,8 +110,18 @@ struct gempe_ctx {
   std::vector<cudaEvent_t> step_events;
   gempe::DeviceBuffer<std::uint32_t> hub_first, hub_items, hub_arrived;
   gempe::DeviceBuffer<double> part_y, part_z;
-  gempe::DeviceBuffer<unsigned long long> hist;
-  gempe::DeviceBuffer<std::uint32_t> status, work_cursor;
+  // {status[8] as u32, hist[1024] as u64} in ONE allocation with the layout of the pinned mirror below: one memset
+  // at the start of a round, one copy at its end
+  gempe::DeviceBuffer<unsigned long long> round_state;
+  struct StatusView {
+    std::uint32_t* p = nullptr;
+    std::uint32_t* get() const { return p; }
+  } status;
+  struct HistView {
+    unsigned long long* p = nullptr;
+    unsigned long long* get() const { return p; }
+  } hist;
+  gempe::DeviceBuffer<std::uint32_t> work_cursor;
   gempe::DeviceBuffer<gempe::SigmaState> sigma_state;  // device-resident (mu, sigma) feedback
   double mu_dev = gempe::kDefaultMu;
   bool use_dev_math = false;  // gather reads RoundMath from sigma_state instead of kernel parameters

@@ -583,9 +583,9 @@ __global__ void scan_tile_offsets_kernel(std::uint32_t* __restrict__ tile_sum, s
   if (threadIdx.x == 0) tile_sum[tiles] = carry;
 }
 
-__global__ void __launch_bounds__(kThreads) scan_apply_kernel(const std::uint32_t* __restrict__ in, std::uint32_t n,
+__global__ void __launch_bounds__(kThreads) scan_apply_kernel(std::uint32_t* __restrict__ in, std::uint32_t n,
                                                               const std::uint32_t* __restrict__ tile_off,
-                                                              std::uint32_t* __restrict__ out) {
+                                                              std::uint32_t* __restrict__ out, bool clear_input) {
   __shared__ std::uint32_t warp_tot[kThreads / 32];
   const std::uint32_t base = blockIdx.x * kScanTile + threadIdx.x * 16;
   std::uint32_t v[16], s = 0;
@@ -607,7 +607,10 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(const std::uint32_
   std::uint32_t run = tile_off[blockIdx.x] + woff + inc - s;
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
-    if (base + q < n) out[base + q] = run;
+    if (base + q < n) {
+      out[base + q] = run;
+      if (clear_input) in[base + q] = 0;  // the counters are ready for the next round
+    }
     run += v[q];
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_off[gridDim.x];
@@ -2254,8 +2257,9 @@ __global__ void __launch_bounds__(kThreads) permute_rows_kernel(const float* __r
 
 // exclusive scan of in[0..n) into out[0..n], out[n] = total: one 1024-thread block, 4 elements per thread and pass
 constexpr std::uint32_t kScanSingleBlockMax = 1u << 14;  // beyond that the three-kernel scan wins (c2, n = 1e5: 50 vs 82 us)
-__global__ void __launch_bounds__(1024) scan_single_block_kernel(const std::uint32_t* __restrict__ in,
-                                                                 std::uint32_t* __restrict__ out, std::uint32_t n) {
+__global__ void __launch_bounds__(1024) scan_single_block_kernel(std::uint32_t* __restrict__ in,
+                                                                 std::uint32_t* __restrict__ out, std::uint32_t n,
+                                                                 bool clear_input) {
   __shared__ std::uint32_t warp_tot[32];
   __shared__ std::uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -2265,7 +2269,10 @@ __global__ void __launch_bounds__(1024) scan_single_block_kernel(const std::uint
     const std::uint32_t i0 = base + threadIdx.x * 4;
     std::uint32_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = i0 + q < n ? in[i0 + q] : 0u;
+    for (int q = 0; q < 4; ++q) {
+      v[q] = i0 + q < n ? in[i0 + q] : 0u;
+      if (clear_input && i0 + q < n) in[i0 + q] = 0;
+    }
     const std::uint32_t mine = v[0] + v[1] + v[2] + v[3];
     std::uint32_t inc = mine;
     for (int off = 1; off < 32; off <<= 1) {
@@ -2421,16 +2428,16 @@ int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::ui
   return 5;
 }
 
-int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
-                cudaStream_t stream) {
+int launch_scan(std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
+                cudaStream_t stream, bool clear_input) {
   if (n <= kScanSingleBlockMax) {  // small graphs are launch-bound: one block walks the array with a running carry
-    scan_single_block_kernel<<<1, 1024, 0, stream>>>(in_cnt, in_off, n);
+    scan_single_block_kernel<<<1, 1024, 0, stream>>>(in_cnt, in_off, n, clear_input);
     return 1;
   }
   const unsigned tiles = blocks_for(n, kScanTile);
   scan_tile_sums_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch);
   scan_tile_offsets_kernel<<<1, 1024, 0, stream>>>(scratch, tiles);
-  scan_apply_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch, in_off);
+  scan_apply_kernel<<<tiles, kThreads, 0, stream>>>(in_cnt, n, scratch, in_off, clear_input);
   return 3;
 }
 

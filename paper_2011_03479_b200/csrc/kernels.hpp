@@ -161,8 +161,9 @@ std::uint32_t partition_grid(std::uint64_t slots);
 int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::uint32_t* in_off, std::uint32_t* in_anchor,
                             cudaStream_t stream);
 // exclusive scan of in_cnt[n] into in_off[n+1]; scratch must hold ceil(n/4096)+1 words
-int launch_scan(const std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
-                cudaStream_t stream);
+// exclusive scan, in_off[n] = total; clear_input zeroes in_cnt behind the read (per-round counters)
+int launch_scan(std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, std::uint32_t* scratch,
+                cudaStream_t stream, bool clear_input = false);
 int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32_t* in_anchor,
                    cudaStream_t stream);
 // sorts every incoming bucket ascending (deterministic mode)
