@@ -20,12 +20,15 @@ ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--chunk-entries", type=int, default=0)
 ap.add_argument("--sigma", type=float, default=1.0)
 ap.add_argument("--bucket-mode", type=int, default=0)
+ap.add_argument("--dim", type=int, default=0, help="override the configuration's dimension")
 ap.add_argument("--warm-iters", type=int, default=0, help="real iterations (device sigma feedback) before timing")
 a = ap.parse_args()
 
 import torch  # noqa: E402
 n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config, device=torch.device('cuda', 0))
 torch.cuda.empty_cache()
+if a.dim:
+    dim = a.dim
 mode = P.NEG_PER_VERTEX_K if a.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
 import time  # noqa: E402
 _t0 = time.perf_counter()
