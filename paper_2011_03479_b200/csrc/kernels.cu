@@ -2586,10 +2586,12 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   if (ld == 1) gather_batched_go<1, 1, 1, 1, 8>(a, lo, hi, precise, stream);
   else if (ld == 2) gather_batched_go<1, 1, 2, 1, 8>(a, lo, hi, precise, stream);
   else if (ld <= 4) gather_batched_go<1, 1, 4, 1, 8>(a, lo, hi, precise, stream);
-  else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 4>(a, lo, hi, precise, stream);
-  else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2>(a, lo, hi, precise, stream);
-  else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1>(a, lo, hi, precise, stream);
-  else if (ld <= 64) gather_batched_go<16, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);
+  // narrow rows need few registers: 128-thread blocks at 8-12 per SM (c3 graph, dimension overridden: d = 8 -40 %,
+  // d = 16 -24 %, d = 32 -24 %, d = 64 -13 % against 256-thread blocks at 2 per SM / 16 rows at 5 per SM)
+  else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 2, 128, 12>(a, lo, hi, precise, stream);
+  else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2, 128, 8>(a, lo, hi, precise, stream);
+  else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);
+  else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);  // 8 rows per group, 32 warps/SM
   else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);  // 16 rows/warp, 20 warps/SM (96 regs)
   // wider rows: 64 row registers per lane as well (8 / 4 rows per batch), 16 warps/SM (d = 256: -19 %, d = 512: -10 %
   // against 4 / 2 rows in 256-thread blocks)
