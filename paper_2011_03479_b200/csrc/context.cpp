@@ -349,12 +349,24 @@ void build_structures(gempe_ctx* c) {
   c->hash_bits = auto_hash_bits(m, c->opt.hash_bits);
   const std::uint64_t cells = 1ull << c->hash_bits;
   c->hash_words.allocate(std::max<std::uint64_t>(1, cells / 32), true);
-  // a sparse table beyond what L2 keeps (c4: 128 MB, 3 % of the cells set) gets a 4x smaller "any cell of the group
-  // set" summary in front of it; dense or small tables do not
-  const bool summarise = cells / 8 > (64ull << 20) && 2 * m <= cells / 16;
-  if (summarise) c->hash_summary.allocate(cells >> (5 + kHashSummaryShift), true); else c->hash_summary.release();
   c->launches += launch_hash_build(c->tmp_src.get(), c->tmp_dst.get(), m, n, static_cast<std::uint32_t>(cells - 1),
-                                   c->hash_words.get(), summarise ? c->hash_summary.get() : nullptr, c->stream);
+                                   c->hash_words.get(), c->stream);
+  // a sparse table beyond what L2 keeps (c4: 128 MB, 3 % of the cells set) gets a 4x smaller "any cell of the group
+  // set" summary in front of it; dense or small tables do not, and neither does the 2^31-cell table (c5: 7 % set --
+  // the wrapping pair_hash aliases heavily at n = 2^24 -- but its 64 MB summary does not stay in L2 next to the
+  // record stream: 18.1 ms of sampling passes with it, 16.9 without).  The density is counted, not estimated from m.
+  c->hash_summary.release();
+  if (cells / 8 > (64ull << 20) && cells / 32 <= (32ull << 20)) {
+    unsigned long long set_cells = 0;
+    c->launches += launch_hash_popcount(c->hash_words.get(), cells / 32, c->round_state.get(), c->stream);
+    cuda_check(cudaMemcpyAsync(&set_cells, c->round_state.get(), sizeof set_cells, cudaMemcpyDeviceToHost, c->stream), "popcount D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "hash popcount");
+    cuda_check(cudaMemsetAsync(c->round_state.get(), 0, sizeof set_cells, c->stream), "status reset");
+    if (set_cells <= cells / 12) {
+      c->hash_summary.allocate(cells >> (5 + kHashSummaryShift));
+      c->launches += launch_hash_summary(c->hash_words.get(), cells >> (5 + kHashSummaryShift), c->hash_summary.get(), c->stream);
+    }
+  }
   cuda_check(cudaStreamSynchronize(c->stream), "hash build");
   timer.lap("hash set (device)");
   if (c->capture) {

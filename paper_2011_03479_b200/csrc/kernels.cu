@@ -55,18 +55,44 @@ __device__ __forceinline__ bool hash_test(const std::uint32_t* __restrict__ word
 
 __global__ void hash_build_kernel(const std::uint32_t* __restrict__ src, const std::uint32_t* __restrict__ dst,
                                   std::uint64_t m, std::uint32_t n, std::uint32_t mask,
-                                  std::uint32_t* __restrict__ words, std::uint32_t* __restrict__ summary) {
+                                  std::uint32_t* __restrict__ words) {
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
   for (std::uint64_t e = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
     const std::uint32_t i = src[e], j = dst[e];
     const std::uint32_t h0 = pair_hash(i, j, n, mask), h1 = pair_hash(j, i, n, mask);
     atomicOr(words + (h0 >> 5), 1u << (h0 & 31u));
     atomicOr(words + (h1 >> 5), 1u << (h1 & 31u));
-    if (summary) {
-      const std::uint32_t g0 = h0 >> kSummaryShift, g1 = h1 >> kSummaryShift;
-      atomicOr(summary + (g0 >> 5), 1u << (g0 & 31u));
-      atomicOr(summary + (g1 >> 5), 1u << (g1 & 31u));
+  }
+}
+
+// number of set cells (decides whether a summary pays: wrapping pair_hash aliases heavily for large n, so the table
+// can be far emptier than 2m cells)
+__global__ void hash_popcount_kernel(const std::uint32_t* __restrict__ words, std::uint64_t nwords,
+                                     unsigned long long* __restrict__ total) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  unsigned long long mine = 0;
+  for (std::uint64_t w = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    mine += __popc(words[w]);
+  }
+  for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(kFull, mine, off);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, mine);
+}
+
+// summary word s covers table words 4s .. 4s+3: bit 8q + k = any of bits 4k .. 4k+3 of word 4s + q
+__global__ void hash_summary_kernel(const std::uint32_t* __restrict__ words, std::uint64_t nsummary,
+                                    std::uint32_t* __restrict__ summary) {
+  static_assert(kSummaryShift == 2, "layout below assumes 4 cells per summary bit");
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t sidx = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; sidx < nsummary; sidx += stride) {
+    const uint4 w = *reinterpret_cast<const uint4*>(words + 4 * sidx);
+    const std::uint32_t in[4] = {w.x, w.y, w.z, w.w};
+    std::uint32_t out = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) out |= ((in[q] >> (4 * k)) & 0xfu ? 1u : 0u) << (8 * q + k);
     }
+    summary[sidx] = out;
   }
 }
 
@@ -2321,10 +2347,23 @@ int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, st
 }
 
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
-                      std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream) {
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream) {
   if (m == 0) return 0;
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
-  hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words, hash_summary);
+  hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words);
+  return 1;
+}
+
+int launch_hash_popcount(const std::uint32_t* hash_words, std::uint64_t nwords, unsigned long long* total, cudaStream_t stream) {
+  cudaMemsetAsync(total, 0, sizeof(unsigned long long), stream);
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((nwords + kThreads - 1) / kThreads, 148u * 16u));
+  hash_popcount_kernel<<<blocks, kThreads, 0, stream>>>(hash_words, nwords, total);
+  return 1;
+}
+
+int launch_hash_summary(const std::uint32_t* hash_words, std::uint64_t nsummary, std::uint32_t* summary, cudaStream_t stream) {
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((nsummary + kThreads - 1) / kThreads, 148u * 16u));
+  hash_summary_kernel<<<blocks, kThreads, 0, stream>>>(hash_words, nsummary, summary);
   return 1;
 }
 

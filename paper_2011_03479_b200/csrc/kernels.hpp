@@ -140,7 +140,10 @@ struct GatherArgs {
 int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                           std::uint32_t* flags, cudaStream_t stream);
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
-                      std::uint32_t hash_mask, std::uint32_t* hash_words, std::uint32_t* hash_summary, cudaStream_t stream);
+                      std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream);
+int launch_hash_popcount(const std::uint32_t* hash_words, std::uint64_t nwords, unsigned long long* total, cudaStream_t stream);
+// summary bit g = some cell of cells 4g .. 4g+3 is set; nsummary = words / 4
+int launch_hash_summary(const std::uint32_t* hash_words, std::uint64_t nsummary, std::uint32_t* summary, cudaStream_t stream);
 constexpr int kHashSummaryShift = 2;  // cells per summary bit = 4 (kernels.cu: kSummaryShift)
 // construction on the device: relabel application and the both-direction CSR (row order = atomic arrival order)
 int launch_relabel_apply(std::uint32_t* src, std::uint32_t* dst, std::uint64_t m, const std::uint32_t* forward,
