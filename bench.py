@@ -203,7 +203,8 @@ def main():
         e = sharded.make_cuda_engine(g, dim, 1, comm_chunks=args.comm_chunks, device=local_rank, neg_mode=neg_mode,
                                      negatives=k if neg_mode == P.NEG_PER_VERTEX_K else 0,
                                      chunk_entries=args.chunk_entries, bucket_mode=args.bucket_mode,
-                                     peer_broadcast=peer_broadcast, exchange=False if test_backend else None)
+                                     peer_broadcast=peer_broadcast,
+                                     exchange=False if (test_backend and not peer_broadcast) else None)
         e.ops.ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
         return e
 
@@ -285,7 +286,7 @@ def main():
                        "l2": "inputs larger than L2 (X %.0f MB + lists)" % (n * dim * 4 / 1e6) if n * dim * 4 > 126e6
                              else "working set fits L2 (reported as is)",
                        "parallelism": f"vertex-sharded x{world}, samples: "
-                                      f"{'own anchors + all-to-all' if eng.ops.exchange_tensors() is not None else 'replicated enumeration'}"
+                                      f"{'own anchors + peer stores from the pack kernel' if eng.ops.direct_exchange else ('own anchors + all-to-all' if eng.ops.exchange_tensors() is not None else 'replicated enumeration')}"
                                       f", coordinates: {exchange_path}"
                                       if world > 1 else "1 GPU"},
             "clocks": clocks, "gpu_launches": int(launches)}

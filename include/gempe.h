@@ -195,6 +195,20 @@ int gempe_coords_ipc_handles(gempe_ctx* ctx, void* out_2x64_bytes);
 int gempe_open_peer(gempe_ctx* ctx, const void* handles_2x64_bytes);
 int gempe_add_peer_pointers(gempe_ctx* ctx, void* x_parity0, void* x_parity1);
 int gempe_clear_peers(gempe_ctx* ctx);
+/* Direct sample exchange (opt.exchange with world > 1; replaces the all-to-all of gempe_exchange_layout): every rank
+ * publishes its receive area (one allocation: records of both round parities, then the counts) and opens those of all
+ * other ranks; from then on the sampling kernel of gempe_begin_round stores each record straight into the region
+ * reserved for this rank in the destination's receive area, and a one-warp kernel publishes the counts.  The caller
+ * only needs ONE barrier per round, between gempe_begin_round and gempe_bucket_received: it also separates the
+ * previous round's gather (peer stores into X) from this round's.
+ *   gempe_exchange_ipc_handle       : the receive area as a CUDA IPC handle (64 bytes)
+ *   gempe_open_peer_exchange        : registers rank `peer_rank`'s receive area from its handle (another process)
+ *   gempe_add_peer_exchange_pointer : the same for a context living in this process (gempe_exchange_recv_area)
+ * Active as soon as all world - 1 peers are registered; gempe_clear_peers drops them. */
+int gempe_exchange_ipc_handle(gempe_ctx* ctx, void* out_64_bytes);
+int gempe_open_peer_exchange(gempe_ctx* ctx, int peer_rank, const void* handle_64_bytes);
+int gempe_add_peer_exchange_pointer(gempe_ctx* ctx, int peer_rank, void* recv_area);
+void* gempe_exchange_recv_area(gempe_ctx* ctx);
 void* gempe_device_coords_parity(gempe_ctx* ctx, int parity);
 int gempe_coords_parity(const gempe_ctx* ctx);
 int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t / X_{t+1} */

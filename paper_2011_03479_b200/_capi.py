@@ -28,7 +28,8 @@ SYMBOLS = [
     "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_probe",
     "gempe_sample", "gempe_set_stream", "gempe_device_coords", "gempe_row_stride", "gempe_padded_rows",
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_exchange_layout", "gempe_bucket_received", "gempe_gather_chunk", "gempe_coords_ipc_handles", "gempe_open_peer",
-    "gempe_add_peer_pointers", "gempe_clear_peers", "gempe_device_coords_parity", "gempe_coords_parity", "gempe_end_round", "gempe_elapsed_ms",
+    "gempe_add_peer_pointers", "gempe_clear_peers", "gempe_exchange_ipc_handle", "gempe_open_peer_exchange",
+    "gempe_add_peer_exchange_pointer", "gempe_exchange_recv_area", "gempe_device_coords_parity", "gempe_coords_parity", "gempe_end_round", "gempe_elapsed_ms",
     "gempe_kernel_launches", "gempe_host_fastmath_table", "gempe_host_optimize_sigma",
     "gempe_host_histogram_objective", "gempe_host_histogram_objective_dsigma", "gempe_host_random_relabel",
     "gempe_host_mix_seed", "gempe_default_iteration_config", "gempe_engine_create", "gempe_engine_destroy",
@@ -132,6 +133,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_open_peer": (i32, [vp, vp]),
         "gempe_add_peer_pointers": (i32, [vp, vp, vp]),
         "gempe_clear_peers": (i32, [vp]),
+        "gempe_exchange_ipc_handle": (i32, [vp, vp]),
+        "gempe_open_peer_exchange": (i32, [vp, i32, vp]),
+        "gempe_add_peer_exchange_pointer": (i32, [vp, i32, vp]),
+        "gempe_exchange_recv_area": (vp, [vp]),
         "gempe_device_coords_parity": (vp, [vp, i32]),
         "gempe_coords_parity": (i32, [vp]),
         "gempe_end_round": (i32, [vp]),

@@ -313,9 +313,16 @@ void build_structures(gempe_ctx* c) {
     c->ex_prefix.upload(prefix);
     const bool external = !region_mode && (world > 1 || c->opt.exchange == 2);
     c->ex_send.allocate(static_cast<std::size_t>(cap) * regions);
-    if (external) c->ex_recv.allocate(static_cast<std::size_t>(cap) * regions); else c->ex_recv.release();
+    // receive area: records [2 parities][regions][cap], then counts [2][regions] (one allocation = one IPC handle); the
+    // second parity is used by the direct exchange only
+    const std::size_t recv_records = 2 * static_cast<std::size_t>(cap) * regions;
+    if (external) c->ex_recv.allocate(recv_records + regions + 1, true); else c->ex_recv.release();
     c->ex_send_count.allocate(regions, true);
-    if (external) c->ex_recv_count.allocate(regions, true); else c->ex_recv_count.release();
+    c->ex_recv_count.release();
+    if (c->ex_registered) c->ex_peers_lost = true;  // a rebuild (relabel) moved the buffers: peers must register again
+    c->ex_peers.assign(external ? world : 0, gempe_ctx::ExchangePeer{});
+    c->ex_registered = 0;
+    if (external) c->ex_peers[rank].recv = c->ex_recv.get();
     const std::uint64_t spill_cap = region_mode ? c->slots : 0;
     c->ex_rank.allocate(static_cast<std::size_t>(cap) * regions + spill_cap);
     if (region_mode) {
@@ -341,7 +348,7 @@ void build_structures(gempe_ctx* c) {
     c->exchange.send_count = c->ex_send_count.get();
     // a single rank is its own peer: what it packed is what it receives
     c->exchange.recv = external ? c->ex_recv.get() : c->ex_send.get();
-    c->exchange.recv_count = external ? c->ex_recv_count.get() : c->ex_send_count.get();
+    c->exchange.recv_count = external ? reinterpret_cast<std::uint32_t*>(c->ex_recv.get() + recv_records) : c->ex_send_count.get();
   }
 
   timer.lap("uploads + allocations");
@@ -418,6 +425,9 @@ void require_live(gempe_ctx* c) {
 void bucket_received(gempe_ctx* c) {
   if (!c->pack_path) throw config_error("context was created without opt.exchange");
   if (!c->bucket_pending) throw config_error("gempe_bucket_received without a preceding gempe_begin_round");
+  if (c->ex_peers_lost && !c->exchange.direct) {
+    throw config_error("the exchange buffers were rebuilt (relabel): register the peers' receive areas again");
+  }
   c->launches += launch_bucket_records(c->exchange, c->exchange.regions, c->n, c->in_cnt.get(),
                                        c->in_off.get(), c->ex_rank.get(), c->in_anchor.get(), c->scan_scratch.get(), c->stream);
   if (c->opt.deterministic) c->launches += launch_sort_buckets(c->in_off.get(), c->in_anchor.get(), c->n, c->stream);
@@ -430,7 +440,22 @@ void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
              "memset status + tallies");
   const SampleArgs a = sample_args(c, iter);
   if (c->pack_path) {
+    ExchangeArgs& x = c->exchange;
+    x.direct = !c->ex_peers.empty() && c->ex_registered + 1 == c->ex_peers.size() && c->ex_peers.size() > 1;
+    if (x.direct) {
+      // receive buffers alternate between rounds: a fast rank may pack round t+1 while a slow one still buckets round t
+      const std::uint32_t world = x.regions, rank = static_cast<std::uint32_t>(c->opt.rank);
+      const std::size_t cap = x.capacity, records = 2 * cap * world;
+      const std::uint32_t parity = static_cast<std::uint32_t>(c->ex_round++ & 1);
+      x.recv = c->ex_recv.get() + static_cast<std::size_t>(parity) * world * cap;
+      x.recv_count = reinterpret_cast<std::uint32_t*>(c->ex_recv.get() + records) + parity * world;
+      for (std::uint32_t d = 0; d < world; ++d) {
+        x.dest_region[d] = c->ex_peers[d].recv + (static_cast<std::size_t>(parity) * world + rank) * cap;
+        x.dest_count[d] = reinterpret_cast<std::uint32_t*>(c->ex_peers[d].recv + records) + parity * world + rank;
+      }
+    }
     c->launches += launch_sample_pack(a, c->exchange, c->stream);
+    if (x.direct) c->launches += launch_publish_counts(c->exchange, c->stream);
     cuda_check(cudaGetLastError(), "sample + pack");
     c->bucket_pending = true;
     if (c->exchange.recv == c->exchange.send) bucket_received(c);  // own peer
@@ -537,6 +562,9 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
 using namespace gempe;
 
 gempe_ctx::~gempe_ctx() {
+  for (const ExchangePeer& p : ex_peers) {
+    if (p.ipc) cudaIpcCloseMemHandle(p.recv);
+  }
   for (const Peer& p : peers) {
     if (!p.ipc) continue;
     cudaIpcCloseMemHandle(p.x[0]);
@@ -1024,9 +1052,56 @@ int gempe_add_peer_pointers(gempe_ctx* c, void* x0, void* x1) {
   });
 }
 
+int gempe_exchange_ipc_handle(gempe_ctx* c, void* out) {
+  return guarded(c, [&] {
+    if (c->ex_peers.empty()) throw config_error("context has no external exchange buffers (opt.exchange with world > 1)");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, c->ex_recv.get()), "cudaIpcGetMemHandle");
+    std::memcpy(out, &h, sizeof h);
+  });
+}
+
+namespace {
+void register_exchange_peer(gempe_ctx* c, int peer_rank, uint2* recv, bool ipc) {
+  if (c->ex_peers.empty()) throw config_error("context has no external exchange buffers (opt.exchange with world > 1)");
+  if (peer_rank < 0 || peer_rank >= static_cast<int>(c->ex_peers.size()) || peer_rank == c->opt.rank) {
+    throw config_error("bad peer rank");
+  }
+  if (c->ex_peers[peer_rank].recv) throw config_error("peer already registered");
+  c->ex_peers[peer_rank].recv = recv;
+  c->ex_peers[peer_rank].ipc = ipc;
+  if (++c->ex_registered + 1 == c->ex_peers.size()) c->ex_peers_lost = false;
+}
+}  // namespace
+
+int gempe_open_peer_exchange(gempe_ctx* c, int peer_rank, const void* handle) {
+  return guarded(c, [&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* ptr = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    register_exchange_peer(c, peer_rank, static_cast<uint2*>(ptr), true);
+  });
+}
+
+int gempe_add_peer_exchange_pointer(gempe_ctx* c, int peer_rank, void* recv_area) {
+  return guarded(c, [&] {
+    if (!recv_area) throw config_error("null peer buffer");
+    register_exchange_peer(c, peer_rank, static_cast<uint2*>(recv_area), false);
+  });
+}
+
+void* gempe_exchange_recv_area(gempe_ctx* c) { return c->ex_recv.get(); }
+
 int gempe_clear_peers(gempe_ctx* c) {
   return guarded(c, [&] {
     cuda_check(cudaStreamSynchronize(c->stream), "clear peers");
+    for (std::size_t r = 0; r < c->ex_peers.size(); ++r) {
+      if (static_cast<int>(r) == c->opt.rank) continue;
+      if (c->ex_peers[r].ipc) cudaIpcCloseMemHandle(c->ex_peers[r].recv);
+      c->ex_peers[r] = gempe_ctx::ExchangePeer{};
+    }
+    c->ex_registered = 0;
     for (const gempe_ctx::Peer& p : c->peers) {
       if (!p.ipc) continue;
       cudaIpcCloseMemHandle(p.x[0]);

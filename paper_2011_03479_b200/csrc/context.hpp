@@ -101,6 +101,16 @@ struct gempe_ctx {
     bool ipc = false;  // opened with cudaIpcOpenMemHandle (closed on destroy)
   };
   std::vector<Peer> peers;
+  // direct sample exchange: every rank's receive area (records of both round parities, then the counts) in this rank's
+  // address space, indexed by rank; the own entry points at ex_recv.  Active once all world - 1 peers are registered.
+  struct ExchangePeer {
+    uint2* recv = nullptr;
+    bool ipc = false;
+  };
+  std::vector<ExchangePeer> ex_peers;
+  std::uint32_t ex_registered = 0;
+  bool ex_peers_lost = false;
+  std::uint64_t ex_round = 0;  // parity of the receive buffers in direct mode
   gempe::DeviceBuffer<uint4> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
   // gempe_step_host pipeline: item / vertex boundaries of the slices whose rows are copied out while later

@@ -281,13 +281,22 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
   if (have) {
     const std::uint32_t pos = sh_base[dest] + local;
     if (pos < x.capacity) {
-      x.send[static_cast<std::size_t>(dest) * x.capacity + pos] = make_uint2(partner, anchor);
+      uint2* region = x.direct ? x.dest_region[dest] : x.send + static_cast<std::size_t>(dest) * x.capacity;
+      region[pos] = make_uint2(partner, anchor);
     } else {
       const std::uint32_t at = x.spill ? atomicAdd(x.spill_count, 1u) : 0xffffffffu;
       if (at < x.spill_capacity) x.spill[at] = make_uint2(partner, anchor);
       else atomicOr(a.status + kStatExchangeOverflow, 1u);
     }
   }
+  if (x.direct) __threadfence_system();  // peer stores are performed before the grid retires
+}
+
+// direct exchange: tell every destination how many records this rank left in its region there
+__global__ void publish_counts_kernel(const ExchangeArgs x) {
+  const std::uint32_t d = threadIdx.x;
+  if (d < x.regions) *x.dest_count[d] = x.send_count[d];
+  __threadfence_system();
 }
 
 // received records -> per-partner counts and arrival ranks.  blockIdx.y = source region: the regions are walked one
@@ -2405,6 +2414,11 @@ int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t 
   if (x.spill) cudaMemsetAsync(x.spill_count, 0, sizeof(std::uint32_t), stream);
   if (x.own_slots == 0) return 0;
   sample_pack_kernel<<<blocks_for(x.own_slots, kThreads), kThreads, 2 * x.regions * sizeof(std::uint32_t), stream>>>(a, x);
+  return 1;
+}
+
+int launch_publish_counts(const ExchangeArgs& x, cudaStream_t stream) {
+  publish_counts_kernel<<<1, 32, 0, stream>>>(x);
   return 1;
 }
 

@@ -69,6 +69,8 @@ struct SampleArgs {
   Ownership own;
 };
 
+constexpr int kMaxPeers = 15;  // other ranks whose X_{t+1} copy this rank writes directly (world <= 16)
+
 // Sharded sampling with an exchange step: this rank samples the streams of the anchors it owns and packs
 // (partner, anchor) records by destination rank; after the all-to-all it buckets the records it received.
 struct ExchangeArgs {
@@ -89,6 +91,11 @@ struct ExchangeArgs {
   uint2* spill;
   std::uint32_t* spill_count;
   std::uint32_t spill_capacity;
+  // direct exchange (every peer's receive buffers opened in this process): the pack kernel stores a record for rank d
+  // straight into the region reserved for THIS rank in d's receive buffer -- no all-to-all follows.  Null otherwise.
+  int direct;
+  uint2* dest_region[kMaxPeers + 1];          // [world] region `rank` of rank d's receive buffer (current parity)
+  std::uint32_t* dest_count[kMaxPeers + 1];   // [world] slot `rank` of rank d's receive counts (current parity)
 };
 
 // Two-level counting sort of the accepted samples by partner (large n).
@@ -101,7 +108,6 @@ struct PartitionArgs {
   uint2* records;               // [S] (partner, anchor), grouped by coarse bucket
 };
 
-constexpr int kMaxPeers = 15;  // other ranks whose X_{t+1} copy this rank writes directly (world <= 16)
 
 struct GatherArgs {
   const float* x_cur;
@@ -156,6 +162,8 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
                  cudaStream_t stream);
 int launch_sample(const SampleArgs& a, cudaStream_t stream);
 int launch_sample_pack(const SampleArgs& a, const ExchangeArgs& x, cudaStream_t stream);
+// direct exchange: fill counts of this rank's regions on every destination (after launch_sample_pack, same stream)
+int launch_publish_counts(const ExchangeArgs& x, cudaStream_t stream);
 int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uint32_t n, std::uint32_t* in_cnt,
                           std::uint32_t* in_off, std::uint32_t* rec_rank, std::uint32_t* in_anchor, std::uint32_t* scratch,
                           cudaStream_t stream);

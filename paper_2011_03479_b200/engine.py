@@ -332,6 +332,22 @@ class Context:
     def add_peer_pointers(self, x_parity0: int, x_parity1: int):
         self._check(self._L.gempe_add_peer_pointers(self._h, C.c_void_p(x_parity0), C.c_void_p(x_parity1)))
 
+    # direct sample exchange
+    def exchange_ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._check(self._L.gempe_exchange_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def open_peer_exchange(self, peer_rank: int, handle: bytes):
+        self._check(self._L.gempe_open_peer_exchange(self._h, peer_rank, C.c_char_p(handle)))
+
+    def add_peer_exchange_pointer(self, peer_rank: int, recv_area: int):
+        self._check(self._L.gempe_add_peer_exchange_pointer(self._h, peer_rank, C.c_void_p(recv_area)))
+
+    @property
+    def exchange_recv_area(self) -> int:
+        return self._L.gempe_exchange_recv_area(self._h)
+
     def clear_peers(self):
         self._check(self._L.gempe_clear_peers(self._h))
 

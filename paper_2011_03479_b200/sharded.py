@@ -14,7 +14,9 @@ replicated integer work).  The 2x512 tallies are summed with one all_reduce.
 `peer_broadcast=True` removes the all-gather altogether: the ranks open each other's coordinate buffers (CUDA IPC,
 peer memory over NVLink / NVSwitch) and the gather kernel stores every row it updates into all ranks' X_{t+1}
 directly -- the update and its broadcast are one kernel, the transfer rides under the remaining rows' compute.
-Between consecutive rounds the ranks pass a barrier (a one-element all_reduce, or the tally all_reduce).
+Between consecutive rounds the ranks pass a barrier (a one-element all_reduce, or the tally all_reduce).  With the
+sample exchange on, the records travel the same way (the pack kernel stores them into the owners' receive areas) and
+ONE barrier per round, between packing and bucketing, orders both transfers.
 
 The collective logic is backend-agnostic (`ops` supplies the compute); tests drive it with gloo on CPU
 tensors, the product with `CudaShardOps` over NCCL.
@@ -59,6 +61,7 @@ class CudaShardOps:
         self.ctx.set_stream(self.stream.cuda_stream)
         self.rows, self.ld = self.ctx.padded_rows, self.ctx.row_stride
         self._exchange = None
+        self.direct_exchange = False  # records travel by peer stores from the pack kernel (connect_peers)
         if kw.get("exchange"):
             send, recv, send_cnt, recv_cnt, cap = self.ctx.exchange_layout()
             if recv != send:  # a single-rank context with exchange=1 is its own peer and buckets inside begin_round
@@ -71,12 +74,20 @@ class CudaShardOps:
         world = dist.get_world_size(group)
         if world == 1:
             return
-        mine = self.ctx.coords_ipc_handles()
+        me = dist.get_rank(group)
+        mine = (self.ctx.coords_ipc_handles(), self.ctx.exchange_ipc_handle() if self._exchange is not None else None)
         handles = [None] * world
         dist.all_gather_object(handles, mine, group=group)
         for r in range(world):
-            if r != dist.get_rank(group):
-                self.ctx.open_peer(handles[r])
+            if r != me:
+                self.ctx.open_peer(handles[r][0])
+        if self._exchange is not None and all(h[1] is not None for h in handles):
+            # direct sample exchange: the pack kernel writes into the peers' receive areas, no all-to-all
+            for r in range(world):
+                if r != me:
+                    self.ctx.open_peer_exchange(r, handles[r][1])
+            self._exchange = None
+            self.direct_exchange = True
 
     def exchange_tensors(self):
         """(send_records[world,cap,2], recv_records, send_counts[world], recv_counts) or None."""
@@ -154,7 +165,13 @@ class ShardedEngine:
         with ctx:
             self.ops.begin_round(mu, sigma, it)  # X-independent: overlaps the previous round's last exchange
             bufs = self.ops.exchange_tensors() if hasattr(self.ops, "exchange_tensors") else None
-            if bufs is not None:
+            if getattr(self.ops, "direct_exchange", False):
+                # the pack kernel already stored the records at their owners: one barrier orders every rank's pack
+                # (and its previous gather, whose peer stores filled X_t) before anybody buckets and gathers
+                self._wait_pending()
+                self._round_barrier(wait=True)
+                self.ops.bucket_received()
+            elif bufs is not None:
                 # region d of every rank's send side lands in region <source rank> of rank d's receive side
                 send, recv, send_cnt, recv_cnt = bufs
                 dist.all_to_all_single(recv_cnt, send_cnt, group=self.group)
@@ -170,16 +187,20 @@ class ShardedEngine:
                     mine = region[self.rank * self.block_rows:(self.rank + 1) * self.block_rows]
                     self._pending.append(dist.all_gather_into_tensor(region, mine, group=self.group, async_op=True))
             self.ops.end_round()
-            if self.peer_broadcast:
-                self._round_barrier()
+            if self.peer_broadcast and not getattr(self.ops, "direct_exchange", False):
+                self._round_barrier()  # with the direct exchange the barrier after the next pack does this job
 
-    def _round_barrier(self):
+    def _round_barrier(self, wait: bool = False):
         """No rank may start the next gather before every rank has finished this one (it reads what the peers wrote
         and overwrites what they were reading)."""
         if dist.get_backend(self.group) == "nccl":
             if self._flag is None:
                 self._flag = torch.zeros(1, device="cuda")
-            self._pending.append(dist.all_reduce(self._flag, group=self.group, async_op=True))  # stream-ordered
+            work = dist.all_reduce(self._flag, group=self.group, async_op=True)  # stream-ordered
+            if wait:
+                work.wait()
+            else:
+                self._pending.append(work)
         else:  # host-side backend (gloo): drain the stream, then meet
             torch.cuda.current_stream().synchronize()
             dist.barrier(group=self.group)

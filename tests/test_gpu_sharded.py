@@ -128,9 +128,10 @@ def test_rank_contexts_with_sample_exchange_reproduce_the_single_gpu_round(world
 @pytest.mark.parametrize("world,chunks,exchange", [(2, 1, 0), (4, 1, 1), (8, 2, 1), (16, 1, 0)])
 @pytest.mark.parametrize("mode,k", [(0, 0), (1, 6)])
 def test_fused_update_and_broadcast_into_peer_buffers(world, chunks, exchange, mode, k):
-    """Peer broadcast: the rank contexts of one process register each other's coordinate buffers and every gather
-    kernel stores the rows it updates into all of them -- no copy stands in for an all-gather here.  Ranks are stepped
-    one after another; after the last one every rank must hold the single-GPU X_{t+1} bit for bit."""
+    """Peer broadcast: the rank contexts of one process register each other's coordinate buffers (and, with the sample
+    exchange on, each other's receive areas): every gather kernel stores the rows it updates into all of them and every
+    pack kernel stores its records at their owners -- no copy stands in for a collective here.  Ranks are stepped one
+    after another; after the last one every rank must hold the single-GPU X_{t+1} bit for bit."""
     import torch
     import paper_2011_03479_b200 as G
     for (n, src, dst), dim in ((er_graph(1003, 6000, 3), 64), (er_graph(1003, 6000, 3), 128),
@@ -139,24 +140,19 @@ def test_fused_update_and_broadcast_into_peer_buffers(world, chunks, exchange, m
         single = G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64)
         ranks = [G.Context(g, dim, 5, neg_mode=mode, negatives=k, deterministic=True, chunk_entries=64, rank=r,
                            world=world, comm_chunks=chunks, exchange=exchange) for r in range(world)]
-        for a in ranks:
-            for b in ranks:
+        for ra, a in enumerate(ranks):
+            for rb, b in enumerate(ranks):
                 if a is not b:
                     a.add_peer_pointers(b.device_coords_parity(0), b.device_coords_parity(1))
-        views = [_exchange_views(c, world) for c in ranks] if exchange else None
+                    if exchange:  # direct sample exchange: the pack kernel writes into b's receive area
+                        a.add_peer_exchange_pointer(rb, b.exchange_recv_area)
         sigma = 1.0
         for it in range(3):
             he, hn = single.iterate(1.5, sigma, it)
             want = single.get_coords()
             for c in ranks:
-                c.begin_round(1.5, sigma, it)
-            if exchange:
-                torch.cuda.synchronize()
-                for s_rank in range(world):
-                    for d in range(world):
-                        views[d][1][s_rank].copy_(views[s_rank][0][d])
-                        views[d][3][s_rank] = views[s_rank][2][d]
-                torch.cuda.synchronize()
+                c.begin_round(1.5, sigma, it)  # exchange: no copy stands in for an all-to-all either
+            torch.cuda.synchronize()
             tot_e, tot_n = np.zeros(512, np.uint64), np.zeros(512, np.uint64)
             for c in ranks:
                 assert c.coords_parity == it % 2
@@ -178,9 +174,10 @@ def test_fused_update_and_broadcast_into_peer_buffers(world, chunks, exchange, m
             c.close()
 
 
-def _ipc_worker(rank, world, port, results):
+def _ipc_worker(rank, world, port, exchange, results):
     """One process per rank, all on cuda:0 (time-sliced; no kernel waits on another process): gloo carries the IPC
-    handles, the tallies and the barriers, the coordinates travel only through the peer stores of the gather kernel."""
+    handles, the tallies and the barriers; the coordinates travel only through the peer stores of the gather kernel and
+    (exchange) the sample records only through those of the pack kernel."""
     import os
     import torch
     import torch.distributed as dist
@@ -193,8 +190,8 @@ def _ipc_worker(rank, world, port, results):
         n, src, dst = er_graph(2003, 12000, 4)
         g = G.Graph(n, src, dst)
         eng = sharded.make_cuda_engine(g, 64, 5, device=0, neg_mode=1, negatives=6, deterministic=True,
-                                       exchange=False, peer_broadcast=True)
-        assert eng.peer_broadcast and eng.chunks == 1
+                                       exchange=exchange, peer_broadcast=True)
+        assert eng.peer_broadcast and eng.chunks == 1 and eng.ops.direct_exchange == exchange
         plain = G.Context(g, 64, 5, neg_mode=1, negatives=6, deterministic=True)
         ok = True
         sigma = 1.0
@@ -213,7 +210,8 @@ def _ipc_worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_peer_broadcast_across_processes_over_cuda_ipc():
+@pytest.mark.parametrize("exchange", [False, True])
+def test_peer_broadcast_across_processes_over_cuda_ipc(exchange):
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
@@ -221,7 +219,7 @@ def test_peer_broadcast_across_processes_over_cuda_ipc():
         port = s.getsockname()[1]
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_ipc_worker, args=(2, port, results), nprocs=2, join=True)
+    mp.spawn(_ipc_worker, args=(2, port, exchange, results), nprocs=2, join=True)
     assert dict(results) == {0: True, 1: True}
 
 
