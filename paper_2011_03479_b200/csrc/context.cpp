@@ -986,6 +986,9 @@ int gempe_probe(gempe_ctx* c, const std::uint32_t* i, const std::uint32_t* j, st
 int gempe_sample(gempe_ctx* c, std::uint64_t iter_index, std::uint32_t* partners, std::uint64_t* total_draws) {
   return guarded(c, [&] {
     require_live(c);
+    if (c->ex_registered) {
+      throw config_error("gempe_sample is a single-context test hook: it would store records into the registered peers");
+    }
     c->round_iter = iter_index;
     sampling_passes(c, iter_index);
     const std::uint32_t* result = c->neg_own.get();
