@@ -360,11 +360,36 @@ def main():
             except Exception as e:  # the reference build is test infrastructure; its absence is reported, not fatal
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
-    elif rank == 0:
-        x_bytes = n * dim * 4
-        line["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                       "note": "multi-GPU e2e not measured separately; state is device-resident (see N=1 line)",
-                       "allgather_bytes_per_step": int(x_bytes * (world - 1) / world)}
+    if world > 1:
+        # end to end at N GPUs with HOST buffers: every rank uploads X_t (each needs all of it; N PCIe links in
+        # parallel), the round runs, every rank returns the rows it owns (together X_{t+1}) and the job-wide tallies
+        x_host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+        ctx.get_coords(x_host.numpy())
+        block, rows_pad, ld = eng.block_rows, eng.ops.rows, eng.ops.ld
+        own = [(min(n, (ch * world + rank) * block), min(n, (ch * world + rank + 1) * block)) for ch in range(eng.chunks)]
+        out_host = torch.empty((sum(hi - lo for lo, hi in own), dim), dtype=torch.float32, pin_memory=True)
+        t_e2e = []
+        for s in range(max(1, args.e2e_steps) + 1):
+            barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                ctx.set_coords(x_host.numpy())
+                eng.round_async(mu, sigma, eng.iter + args.steps + s)
+                eng.finish_round()
+                x_dev = torch.as_tensor(sharded._DeviceArray(ctx.device_coords(0), (rows_pad, ld)), device=eng.ops.device)
+                at = 0
+                for lo, hi in own:
+                    out_host[at:at + hi - lo].copy_(x_dev[lo:hi, :dim], non_blocking=True)
+                    at += hi - lo
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            t_e2e.append(float(dt.item()))
+        e2e_s = float(np.median(t_e2e[1:]))
+        if rank == 0:
+            line["e2e"] = {"value": pair_terms / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(world * n * dim * 4),
+                           "d2h_bytes_per_step": int(n * dim * 4 + 2 * 512 * 8), "ms_per_step": e2e_s * 1e3,
+                           "call": "per rank: X_t in (pinned host), sharded round, owned rows of X_{t+1} + tallies out"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
