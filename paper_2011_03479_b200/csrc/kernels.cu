@@ -1435,7 +1435,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
 template <int VEC, bool PRECISE>
 __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArgs a, std::uint32_t item_lo,
                                                                  std::uint32_t item_hi) {
-  constexpr int kInflight = 4;
+#ifndef GEMPE_INFLIGHT
+#define GEMPE_INFLIGHT 4
+#endif
+  constexpr int kInflight = GEMPE_INFLIGHT;
   __shared__ unsigned int sh_hist[2 * kBins];
   using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
   __shared__ tab_t sh_tab;
