@@ -174,6 +174,45 @@ def test_fused_update_and_broadcast_into_peer_buffers(world, chunks, exchange, m
             c.close()
 
 
+def test_exchange_and_peer_api_misuse_is_reported():
+    """The sharding entry points fail loudly (config_error) when called out of order or on the wrong kind of context."""
+    import paper_2011_03479_b200 as G
+    n, src, dst = er_graph(500, 2000, 1)
+    g = G.Graph(n, src, dst)
+    plain = G.Context(g, 8, 1)
+    with pytest.raises(G.ConfigError):
+        plain.exchange_layout()              # no exchange buffers
+    with pytest.raises(G.ConfigError):
+        plain.bucket_received()              # nothing packed
+    with pytest.raises(G.ConfigError):
+        plain.exchange_ipc_handle()          # single rank: nothing to publish
+    with pytest.raises(G.ConfigError):
+        plain.add_peer_pointers(0, 0)        # null buffers
+    a = G.Context(g, 8, 1, rank=0, world=2, exchange=1)
+    b = G.Context(g, 8, 1, rank=1, world=2, exchange=1)
+    with pytest.raises(G.ConfigError):
+        a.add_peer_exchange_pointer(0, b.exchange_recv_area)   # own rank
+    with pytest.raises(G.ConfigError):
+        a.add_peer_exchange_pointer(2, b.exchange_recv_area)   # outside the world
+    a.add_peer_exchange_pointer(1, b.exchange_recv_area)
+    with pytest.raises(G.ConfigError):
+        a.add_peer_exchange_pointer(1, b.exchange_recv_area)   # twice
+    with pytest.raises(G.ConfigError):
+        a.sample(0)                          # the hook would write into b
+    a.begin_round(1.5, 1.0, 0)
+    with pytest.raises(G.ConfigError):
+        a.gather_chunk(0)                    # records packed but not bucketed
+    with pytest.raises(G.ConfigError):
+        a.gather_chunk(5)                    # no such chunk
+    a.clear_peers()
+    for c in (plain, a, b):
+        c.close()
+    with pytest.raises(G.ConfigError):
+        G.Context(g, 8, 1, rank=2, world=2)  # rank outside the world
+    with pytest.raises(G.ConfigError):
+        G.Context(g, 8, 1, exchange=7)
+
+
 def _ipc_worker(rank, world, port, exchange, results):
     """One process per rank, all on cuda:0 (time-sliced; no kernel waits on another process): gloo carries the IPC
     handles, the tallies and the barriers; the coordinates travel only through the peer stores of the gather kernel and
