@@ -337,6 +337,25 @@ def main():
                                   "what": "round + device sigma search + PE estimate (run_single_iteration), no host sync"}
         ctx.elapsed_ms()
 
+        # small graphs: the same rounds as one CUDA graph of 50, gaps between the ~5 kernels removed
+        if ms_per_step < 1.0:
+            reps = 50
+            ctx.graph_capture(mu, sigma, eng.iter + 100, reps)
+            ctx.graph_launch()
+            torch.cuda.synchronize()
+            if reps % 2:
+                ctx.graph_capture(mu, sigma, eng.iter + 100, reps)
+            ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ge0.record(stream)
+            ctx.graph_launch()
+            ge1.record(stream)
+            torch.cuda.synchronize()
+            ctx.sync()
+            g_ms = ge0.elapsed_time(ge1) / reps
+            line["cuda_graph"] = {"rounds_per_graph": reps, "ms_per_step": g_ms, "value": pair_terms / (g_ms * 1e-3),
+                                  "unit": UNIT, "what": "50 rounds captured into one CUDA graph, one launch"}
+            ctx.elapsed_ms()
+
         # end to end through the C-ABI with HOST buffers: X_t in (pinned), round, X_{t+1} + tallies out
         x_host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
         x_np = x_host.numpy()

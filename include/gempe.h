@@ -131,6 +131,14 @@ int gempe_step_host(gempe_ctx* ctx, const float* x_in, float* x_out, double mu, 
 /* Same round, enqueue-only: no host synchronisation.  gempe_sync waits, checks the status word and
  * returns the tallies of the LAST round. */
 int gempe_iterate_async(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index);
+/* `count` consecutive rounds (iteration indices first_iter .. first_iter + count - 1, fixed mu and sigma) captured
+ * into one CUDA graph and replayed with one launch: small graphs (BASELINE configs 1-2) are bound by the gaps
+ * between their ~5 kernels per round, not by the kernels.  gempe_graph_launch is asynchronous (gempe_sync waits and
+ * returns the tallies of the LAST round); a replay repeats the same sample streams from the current coordinates.
+ * Capture again after anything that swaps the coordinate buffers an odd number of times, after gempe_relabel, and
+ * to change sigma.  Single-rank contexts only. */
+int gempe_graph_capture(gempe_ctx* ctx, double mu, double sigma, uint64_t first_iter, int count);
+int gempe_graph_launch(gempe_ctx* ctx);
 int gempe_sync(gempe_ctx* ctx, uint64_t* hist_edge, uint64_t* hist_nonedge);
 
 /* Device-resident sigma feedback: optimize_sigma_detail, the 1.5x growth cap and the PE

@@ -562,6 +562,7 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
 using namespace gempe;
 
 gempe_ctx::~gempe_ctx() {
+  if (round_graph) cudaGraphExecDestroy(round_graph);
   for (const ExchangePeer& p : ex_peers) {
     if (p.ipc) cudaIpcCloseMemHandle(p.recv);
   }
@@ -829,6 +830,62 @@ int gempe_iterate_async(gempe_ctx* c, double mu, double sigma, std::uint64_t ite
     gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
     cuda_check(cudaEventRecord(next_event(c), c->stream), "event");
     c->cur ^= 1;
+  });
+}
+
+// ---- CUDA-graph replay of a run of rounds (fixed mu, sigma; iteration indices first_iter .. first_iter + count - 1) ----
+int gempe_graph_capture(gempe_ctx* c, double mu, double sigma, std::uint64_t first_iter, int count) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (count < 1) throw config_error("graph needs at least one round");
+    if (c->opt.world != 1 || (c->pack_path && c->exchange.recv != c->exchange.send)) {
+      throw config_error("graph capture is for single-rank contexts");
+    }
+    if (c->round_graph) {
+      cudaGraphExecDestroy(c->round_graph);
+      c->round_graph = nullptr;
+    }
+    set_round_math(c, mu, sigma);
+    const int start = c->cur;
+    const std::uint64_t launches0 = c->launches;
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      for (int r = 0; r < count; ++r) {
+        sampling_passes(c, first_iter + static_cast<std::uint64_t>(r));
+        gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
+        c->cur ^= 1;
+      }
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      c->cur = start;
+      throw;
+    }
+    c->cur = start;  // nothing ran yet: the parity moves when the graph is launched
+    cuda_check(cudaStreamEndCapture(c->stream, &graph), "end capture");
+    c->graph_launches_per_replay = c->launches - launches0;
+    c->launches = launches0;
+    const cudaError_t inst = cudaGraphInstantiate(&c->round_graph, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(inst, "graph instantiate");
+    c->graph_rounds = count;
+    c->graph_start_parity = start;
+    c->graph_last_iter = first_iter + static_cast<std::uint64_t>(count) - 1;
+  });
+}
+
+int gempe_graph_launch(gempe_ctx* c) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (!c->round_graph) throw config_error("no captured graph (gempe_graph_capture)");
+    if (c->cur != c->graph_start_parity) {
+      throw config_error("the coordinate buffers have swapped since the capture: capture again");
+    }
+    cuda_check(cudaGraphLaunch(c->round_graph, c->stream), "graph launch");
+    c->launches += c->graph_launches_per_replay;
+    c->round_iter = c->graph_last_iter;
+    if (c->graph_rounds & 1) c->cur ^= 1;
   });
 }
 

@@ -93,6 +93,10 @@ struct gempe_ctx {
   gempe::DeviceBuffer<std::uint64_t> ex_first_slot, ex_prefix;
   gempe::DeviceBuffer<uint2> ex_send, ex_recv, ex_spill;
   gempe::DeviceBuffer<std::uint32_t> ex_send_count, ex_recv_count, ex_rank, ex_spill_count;
+  // a captured run of rounds (gempe_graph_capture): small graphs are bound by launch gaps, a CUDA graph removes them
+  cudaGraphExec_t round_graph = nullptr;
+  int graph_rounds = 0, graph_start_parity = 0;
+  std::uint64_t graph_launches_per_replay = 0, graph_last_iter = 0;
   bool pack_path = false;       // sampling goes through sample_pack + bucket_records (opt.exchange, or bucket_mode 3)
   bool bucket_pending = false;  // records packed, gempe_bucket_received not yet called
   // fused update + broadcast: X buffers (both parities, indexed like x[]) of the other ranks, in this rank's address space

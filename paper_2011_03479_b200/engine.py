@@ -255,6 +255,13 @@ class Context:
                                                _capi.ptr(hn)))
         return s.value, pe.value, nw.value, he, hn
 
+    def graph_capture(self, mu: float, sigma: float, first_iter: int, count: int):
+        """Captures `count` rounds into a CUDA graph (replayed by graph_launch)."""
+        self._check(self._L.gempe_graph_capture(self._h, mu, sigma, first_iter, count))
+
+    def graph_launch(self):
+        self._check(self._L.gempe_graph_launch(self._h))
+
     def iterate_auto_async(self, iter_index: int):
         self._check(self._L.gempe_iterate_auto_async(self._h, iter_index))
 

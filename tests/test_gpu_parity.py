@@ -662,6 +662,36 @@ def test_zero_negatives_per_vertex_and_large_k(G, oracle, golden_fastmath):
     check_round(G, oracle, golden_fastmath, (n, src, dst), 8, seed=2, neg_mode=1, k=70, iters=1)  # buckets > 32 entries
 
 
+@pytest.mark.parametrize("dim,mode,k,count", [(2, 1, 5, 6), (2, 0, 0, 5), (64, 1, 4, 3), (128, 1, 6, 4)])
+def test_cuda_graph_replay_equals_the_same_rounds_launched_one_by_one(G, dim, mode, k, count):
+    """gempe_graph_capture / gempe_graph_launch: `count` rounds in one CUDA graph give bit-identical coordinates and
+    last-round tallies (sorted buckets), for even and odd counts (buffer parity), and a second replay continues from
+    the coordinates the first one left."""
+    n, src, dst = er_graph(4000, 20000, 21)
+    g = G.Graph(n, src, dst)
+    a = G.Context(g, dim, 3, neg_mode=mode, negatives=k, deterministic=True)
+    b = G.Context(g, dim, 3, neg_mode=mode, negatives=k, deterministic=True)
+    for it in range(2):  # some history first
+        a.iterate(1.5, 1.0, it)
+        b.iterate(1.5, 1.0, it)
+    with pytest.raises(G.ConfigError):
+        b.graph_launch()  # nothing captured
+    b.graph_capture(1.5, 0.9, 2, count)
+    for replay in range(2):
+        for r in range(count):
+            he, hn = a.iterate(1.5, 0.9, 2 + r)
+        if replay == 1 and count % 2 == 1:
+            with pytest.raises(G.ConfigError):  # an odd replay swapped the buffers: the capture is stale
+                b.graph_launch()
+            b.graph_capture(1.5, 0.9, 2, count)
+        b.graph_launch()
+        ge, gn = b.sync()
+        assert np.array_equal(he, ge) and np.array_equal(hn, gn)
+        assert np.array_equal(a.get_coords().view(np.uint32), b.get_coords().view(np.uint32))
+    a.close()
+    b.close()
+
+
 def test_many_rounds_async_then_sync_matches_stepwise(G):
     n, src, dst = er_graph(2000, 9000, 4)
     a = G.Context(G.Graph(n, src, dst), 32, 6, neg_mode=1, negatives=5, deterministic=True)
