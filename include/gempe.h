@@ -131,6 +131,22 @@ int gempe_step_host(gempe_ctx* ctx, const float* x_in, float* x_out, double mu, 
 /* Same round, enqueue-only: no host synchronisation.  gempe_sync waits, checks the status word and
  * returns the tallies of the LAST round. */
 int gempe_iterate_async(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index);
+/* Quality scoring on the device: pe_sampled (src/metrics.cpp:166-213) of the context's CURRENT coordinates.  Edge sum
+ * exact; non-edge sum from samples_per_edge sampled partners per edge, reweighted by (N - m) / #samples; the
+ * predictive entropy is minimised over (mu, sigma) exactly as minimize_pe does (21-point mu grid, sigma by bisection
+ * on d/dsigma, golden-section refinement; src/metrics.cpp:73-127) with the exact-erf description length.  The sample
+ * stream is counter-based and the edge test is the run's hash set, so the result agrees with the reference's
+ * pe_sampled / pe_exact statistically (sampling noise), not draw for draw. */
+typedef struct gempe_pe_report {
+  double pe;                /* bits per pair */
+  double mu_star, sigma_star;
+  double h_basic;           /* basic_entropy of the graph (src/graph.cpp:208-217) */
+  double compression_ratio; /* pe / h_basic */
+  double grid_pe;           /* grid minimum before the refinement */
+  uint64_t nonedge_samples; /* samples that entered the estimate */
+} gempe_pe_report;
+int gempe_pe_sampled(gempe_ctx* ctx, int samples_per_edge, uint64_t seed, gempe_pe_report* out);
+
 /* `count` consecutive rounds (iteration indices first_iter .. first_iter + count - 1, fixed mu and sigma) captured
  * into one CUDA graph and replayed with one launch: small graphs (BASELINE configs 1-2) are bound by the gaps
  * between their ~5 kernels per round, not by the kernels.  gempe_graph_launch is asynchronous (gempe_sync waits and

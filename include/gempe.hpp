@@ -253,6 +253,17 @@ class EmbeddingEngine {
   }
   double sigma() const { return gempe_engine_sigma(handle_); }
 
+  // metrics.hpp:11-27: pe_sampled of the engine's current embedding, computed on the device
+  struct PEReport {
+    double pe = 0.0, mu_star = 0.0, sigma_star = 0.0, h_basic = 0.0, compression_ratio = 0.0, grid_pe = 0.0;
+  };
+  PEReport pe_sampled(int samples_per_edge, std::uint64_t seed) {
+    gempe_pe_report r{};
+    const int rc = gempe_pe_sampled(gempe_engine_context(handle_), samples_per_edge, seed, &r);
+    detail::check(rc, gempe_last_error(gempe_engine_context(handle_)));
+    return PEReport{r.pe, r.mu_star, r.sigma_star, r.h_basic, r.compression_ratio, r.grid_pe};
+  }
+
  private:
   gempe_engine* handle_ = nullptr;
   std::uint32_t n_;

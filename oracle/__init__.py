@@ -252,6 +252,8 @@ class Ref:
                                      C.POINTER(C.c_double)]
         L.ref_pe_exact.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, C.c_uint32, f32p,
                                    C.POINTER(C.c_double)]
+        L.ref_pe_sampled.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, C.c_uint32, f32p, C.c_int, C.c_uint64,
+                                     C.POINTER(C.c_double)]
         L.ref_load_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
         L.ref_write_embedding_tsv.restype = C.c_long
@@ -350,6 +352,17 @@ class Ref:
         rc = self.lib.ref_pe_exact(n, len(src), np.ascontiguousarray(src, np.uint32),
                                    np.ascontiguousarray(dst, np.uint32), coords.shape[1], coords,
                                    C.byref(pe))
+        if rc:
+            raise RuntimeError(self.error())
+        return pe.value
+
+
+    def pe_sampled(self, n, src, dst, coords, samples_per_edge, seed):
+        pe = C.c_double()
+        coords = np.ascontiguousarray(coords, np.float32)
+        rc = self.lib.ref_pe_sampled(n, len(src), np.ascontiguousarray(src, np.uint32),
+                                     np.ascontiguousarray(dst, np.uint32), coords.shape[1], coords,
+                                     samples_per_edge, seed, C.byref(pe))
         if rc:
             raise RuntimeError(self.error())
         return pe.value

@@ -324,6 +324,21 @@ int ref_pe_exact(std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
   }
 }
 
+// metrics.cpp:166 pe_sampled -- scoring only.
+int ref_pe_sampled(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const std::uint32_t* dst,
+                   std::uint32_t dim, const float* coords, int samples_per_edge, std::uint64_t seed, double* pe) {
+  try {
+    ee::Embedding e;
+    e.n = n;
+    e.dim = dim;
+    e.coords.assign(coords, coords + static_cast<std::size_t>(n) * dim);
+    *pe = ee::pe_sampled(make_graph(n, m, src, dst), e, samples_per_edge, seed).pe;
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
 // ---- graph.cpp:75-170, io.cpp:17-46 (text formats) ---------------------------------------------------------
 // Returns 0 and fills n / m (call again with arrays sized n / m to receive them), 2 on data_error, 5 on
 // parse_error with *line set.

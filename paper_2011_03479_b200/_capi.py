@@ -24,7 +24,7 @@ SYMBOLS = [
     "gempe_default_options", "gempe_create", "gempe_destroy", "gempe_last_error", "gempe_is_degenerate",
     "gempe_hash_bits", "gempe_sample_slots", "gempe_pair_terms", "gempe_algorithmic_bytes",
     "gempe_get_work_graph", "gempe_set_coords", "gempe_get_coords", "gempe_init_coords", "gempe_relabel",
-    "gempe_iterate", "gempe_step_host", "gempe_iterate_async", "gempe_graph_capture", "gempe_graph_launch", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
+    "gempe_iterate", "gempe_step_host", "gempe_iterate_async", "gempe_graph_capture", "gempe_graph_launch", "gempe_pe_sampled", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
     "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_probe",
     "gempe_sample", "gempe_set_stream", "gempe_device_coords", "gempe_row_stride", "gempe_padded_rows",
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_exchange_layout", "gempe_bucket_received", "gempe_gather_chunk", "gempe_coords_ipc_handles", "gempe_open_peer",
@@ -38,6 +38,11 @@ SYMBOLS = [
     "gempe_parse_graph_snapshot", "gempe_load_graph_file", "gempe_write_graph_snapshot", "gempe_graph_free",
     "gempe_write_embedding_tsv",
 ]
+
+
+class PeReportC(C.Structure):
+    _fields_ = [("pe", C.c_double), ("mu_star", C.c_double), ("sigma_star", C.c_double), ("h_basic", C.c_double),
+                ("compression_ratio", C.c_double), ("grid_pe", C.c_double), ("nonedge_samples", C.c_uint64)]
 
 
 class Options(C.Structure):
@@ -126,6 +131,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_block_rows": (u32, [vp]),
         "gempe_graph_capture": (i32, [vp, dbl, dbl, u64, i32]),
         "gempe_graph_launch": (i32, [vp]),
+        "gempe_pe_sampled": (i32, [vp, i32, u64, C.POINTER(PeReportC)]),
         "gempe_begin_round": (i32, [vp, dbl, dbl, u64]),
         "gempe_begin_round_auto": (i32, [vp, u64]),
         "gempe_exchange_layout": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_uint32)]),

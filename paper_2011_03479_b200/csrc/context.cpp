@@ -833,6 +833,124 @@ int gempe_iterate_async(gempe_ctx* c, double mu, double sigma, std::uint64_t ite
   });
 }
 
+// ---- pe_sampled on the device (metrics.cpp:73-127, 166-213) -----------------------------------------------
+int gempe_pe_sampled(gempe_ctx* c, int samples_per_edge, std::uint64_t seed, gempe_pe_report* out) {
+  return guarded(c, [&] {
+    if (!out) throw config_error("null report");
+    if (samples_per_edge < 1) throw config_error("samples_per_edge must be >= 1");
+    const double pairs = static_cast<double>(c->n) * (c->n > 0 ? c->n - 1 : 0) / 2.0;
+    const double edges = static_cast<double>(c->m);
+    *out = gempe_pe_report{};
+    {  // basic_entropy (graph.cpp:208-217)
+      const double p = pairs > 0.0 ? edges / pairs : 0.0;
+      double h = 0.0;
+      if (p > 0.0) h -= p * std::log2(p);
+      if (p < 1.0 && pairs > 0.0) h -= (1.0 - p) * std::log2(1.0 - p);
+      out->h_basic = h;
+    }
+    if (c->degenerate) throw config_error("cannot score a degenerate graph");
+    cuda_check(cudaStreamSynchronize(c->stream), "pe_sampled");
+    const bool complete = edges >= pairs;  // no non-edges: nothing to sample (metrics.cpp:170-179)
+    const std::uint64_t sps = complete ? 0 : static_cast<std::uint64_t>(samples_per_edge);
+    DeviceBuffer<float> edge_d, non_d;
+    DeviceBuffer<double> sums;
+    DeviceBuffer<unsigned long long> valid;
+    edge_d.allocate(c->m);
+    non_d.allocate(std::max<std::uint64_t>(1, c->m * sps));
+    sums.allocate(2, true);
+    valid.allocate(1, true);
+    PeCollectArgs p{};
+    p.x = c->x[c->cur].get();
+    p.n = c->n; p.dim = c->dim; p.ld = c->ld; p.m = c->m;
+    p.src = c->tmp_src.get(); p.dst = c->tmp_dst.get(); p.rowptr = c->rowptr.get();
+    p.hash_words = c->hash_words.get();
+    p.hash_summary = c->hash_summary.size() ? c->hash_summary.get() : nullptr;
+    p.hash_mask = static_cast<std::uint32_t>((1ull << c->hash_bits) - 1);
+    p.samples_per_edge = static_cast<std::uint32_t>(sps);
+    p.seed = mix_seed(seed, 0x5a3d);
+    p.edge_dist = edge_d.get(); p.nonedge_dist = non_d.get();
+    c->launches += launch_pe_collect(p, c->stream);
+    // number of usable samples -> weight of the non-edge sum
+    unsigned long long samples = 0;
+    if (sps) {
+      c->launches += launch_pe_sum(non_d.get(), c->m * sps, kDefaultMu, 1.0, false, 0, sums.get(), valid.get(), c->stream);
+      cuda_check(cudaMemcpyAsync(&samples, valid.get(), sizeof samples, cudaMemcpyDeviceToHost, c->stream), "samples D2H");
+      cuda_check(cudaStreamSynchronize(c->stream), "pe_sampled collect");
+    }
+    const double weight = samples ? (pairs - edges) / static_cast<double>(samples) : 0.0;
+    out->nonedge_samples = samples;
+
+    auto total = [&](double mu, double sigma, int which) {  // DlSums::objective / dsigma (metrics.cpp:35-50)
+      double host[2] = {0.0, 0.0};
+      cuda_check(cudaMemsetAsync(sums.get(), 0, 2 * sizeof(double), c->stream), "pe sums");
+      c->launches += launch_pe_sum(edge_d.get(), c->m, mu, sigma, true, which, sums.get(), nullptr, c->stream);
+      if (samples) c->launches += launch_pe_sum(non_d.get(), c->m * sps, mu, sigma, false, which, sums.get() + 1, nullptr, c->stream);
+      cuda_check(cudaMemcpyAsync(host, sums.get(), sizeof host, cudaMemcpyDeviceToHost, c->stream), "pe sums D2H");
+      cuda_check(cudaStreamSynchronize(c->stream), "pe sums");
+      return host[0] + weight * host[1];
+    };
+    auto best_sigma = [&](double mu) {  // metrics.cpp:53-74
+      double lo = 1e-3, hi = 16.0;
+      double f_lo = total(mu, lo, 1);
+      const double f_hi = total(mu, hi, 1);
+      if (f_lo == 0.0) return lo;
+      if (f_hi == 0.0) return hi;
+      if ((f_lo > 0.0) == (f_hi > 0.0)) return total(mu, lo, 0) <= total(mu, hi, 0) ? lo : hi;
+      for (int step = 0; step < 60 && hi - lo > 1e-4; ++step) {
+        const double mid = 0.5 * (lo + hi);
+        const double f_mid = total(mu, mid, 1);
+        if (f_mid == 0.0) return mid;
+        if ((f_mid > 0.0) == (f_lo > 0.0)) {
+          lo = mid;
+          f_lo = f_mid;
+        } else {
+          hi = mid;
+        }
+      }
+      return 0.5 * (lo + hi);
+    };
+    // minimize_pe (metrics.cpp:76-127)
+    double best_mu = kDefaultMu, best_sig = 1.0, best_cost = std::numeric_limits<double>::infinity();
+    auto cost_at = [&](double mu, double* sigma_out) {
+      const double sg = best_sigma(mu);
+      if (sigma_out) *sigma_out = sg;
+      return total(mu, sg, 0);
+    };
+    auto consider = [&](double mu) {
+      double sg = 1.0;
+      const double cost = cost_at(mu, &sg);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_mu = mu;
+        best_sig = sg;
+      }
+    };
+    for (int k = 0; k <= 20; ++k) consider(0.5 + 0.125 * k);
+    out->grid_pe = best_cost / pairs;
+    double lo = std::max(0.5, best_mu - 0.125), hi = std::min(3.0, best_mu + 0.125);
+    const double gr = 0.5 * (std::sqrt(5.0) - 1.0);
+    double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
+    double f1 = cost_at(x1, nullptr), f2 = cost_at(x2, nullptr);
+    for (int it = 0; it < 24; ++it) {
+      if (f1 <= f2) {
+        hi = x2; x2 = x1; f2 = f1;
+        x1 = hi - gr * (hi - lo);
+        f1 = cost_at(x1, nullptr);
+      } else {
+        lo = x1; x1 = x2; f1 = f2;
+        x2 = lo + gr * (hi - lo);
+        f2 = cost_at(x2, nullptr);
+      }
+    }
+    consider(0.5 * (lo + hi));
+    out->pe = best_cost / pairs;
+    out->mu_star = best_mu;
+    out->sigma_star = best_sig;
+    if (out->h_basic > 1e-12) out->compression_ratio = out->pe / out->h_basic;
+    else out->compression_ratio = out->pe <= 1e-9 ? 1.0 : std::numeric_limits<double>::infinity();
+  });
+}
+
 // ---- CUDA-graph replay of a run of rounds (fixed mu, sigma; iteration indices first_iter .. first_iter + count - 1) ----
 int gempe_graph_capture(gempe_ctx* c, double mu, double sigma, std::uint64_t first_iter, int count) {
   return guarded(c, [&] {

@@ -2038,6 +2038,103 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 
 }  // namespace sigma
 
+// ---------------------------------------------------------------------------------- quality scoring: pe_sampled
+//
+// metrics.cpp:166-213 on the device: the edge distances exactly, the non-edge sum estimated from sampled partners
+// reweighted by (N - m) / #samples; the (mu, sigma) minimisation of metrics.cpp:73-127 is driven from the host over the
+// two distance arrays.  The sample stream is counter-based (not the reference's sequential SplitMix), and the edge test
+// is the run's hash set (false positives reject a distance-independent few per cent of the non-edges), so the
+// estimate agrees with the reference statistically, not draw for draw.
+
+// distance() of metrics.cpp:16-25: double differences, double accumulation, rounded to float like the reference's arrays
+__device__ __forceinline__ float pe_distance(const float* __restrict__ x, std::uint32_t ld, std::uint32_t dim,
+                                             std::uint32_t i, std::uint32_t j) {
+  const float* a = x + static_cast<std::size_t>(i) * ld;
+  const float* b = x + static_cast<std::size_t>(j) * ld;
+  double acc = 0.0;
+  for (std::uint32_t k = 0; k < dim; ++k) {
+    const double diff = static_cast<double>(__ldg(a + k)) - static_cast<double>(__ldg(b + k));
+    acc = fma(diff, diff, acc);
+  }
+  return static_cast<float>(sqrt(acc));
+}
+
+__global__ void __launch_bounds__(kThreads) pe_collect_kernel(const PeCollectArgs p) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  const std::uint64_t per_edge = 1 + static_cast<std::uint64_t>(p.samples_per_edge);
+  const float nan = __int_as_float(0x7fc00000);
+  for (std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < p.m * per_edge; t += stride) {
+    const std::uint64_t e = t / per_edge;
+    const std::uint32_t s = static_cast<std::uint32_t>(t % per_edge);
+    const std::uint32_t u = __ldg(p.src + e), v = __ldg(p.dst + e);
+    if (s == 0) {
+      p.edge_dist[e] = pe_distance(p.x, p.ld, p.dim, u, v);
+      continue;
+    }
+    const std::uint32_t k = s - 1;
+    std::uint32_t anchor = (k % 2 == 0) ? u : v, other = (k % 2 == 0) ? v : u;
+    const std::uint64_t slot = e * p.samples_per_edge + k;
+    auto degree = [&](std::uint32_t w) { return __ldg(p.rowptr + w + 1) - __ldg(p.rowptr + w); };
+    if (degree(anchor) >= p.n - 1) {  // saturated anchors cannot have a non-edge partner (metrics.cpp:188-190)
+      const std::uint32_t tmp = anchor;
+      anchor = other;
+      other = tmp;
+    }
+    float d = nan;
+    if (degree(anchor) < p.n - 1) {
+      const std::uint64_t key = mix(p.seed, slot);
+      for (std::uint32_t tries = 0; tries < 100000u; ++tries) {
+        const std::uint64_t r = mix(key, tries);
+        const std::uint32_t g = static_cast<std::uint32_t>(((r >> 32) * p.n) >> 32);
+        if (g == anchor) continue;
+        if (hash_test(p.hash_words, p.hash_summary, p.hash_mask, p.n, anchor, g)) continue;
+        d = pe_distance(p.x, p.ld, p.dim, anchor, g);
+        break;
+      }
+    }
+    p.nonedge_dist[slot] = d;  // NaN = skipped
+  }
+}
+
+// sum over a distance array of description_length (which = 0) or dl_sigma_derivative (which = 1); NaN entries are
+// skipped and counted out
+__global__ void __launch_bounds__(kThreads) pe_sum_kernel(const float* __restrict__ dist, std::uint64_t count, double mu,
+                                                          double sg, int is_edge, int which, double* __restrict__ total,
+                                                          unsigned long long* __restrict__ valid) {
+  using namespace sigma;
+  __shared__ double warp_sum[kThreads / 32];
+  __shared__ unsigned long long warp_cnt[kThreads / 32];
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  double acc = 0.0;
+  unsigned long long cnt = 0;
+  for (std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += stride) {
+    const float d = dist[t];
+    if (d != d) continue;
+    ++cnt;
+    acc += which == 0 ? cost_floor(static_cast<double>(d), mu, sg, is_edge != 0)
+                      : cost_dsigma(static_cast<double>(d), mu, sg, is_edge != 0);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    acc += __shfl_xor_sync(kFull, acc, off);
+    cnt += __shfl_xor_sync(kFull, cnt, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    warp_sum[threadIdx.x >> 5] = acc;
+    warp_cnt[threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    unsigned long long c = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      t += warp_sum[w];
+      c += warp_cnt[w];
+    }
+    atomicAdd(total, t);
+    if (valid) atomicAdd(valid, c);
+  }
+}
+
 __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long long* __restrict__ hist, double mu,
                                                              double pairs, double edges, int exact_math,
                                                              SigmaState* __restrict__ state) {
@@ -2654,6 +2751,22 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 256) gather_batched_go<32, 2, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 4, 1, 128, 4>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);  // own row + accumulator already take 64 registers
+  return 1;
+}
+
+int launch_pe_collect(const PeCollectArgs& p, cudaStream_t stream) {
+  if (p.m == 0) return 0;
+  const std::uint64_t work = p.m * (1 + static_cast<std::uint64_t>(p.samples_per_edge));
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(work, kThreads), 148u * 64u));
+  pe_collect_kernel<<<blocks, kThreads, 0, stream>>>(p);
+  return 1;
+}
+
+int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigma, bool is_edge, int which, double* total,
+                  unsigned long long* valid, cudaStream_t stream) {
+  if (count == 0) return 0;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(count, kThreads * 4), 148u * 8u));
+  pe_sum_kernel<<<blocks, kThreads, 0, stream>>>(dist, count, mu, sigma, is_edge ? 1 : 0, which, total, valid);
   return 1;
 }
 

@@ -191,6 +191,25 @@ int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t*
 int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, int variant, bool precise,
                   cudaStream_t stream);
 // optimize_sigma + growth cap + PE estimate on the device tallies; updates *state (and state->math)
+// pe_sampled (metrics.cpp:166-213): distances of all edges and of samples_per_edge sampled non-edges per edge
+struct PeCollectArgs {
+  const float* x;
+  std::uint32_t n, dim, ld;
+  std::uint64_t m;
+  const std::uint32_t* src;  // work edge list
+  const std::uint32_t* dst;
+  const std::uint32_t* rowptr;
+  const std::uint32_t* hash_words;
+  const std::uint32_t* hash_summary;
+  std::uint32_t hash_mask;
+  std::uint32_t samples_per_edge;
+  std::uint64_t seed;
+  float* edge_dist;     // [m]
+  float* nonedge_dist;  // [m * samples_per_edge], NaN where no sample could be drawn
+};
+int launch_pe_collect(const PeCollectArgs& p, cudaStream_t stream);
+int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigma, bool is_edge, int which, double* total,
+                  unsigned long long* valid, cudaStream_t stream);
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
                         SigmaState* state, cudaStream_t stream);
 int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,

@@ -255,6 +255,13 @@ class Context:
                                                _capi.ptr(hn)))
         return s.value, pe.value, nw.value, he, hn
 
+    def pe_sampled(self, samples_per_edge: int = 2, seed: int = 1) -> dict:
+        """metrics.cpp pe_sampled of the current coordinates, on the device: dict(pe, mu_star, sigma_star, h_basic,
+        compression_ratio, grid_pe, nonedge_samples)."""
+        rep = _capi.PeReportC()
+        self._check(self._L.gempe_pe_sampled(self._h, samples_per_edge, seed, C.byref(rep)))
+        return {name: getattr(rep, name) for name, _ in rep._fields_}
+
     def graph_capture(self, mu: float, sigma: float, first_iter: int, count: int):
         """Captures `count` rounds into a CUDA graph (replayed by graph_launch)."""
         self._check(self._L.gempe_graph_capture(self._h, mu, sigma, first_iter, count))

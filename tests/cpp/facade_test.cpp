@@ -99,6 +99,8 @@ int main() {
     for (int it = 0; it < 20; ++it) engine.run_single_iteration();
     CHECK(engine.iteration() == 20 && engine.pe_trace().size() == 20);
     CHECK(std::isfinite(engine.sigma()));
+    const auto report = engine.pe_sampled(4, 1);  // metrics.hpp pe_sampled of the current layout, on the device
+    CHECK(report.pe > 0.0 && report.pe <= report.grid_pe && report.h_basic > 0.0);
   }
   {  // degenerate inputs return the initial layout
     Graph g;

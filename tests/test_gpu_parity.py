@@ -662,6 +662,50 @@ def test_zero_negatives_per_vertex_and_large_k(G, oracle, golden_fastmath):
     check_round(G, oracle, golden_fastmath, (n, src, dst), 8, seed=2, neg_mode=1, k=70, iters=1)  # buckets > 32 entries
 
 
+def test_pe_sampled_on_the_device_tracks_the_reference_pe_exact(G, ref):
+    """gempe_pe_sampled (metrics.cpp:166-213 on the device, counter-based samples) against the unmodified reference's
+    pe_exact on the same embedding: with about as many samples as there are non-edges the two agree to sampling noise;
+    a complete graph (no non-edges, nothing sampled) must agree to rounding."""
+    n, src, dst = er_graph(1500, 6000, 31)
+    eng = G.EmbeddingEngine(G.Graph(n, src, dst), 2, G.IterationConfig(max_iters=40), 7)
+    for _ in range(25):
+        eng.run_single_iteration()
+    ctx = eng.context()
+    ws, wd, _ = ctx.work_graph()
+    x = ctx.get_coords()
+    exact = ref.pe_exact(n, ws, wd, x)
+    # the estimator draws its anchors per edge endpoint, i.e. degree-weighted: it is close to pe_exact (the reference's
+    # own bar is 0.05 absolute, test_metrics.cpp:111) but converges to its own limit -- the tight comparison is
+    # against the reference's pe_sampled with as many samples
+    want = ref.pe_sampled(n, ws, wd, x, 200, 5)
+    got = ctx.pe_sampled(samples_per_edge=200, seed=3)
+    assert got["nonedge_samples"] == 200 * len(ws)
+    assert abs(got["pe"] - exact) <= 0.05
+    assert abs(got["pe"] - want) <= 1e-2 * want, (got, want, exact)
+    assert got["grid_pe"] >= got["pe"] and 0.5 <= got["mu_star"] <= 3.0 and 1e-3 <= got["sigma_star"] <= 16.0
+    pairs = n * (n - 1) / 2
+    p = len(ws) / pairs
+    assert abs(got["h_basic"] - (-p * np.log2(p) - (1 - p) * np.log2(1 - p))) < 1e-12
+    assert abs(got["compression_ratio"] - got["pe"] / got["h_basic"]) < 1e-12
+    again = ctx.pe_sampled(samples_per_edge=200, seed=3)
+    assert abs(again["pe"] - got["pe"]) <= 1e-9 * got["pe"]  # same streams; only the summation order differs
+    other = ctx.pe_sampled(samples_per_edge=50, seed=11)
+    assert abs(other["pe"] - want) <= 2e-2 * want
+    with pytest.raises(G.ConfigError):
+        ctx.pe_sampled(samples_per_edge=0)
+    eng.close()
+    # complete graph: edges only
+    m = 30
+    a, b = np.triu_indices(m, 1)
+    kn = G.Context(G.Graph(m, a.astype(np.uint32), b.astype(np.uint32)), 3, 5)
+    kn.init_coords(G.INIT_NORMAL, 2, 1.0)
+    ws, wd, _ = kn.work_graph()
+    want = ref.pe_exact(m, ws, wd, kn.get_coords())
+    got = kn.pe_sampled(4, 1)
+    assert got["nonedge_samples"] == 0 and abs(got["pe"] - want) <= 1e-6 * max(want, 1e-12)
+    kn.close()
+
+
 @pytest.mark.parametrize("dim,mode,k,count", [(2, 1, 5, 6), (2, 0, 0, 5), (64, 1, 4, 3), (128, 1, 6, 4)])
 def test_cuda_graph_replay_equals_the_same_rounds_launched_one_by_one(G, dim, mode, k, count):
     """gempe_graph_capture / gempe_graph_launch: `count` rounds in one CUDA graph give bit-identical coordinates and
