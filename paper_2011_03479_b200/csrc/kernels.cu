@@ -2748,7 +2748,9 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
   else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);  // 16 rows/warp, 20 warps/SM (96 regs)
   // wider rows: 64 row registers per lane as well (8 / 4 rows per batch), 16 warps/SM (d = 256: -19 %, d = 512: -10 %
   // against 4 / 2 rows in 256-thread blocks)
+  else if (ld <= 192) gather_batched_go<16, 3, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream);  // 2 half-warps x 8 rows
   else if (ld <= 256) gather_batched_go<32, 2, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream);
+  else if (ld <= 384) gather_batched_go<32, 3, 4, 4, 1, 128, 4>(a, lo, hi, precise, stream);
   else if (ld <= 512) gather_batched_go<32, 4, 4, 4, 1, 128, 4>(a, lo, hi, precise, stream);
   else gather_batched_go<32, 8, 4, 1, 1>(a, lo, hi, precise, stream);  // own row + accumulator already take 64 registers
   return 1;
