@@ -208,16 +208,18 @@ void build_structures(gempe_ctx* c) {
                        [&](const uint4& a, const uint4& b) { return adjacency_len(a) > adjacency_len(b); });
     }
   }
-  // slices for the host-buffer pipeline: ~equal item counts, cut at vertex boundaries (a hub's slices stay together)
+  // slices for the host-buffer pipeline, cut at vertex boundaries (a hub's slices stay together)
   c->step_item_off.assign(1, 0);
   c->step_vertex_off.assign(1, 0);
   if (world == 1 && !items.empty() && sorted_items) {  // vertex order is gone: one slice
     c->step_item_off.push_back(static_cast<std::uint32_t>(items.size()));
     c->step_vertex_off.push_back(n);
   } else if (world == 1 && !items.empty()) {
-    constexpr std::uint32_t kSlices = 8;
+    // geometric slices (1/64, 1/32, ..., 1/2 of the items): the copy out is the slower side, so only the time to the
+    // FIRST finished slice is exposed -- keep that one short
+    constexpr std::uint32_t kSlices = 7;
     for (std::uint32_t k = 1; k < kSlices; ++k) {
-      std::uint64_t at = static_cast<std::uint64_t>(items.size()) * k / kSlices;
+      std::uint64_t at = static_cast<std::uint64_t>(items.size()) >> (kSlices - k);
       while (at < items.size() && items[at].w != 0) ++at;  // first item of a vertex
       if (at >= items.size() || at <= c->step_item_off.back()) continue;
       c->step_item_off.push_back(static_cast<std::uint32_t>(at));
