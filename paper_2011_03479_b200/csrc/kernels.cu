@@ -787,7 +787,11 @@ __device__ __forceinline__ void pair_terms_f(float delta, bool is_edge, const Ro
 template <int VEC>
 __device__ __forceinline__ void load_row(const float* __restrict__ p, float (&v)[VEC]) {
   if constexpr (VEC == 4) {
+#ifdef GEMPE_ROW_LOADS_CG
+    const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+#else
     const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+#endif
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else if constexpr (VEC == 2) {
     const float2 t = __ldg(reinterpret_cast<const float2*>(p));
