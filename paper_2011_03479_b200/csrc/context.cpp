@@ -626,7 +626,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
     // hub split: d <= 4 runs one thread per item (32 adjacency positions bound its serial latency chain), wider rows one warp per item
     const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 32u :  // c2 sweep: 16 -> 76 us, 32 -> 60, 64 -> 80, 128 -> 117
-                                                                                      std::max(256u, 4096u / lanes_per_row(c->ld));  // c4 sweep: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41
+                                                                                      std::max(c->opt.world == 1 ? 256u : 128u, 4096u / lanes_per_row(c->ld));
+    // c4 sweep on one GPU: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41; a rank of 8 launches 1/8 .. 1/32 of
+    // the items at a time and wants the finer split (0.74 ms per rank at 128, 0.88 at 256)
     c->chunk_entries = opt->chunk_entries ? opt->chunk_entries : default_chunk;
     cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;

@@ -301,23 +301,54 @@ __global__ void publish_counts_kernel(const ExchangeArgs x) {
 
 // received records -> per-partner counts and arrival ranks.  blockIdx.y = source region: the regions are walked one
 // after another, so with contiguous vertex ranges the counters touched at any time are one range's (L2-resident).
+// kRecIlp records per thread: both kernels are chains of dependent memory operations (record -> counter / offset ->
+// store) at a few per cent issue utilisation, so independent chains per thread are what fills the memory system
+constexpr int kRecIlp = 4;
 __global__ void __launch_bounds__(kThreads) count_records_kernel(const ExchangeArgs x, std::uint32_t* __restrict__ in_cnt,
                                                                  std::uint32_t* __restrict__ rec_rank) {
-  const std::uint32_t from = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= min(x.recv_count[from], x.capacity)) return;
-  const std::size_t idx = static_cast<std::size_t>(from) * x.capacity + j;
-  rec_rank[idx] = atomicAdd(in_cnt + x.recv[idx].x, 1u);
+  const std::uint32_t from = blockIdx.y, count = min(x.recv_count[from], x.capacity);
+  const std::uint32_t j0 = blockIdx.x * (kThreads * kRecIlp) + threadIdx.x;
+  const std::size_t base = static_cast<std::size_t>(from) * x.capacity;
+  std::uint32_t partner[kRecIlp], rank[kRecIlp];
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) {
+    const std::uint32_t j = j0 + q * kThreads;
+    partner[q] = j < count ? x.recv[base + j].x : 0xffffffffu;
+  }
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) rank[q] = partner[q] != 0xffffffffu ? atomicAdd(in_cnt + partner[q], 1u) : 0u;
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) {
+    const std::uint32_t j = j0 + q * kThreads;
+    if (j < count) rec_rank[base + j] = rank[q];
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) scatter_records_kernel(const ExchangeArgs x,
                                                                    const std::uint32_t* __restrict__ rec_rank,
                                                                    const std::uint32_t* __restrict__ in_off,
                                                                    std::uint32_t* __restrict__ in_anchor) {
-  const std::uint32_t from = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= min(x.recv_count[from], x.capacity)) return;
-  const std::size_t idx = static_cast<std::size_t>(from) * x.capacity + j;
-  const uint2 rec = x.recv[idx];
-  in_anchor[in_off[rec.x] + rec_rank[idx]] = rec.y;
+  const std::uint32_t from = blockIdx.y, count = min(x.recv_count[from], x.capacity);
+  const std::uint32_t j0 = blockIdx.x * (kThreads * kRecIlp) + threadIdx.x;
+  const std::size_t base = static_cast<std::size_t>(from) * x.capacity;
+  uint2 rec[kRecIlp];
+  std::uint32_t rank[kRecIlp], off[kRecIlp];
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) {
+    const std::uint32_t j = j0 + q * kThreads;
+    rec[q] = make_uint2(0xffffffffu, 0u);
+    rank[q] = 0;
+    if (j < count) {
+      rec[q] = x.recv[base + j];
+      rank[q] = rec_rank[base + j];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) off[q] = rec[q].x != 0xffffffffu ? in_off[rec[q].x] : 0u;
+#pragma unroll
+  for (int q = 0; q < kRecIlp; ++q) {
+    if (rec[q].x != 0xffffffffu) in_anchor[off[q] + rank[q]] = rec[q].y;
+  }
 }
 
 // the spill area (see ExchangeArgs): same two steps, grid-stride, normally zero records
@@ -2531,7 +2562,7 @@ int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uin
                           cudaStream_t stream) {
   cudaMemsetAsync(in_cnt, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
   int launches = 0;
-  const dim3 grid(blocks_for(x.capacity, kThreads), sources);
+  const dim3 grid(blocks_for(x.capacity, kThreads * kRecIlp), sources);
   std::uint32_t* spill_rank = rec_rank + static_cast<std::size_t>(sources) * x.capacity;
   if (x.capacity) {
     count_records_kernel<<<grid, kThreads, 0, stream>>>(x, in_cnt, rec_rank);

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--chunks", type=int, default=4)
     ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--chunk-entries", type=int, default=0)
     ap.add_argument("--peers", action="store_true",
                     help="also time the fused update + broadcast with world-1 stand-in peer buffers in LOCAL memory "
                          "(instruction and store-issue overhead only; NVLink is not involved on one GPU)")
@@ -46,7 +47,7 @@ def main():
         for exchange, peers in ([(0, 0)] if world == 1 else [(0, 0), (1, 0)] + ([(1, 1)] if args.peers else [])):
             chunks = 1 if (world == 1 or peers) else args.chunks
             ctx = G.Context(g, dim, 1, neg_mode=mode, negatives=k, rank=0, world=world, comm_chunks=chunks,
-                            exchange=exchange)
+                            exchange=exchange, chunk_entries=args.chunk_entries)
             ctx.set_stream(stream.cuda_stream)
             ctx.init_coords(G.INIT_NORMAL, 1, 0.01)
             dummies = []
