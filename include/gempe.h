@@ -176,6 +176,10 @@ void* gempe_device_tallies(gempe_ctx* ctx);
  * round, in double.  Capture must be switched on before the round. */
 int gempe_set_capture(gempe_ctx* ctx, int on);
 int gempe_get_yz(gempe_ctx* ctx, double* y, double* z);
+/* The same for `count` selected work rows (y: count*dim, z: count), and the coordinates of selected rows
+ * (x: count*dim): at BASELINE config 5 the full arrays are 17 GB / 8.6 GB, a parity check needs thousands of rows. */
+int gempe_get_yz_rows(gempe_ctx* ctx, const uint32_t* rows, uint64_t count, double* y, double* z);
+int gempe_get_coords_rows(gempe_ctx* ctx, const uint32_t* rows, uint64_t count, float* x);
 
 /* Bit-exact test hooks.
  * gempe_probe  == EdgeHashSet::maybe_edge (include/entropy_embed/hash_set.hpp:28-30) on WORK ids.

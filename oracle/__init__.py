@@ -120,6 +120,11 @@ class Oracle:
                                  C.POINTER(GoFastMath), C.c_void_p, C.c_uint32, C.c_void_p,
                                  f64p, f64p, u64p, u64p, f32p, u32p, C.POINTER(C.c_uint64)]
 
+        L.go_pairs_accumulate.restype = None
+        L.go_pairs_accumulate.argtypes = [C.c_uint32, C.c_void_p, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                          C.c_uint64, u32p, u32p, C.c_int, C.c_double, C.c_double,
+                                          C.POINTER(GoFastMath), f64p, f64p, C.c_void_p]
+
     # -- thin conveniences -------------------------------------------------------------------
     def hash_build(self, n, src, dst, bits_override=0):
         src = np.ascontiguousarray(src, np.uint32)
@@ -151,6 +156,23 @@ class Oracle:
                                        np.ascontiguousarray(hn, np.uint64), nonedge_weight, mu,
                                        C.byref(steps))
         return s, steps.value
+
+    def subset_yz(self, n, x, subset, edge_pairs, sample_pairs, mu, sigma, fm):
+        """(y, z) of the vertices in `subset` from explicit pair lists (go_pairs_accumulate): edge_pairs /
+        sample_pairs = (a, b) uint32 arrays holding every pair that touches a subset vertex exactly once."""
+        x = np.ascontiguousarray(x, np.float32)
+        dim = x.shape[1]
+        subset = np.asarray(subset, np.int64)
+        index = np.full(n, -1, np.int32)
+        index[subset] = np.arange(subset.size, dtype=np.int32)
+        y = np.zeros((subset.size, dim), np.float64)
+        z = np.zeros(subset.size, np.float64)
+        for (a, b), is_edge in ((edge_pairs, 1), (sample_pairs, 0)):
+            a = np.ascontiguousarray(a, np.uint32)
+            b = np.ascontiguousarray(b, np.uint32)
+            self.lib.go_pairs_accumulate(dim, x.ctypes.data_as(C.c_void_p), index, a.size, a, b, is_edge, mu, sigma,
+                                         C.byref(fm) if fm is not None else None, y, z, None)
+        return y, z
 
     def iterate(self, n, src, dst, x, neg_mode, k, seed, it, mu, sigma, fm, table,
                 forced_partners=None):

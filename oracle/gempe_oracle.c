@@ -384,3 +384,32 @@ int go_iterate(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
   }
   return bad ? 3 : 0;
 }
+
+/* add_pair for a vertex subset: same terms as add_pair_f64, rows of the subset only. */
+void go_pairs_accumulate(uint32_t dim, const float* x, const int32_t* sub_index, uint64_t count,
+                         const uint32_t* a, const uint32_t* b, int is_edge, double mu, double sigma,
+                         const go_fastmath* fm, double* y_sub, double* z_sub, uint64_t* hist) {
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint32_t u = a[i], v = b[i];
+    const float* xu = x + (size_t)u * dim;
+    const float* xv = x + (size_t)v * dim;
+    const double delta = pair_distance(xu, xv, dim);
+    if (hist) hist[go_hist_bin(delta)]++;
+    double d_target, w;
+    go_parabola(delta, mu, sigma, is_edge, fm, &d_target, &w);
+    if (!(w > 0.0)) continue;
+    const double target = d_target > 0.0 ? d_target : 0.0;
+    const double s = delta > 0.0 ? target / delta : 0.0;
+    const int32_t ru = sub_index[u], rv = sub_index[v];
+    double* yu = ru >= 0 ? y_sub + (size_t)ru * dim : 0;
+    double* yv = rv >= 0 ? y_sub + (size_t)rv * dim : 0;
+    for (uint32_t c = 0; c < dim; ++c) {
+      const double p = xu[c], q = xv[c];
+      const double diff = p - q;
+      if (yu) yu[c] += w * (q + s * diff);
+      if (yv) yv[c] += w * (p - s * diff);
+    }
+    if (ru >= 0) z_sub[ru] += w;
+    if (rv >= 0) z_sub[rv] += w;
+  }
+}

@@ -88,6 +88,16 @@ int go_iterate(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                const uint32_t* forced_partners, double* y, double* z, uint64_t* hist_edge,
                uint64_t* hist_nonedge, float* x_next, uint32_t* partners, uint64_t* total_draws);
 
+/* ---- the same pair arithmetic on an explicit pair list, accumulated for a vertex SUBSET -----
+ * For sizes where a whole round is minutes of CPU work (BASELINE config 5): every pair (a[i], b[i])
+ * goes through pair_distance + parabola + add_pair exactly as in go_iterate, but only endpoints with
+ * sub_index[v] >= 0 receive their sums, in row sub_index[v] of y_sub (rows x dim) / z_sub.  The caller
+ * lists every pair that touches a subset vertex once (edges incident to it; samples it anchors or
+ * receives).  hist (GO_BINS, may be NULL) tallies the listed pairs. */
+void go_pairs_accumulate(uint32_t dim, const float* x, const int32_t* sub_index, uint64_t count,
+                         const uint32_t* a, const uint32_t* b, int is_edge, double mu, double sigma,
+                         const go_fastmath* fm, double* y_sub, double* z_sub, uint64_t* hist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ SYMBOLS = [
     "gempe_hash_bits", "gempe_sample_slots", "gempe_pair_terms", "gempe_algorithmic_bytes",
     "gempe_get_work_graph", "gempe_set_coords", "gempe_get_coords", "gempe_init_coords", "gempe_relabel",
     "gempe_iterate", "gempe_step_host", "gempe_iterate_async", "gempe_graph_capture", "gempe_graph_launch", "gempe_pe_sampled", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
-    "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_probe",
+    "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_get_yz_rows", "gempe_get_coords_rows", "gempe_probe",
     "gempe_sample", "gempe_set_stream", "gempe_device_coords", "gempe_row_stride", "gempe_padded_rows",
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_exchange_layout", "gempe_bucket_received", "gempe_gather_chunk", "gempe_coords_ipc_handles", "gempe_open_peer",
     "gempe_add_peer_pointers", "gempe_clear_peers", "gempe_exchange_ipc_handle", "gempe_open_peer_exchange",
@@ -122,6 +122,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_device_tallies": (vp, [vp]),
         "gempe_set_capture": (i32, [vp, i32]),
         "gempe_get_yz": (i32, [vp, vp, vp]),
+        "gempe_get_yz_rows": (i32, [vp, vp, u64, vp, vp]),
+        "gempe_get_coords_rows": (i32, [vp, vp, u64, vp]),
         "gempe_probe": (i32, [vp, vp, vp, u64, vp]),
         "gempe_sample": (i32, [vp, u64, vp, C.POINTER(u64)]),
         "gempe_set_stream": (i32, [vp, vp]),

@@ -40,18 +40,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
+    headers = [h if os.path.isabs(h) else os.path.join(CSRC, h) for h in HEADERS] + [os.path.abspath(__file__)]
+    flags_tag = os.path.join(OUT_DIR, ".flags")
+    flags_now = " ".join(NVCC_FLAGS + CXX_FLAGS)
+    flags_same = os.path.exists(flags_tag) and open(flags_tag).read() == flags_now
+
+    def fresh(obj, source):  # the object is newer than its source and every header, and the flags did not change
+        return (not force and flags_same and os.path.exists(obj) and
+                all(os.path.getmtime(obj) > os.path.getmtime(d) for d in [source] + headers))
+
     objs = []
     for s in CU_SOURCES:
         o = os.path.join(OUT_DIR, s + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+        if not fresh(o, os.path.join(CSRC, s)):
+            cmd = [NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            subprocess.check_call(cmd)
         objs.append(o)
     for s in CXX_SOURCES:
         o = os.path.join(OUT_DIR, s + ".o")
-        subprocess.check_call(["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, s), "-o", o])
+        if not fresh(o, os.path.join(CSRC, s)):
+            subprocess.check_call(["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, s), "-o", o])
         objs.append(o)
+    with open(flags_tag, "w") as f:
+        f.write(flags_now)
     subprocess.check_call([NVCC, "-shared", "-o", LIB, *objs, "-cudart", "static",
                            "-Xlinker", "--exclude-libs=ALL"])
     return LIB

@@ -768,6 +768,33 @@ int gempe_get_yz(gempe_ctx* c, double* y, double* z) {
   });
 }
 
+int gempe_get_yz_rows(gempe_ctx* c, const std::uint32_t* rows, std::uint64_t count, double* y, double* z) {
+  return guarded(c, [&] {
+    if (!c->capture || c->cap_y.size() == 0) throw config_error("capture is off");
+    if (count && !rows) throw config_error("null row list");
+    for (std::uint64_t i = 0; i < count; ++i) {
+      if (rows[i] >= c->n) throw config_error("row out of range");
+      if (y) cuda_check(cudaMemcpyAsync(y + i * c->dim, c->cap_y.get() + static_cast<std::size_t>(rows[i]) * c->dim,
+                                        c->dim * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "y rows D2H");
+      if (z) cuda_check(cudaMemcpyAsync(z + i, c->cap_z.get() + rows[i], sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+                        "z rows D2H");
+    }
+    cuda_check(cudaStreamSynchronize(c->stream), "get_yz_rows");
+  });
+}
+
+int gempe_get_coords_rows(gempe_ctx* c, const std::uint32_t* rows, std::uint64_t count, float* x) {
+  return guarded(c, [&] {
+    if (!x || (count && !rows)) throw config_error("null argument");
+    for (std::uint64_t i = 0; i < count; ++i) {
+      if (rows[i] >= c->n) throw config_error("row out of range");
+      cuda_check(cudaMemcpyAsync(x + i * c->dim, c->x[c->cur].get() + static_cast<std::size_t>(rows[i]) * c->ld,
+                                 c->dim * sizeof(float), cudaMemcpyDeviceToHost, c->stream), "coordinate rows D2H");
+    }
+    cuda_check(cudaStreamSynchronize(c->stream), "get_coords_rows");
+  });
+}
+
 int gempe_begin_round(gempe_ctx* c, double mu, double sigma, std::uint64_t iter_index) {
   return guarded(c, [&] {
     require_live(c);

@@ -297,6 +297,19 @@ class Context:
         self._check(self._L.gempe_get_yz(self._h, _capi.ptr(y), _capi.ptr(z)))
         return y, z
 
+    def get_yz_rows(self, rows):
+        rows = np.ascontiguousarray(rows, np.uint32)
+        y = np.zeros((rows.size, self.dim), np.float64)
+        z = np.zeros(rows.size, np.float64)
+        self._check(self._L.gempe_get_yz_rows(self._h, _capi.ptr(rows), rows.size, _capi.ptr(y), _capi.ptr(z)))
+        return y, z
+
+    def get_coords_rows(self, rows):
+        rows = np.ascontiguousarray(rows, np.uint32)
+        x = np.zeros((rows.size, self.dim), np.float32)
+        self._check(self._L.gempe_get_coords_rows(self._h, _capi.ptr(rows), rows.size, _capi.ptr(x)))
+        return x
+
     # -- bit-exact hooks -----------------------------------------------------------------------------
     def probe(self, i, j) -> np.ndarray:
         i = np.ascontiguousarray(i, np.uint32)
