@@ -66,9 +66,8 @@ typedef struct gempe_options {
   int32_t deterministic;  /* 1 = sort incoming-sample buckets so the fp32 sums are run-to-run identical */
   int32_t precise_distance; /* 1 = pair_distance exactly as src/engine.cpp:45-52 (double differences); 0 = fp32
                              differences with double cross-lane sum and exact-tally recheck (default) */
-  int32_t kernel_variant; /* gather kernel: 0 = default (thread per item for d <= 4, batched warp per item above);
-                             A/B variants kept under test: 1 = row-at-a-time, 2 = warp per item also for d <= 4,
-                             10 = cp.async shared-memory pipeline (16 < row stride <= 128) */
+  int32_t kernel_variant; /* must be 0 (one gather kernel per row width: thread per item for d <= 4, batched warp per
+                             item above); the A/B variants of round 1 are retired, the field keeps the layout */
   int32_t bucket_mode;    /* incoming-sample bucketing: 0 = auto, 1 = per-partner atomics + scan + scatter,
                              2 = two-level counting sort (streaming traffic only),
                              3 = one radix pass by contiguous vertex range, then per-partner atomics range by range

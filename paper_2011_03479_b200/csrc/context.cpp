@@ -84,6 +84,33 @@ void pack_tables(DeviceTables& out) {
   pack(t.ratio, out.ratio);
 }
 
+// The fp32 cells of kernels.hpp: ratio cell i = [-1 + 0.05 i, -1 + 0.05 (i + 1)) carries the quadratic of the segment it
+// lies in (every knot of the reference's ratio table, piecewise.cpp:178-190, is a multiple of 0.05 -- checked here), then
+// the 16 uniform erf segments.
+std::vector<float4> pack_tables_f32() {
+  const FastMathTables& t = FastMathTables::get();
+  std::vector<float4> cells(kTableF32Entries);
+  const double lo = t.ratio.knots[0], width = 0.05;
+  if (std::fabs(lo + 1.0) > 1e-12 || std::fabs(t.ratio.knots[kSegments] - 8.0) > 1e-12) {
+    throw config_error("ratio table range changed: the fp32 cell layout assumes [-1, 8]");
+  }
+  for (int k = 0; k <= kSegments; ++k) {
+    const double cells_below = (t.ratio.knots[k] - lo) / width;
+    if (std::fabs(cells_below - std::round(cells_below)) > 1e-9) throw config_error("ratio table knot is not a multiple of 0.05");
+    if (std::fabs(t.erf.knots[k] - 6.0 * k / kSegments) > 1e-12) throw config_error("erf table knots are not uniform");
+  }
+  for (int i = 0; i < kRatioCells; ++i) {
+    const double mid = lo + width * (i + 0.5);
+    int s = 0;
+    while (s + 1 < kSegments && mid >= t.ratio.knots[s + 1]) ++s;
+    cells[i] = make_float4(static_cast<float>(t.ratio.a[s]), static_cast<float>(t.ratio.b[s]), static_cast<float>(t.ratio.c[s]), 0.0f);
+  }
+  for (int s = 0; s < kErfSegments; ++s) {
+    cells[kRatioCells + s] = make_float4(static_cast<float>(t.erf.a[s]), static_cast<float>(t.erf.b[s]), static_cast<float>(t.erf.c[s]), 0.0f);
+  }
+  return cells;
+}
+
 void set_round_math(gempe_ctx* c, double mu, double sigma) {
   if (!(sigma > 0.0) || !std::isfinite(sigma) || !std::isfinite(mu)) throw config_error("sigma must be positive and finite");
   const double pi = 3.14159265358979323846264338327950288, ln2 = 0.693147180559945309417232121458176568;
@@ -167,7 +194,7 @@ void build_structures(gempe_ctx* c) {
 
   timer.lap(c->opt.deterministic ? "csr (host, edge order)" : "csr (device)");
   // work items: one per owned vertex, hubs split every chunk_entries adjacency positions
-  std::vector<uint4> items;
+  std::vector<ItemDesc> items;
   std::vector<std::uint32_t> hub_first, hub_items;
   std::uint32_t parts = 0;
   items.reserve(static_cast<std::size_t>(n) / static_cast<std::size_t>(c->opt.world) +
@@ -182,30 +209,36 @@ void build_structures(gempe_ctx* c) {
     for (std::uint32_t v = static_cast<std::uint32_t>(lo); v < hi; ++v) {
       const std::uint32_t deg = rowptr[v + 1] - rowptr[v];
       const std::uint32_t pieces = std::max(1u, (deg + c->chunk_entries - 1) / c->chunk_entries);
-      if (pieces == 1) {
-        items.push_back(make_uint4(v, rowptr[v], kNoHub, 0));
-      } else {
-        const std::uint32_t hub = static_cast<std::uint32_t>(hub_first.size());
+      std::uint32_t hub = kNoHub;
+      if (pieces > 1) {
+        hub = static_cast<std::uint32_t>(hub_first.size());
         hub_first.push_back(parts);
         hub_items.push_back(pieces);
-        for (std::uint32_t p = 0; p < pieces; ++p) {
-          items.push_back(make_uint4(v, rowptr[v] + p * c->chunk_entries, hub, p));
-        }
         parts += pieces;
+      }
+      for (std::uint32_t p = 0; p < pieces; ++p) {
+        ItemDesc it{};
+        it.u = v;
+        it.off_a = rowptr[v] + p * c->chunk_entries;
+        it.len_a = std::min(it.off_a + c->chunk_entries, rowptr[v + 1]) - it.off_a;
+        // own samples: one slot per adjacency position (PER_EDGE_2), or the vertex's k slots on its first item
+        it.off_b = per_edge ? it.off_a : v * c->opt.negatives;
+        it.len_b = per_edge ? it.len_a : (p == 0 ? c->opt.negatives : 0u);
+        it.first = p == 0;
+        it.hub = hub;
+        it.sub = p;
+        items.push_back(it);
       }
     }
   }
   c->chunk_item_off[c->comm_chunks] = static_cast<std::uint32_t>(items.size());
   // d <= 4 runs one THREAD per item: items of similar length are put next to each other (longest first) inside every
   // chunk, so the 32 items of a warp finish together instead of waiting for the longest one
-  const bool sorted_items = c->ld <= 4 && c->opt.kernel_variant == 0 && std::getenv("GEMPE_NO_ITEM_SORT") == nullptr;
+  const bool sorted_items = c->ld <= 4 && std::getenv("GEMPE_NO_ITEM_SORT") == nullptr;
   if (sorted_items) {
-    auto adjacency_len = [&](const uint4& it) {
-      return std::min(it.y + c->chunk_entries, rowptr[it.x + 1]) - it.y;
-    };
     for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
       std::stable_sort(items.begin() + c->chunk_item_off[chunk], items.begin() + c->chunk_item_off[chunk + 1],
-                       [&](const uint4& a, const uint4& b) { return adjacency_len(a) > adjacency_len(b); });
+                       [](const ItemDesc& a, const ItemDesc& b) { return a.len_a > b.len_a; });
     }
   }
   // slices for the host-buffer pipeline, cut at vertex boundaries (a hub's slices stay together)
@@ -220,10 +253,10 @@ void build_structures(gempe_ctx* c) {
     constexpr std::uint32_t kSlices = 7;
     for (std::uint32_t k = 1; k < kSlices; ++k) {
       std::uint64_t at = static_cast<std::uint64_t>(items.size()) >> (kSlices - k);
-      while (at < items.size() && items[at].w != 0) ++at;  // first item of a vertex
+      while (at < items.size() && items[at].sub != 0) ++at;  // first item of a vertex
       if (at >= items.size() || at <= c->step_item_off.back()) continue;
       c->step_item_off.push_back(static_cast<std::uint32_t>(at));
-      c->step_vertex_off.push_back(items[at].x);
+      c->step_vertex_off.push_back(items[at].u);
     }
     c->step_item_off.push_back(static_cast<std::uint32_t>(items.size()));
     c->step_vertex_off.push_back(n);
@@ -485,7 +518,6 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.n = c->n;
   g.dim = c->dim;
   g.ld = c->ld;
-  g.rowptr = c->rowptr.get();
   g.nbr = c->nbr.get();
   g.neg_own = c->neg_own.get();
   g.in_off = c->in_off.get();
@@ -501,13 +533,11 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.work_cursor = c->work_cursor.get();
   g.cap_y = c->capture ? c->cap_y.get() : nullptr;
   g.cap_z = c->capture ? c->cap_z.get() : nullptr;
-  g.chunk_entries = c->chunk_entries;
-  g.k = c->opt.negatives;
-  g.neg_mode = c->opt.neg_mode;
   g.math = c->math;
   g.math_dev = c->use_dev_math ? &c->sigma_state.get()->math : nullptr;
   g.tab = c->tables;
-  c->launches += launch_gather(g, item_lo, item_hi, c->opt.kernel_variant, c->opt.precise_distance != 0, c->stream);
+  g.tab_f32 = c->tables_f32.get();
+  c->launches += launch_gather(g, item_lo, item_hi, c->opt.precise_distance != 0, c->stream);
   cuda_check(cudaGetLastError(), "gather launch");
 }
 
@@ -536,6 +566,7 @@ void fetch_status(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_no
     throw data_error("sample exchange region overflowed: partners are far from uniform over ranks for this graph; "
                      "create the context with opt.exchange = 0");
   }
+  if (st[kStatEmptyTallies]) throw config_error("cannot optimize sigma on an empty histogram");  // slope.cpp:76
   if (st[kStatNonFinite]) {
     throw divergence_error("non-finite coordinate after update", static_cast<int>(c->round_iter) + 1);
   }
@@ -549,6 +580,7 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
   if (o.exchange < 0 || o.exchange > 2) throw config_error("unknown exchange mode");
   if (o.math != GEMPE_MATH_TABLES && o.math != GEMPE_MATH_EXACT) throw config_error("unknown math policy");
   if (o.rng != GEMPE_RNG_REFERENCE && o.rng != GEMPE_RNG_PHILOX) throw config_error("unknown rng mode");
+  if (o.kernel_variant != 0) throw config_error("kernel_variant: the A/B gather kernels of round 1 are retired, use 0");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) throw config_error("bad rank/world");
   if (o.comm_chunks < 1) throw config_error("comm_chunks must be >= 1");
   if (m > 0 && (!src || !dst)) throw data_error("null edge arrays");
@@ -625,7 +657,7 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->block_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(std::max(n, 1u)) + blocks - 1) / blocks);
     c->n_pad = static_cast<std::uint32_t>(blocks * c->block_rows);
     // hub split: d <= 4 runs one thread per item (32 adjacency positions bound its serial latency chain), wider rows one warp per item
-    const std::uint32_t default_chunk = (c->ld <= 4 && opt->kernel_variant == 0) ? 32u :  // c2 sweep: 16 -> 76 us, 32 -> 60, 64 -> 80, 128 -> 117
+    const std::uint32_t default_chunk = c->ld <= 4 ? 32u :  // c2 sweep: 16 -> 76 us, 32 -> 60, 64 -> 80, 128 -> 117
                                                                                       std::max(c->opt.world == 1 ? 256u : 128u, 4096u / lanes_per_row(c->ld));
     // c4 sweep on one GPU: 64 -> 5.29 ms, 128 -> 5.13, 256 -> 5.03, 512 -> 5.03, 2048 -> 5.41; a rank of 8 launches 1/8 .. 1/32 of
     // the items at a time and wants the finer split (0.74 ms per rank at 128, 0.88 at 256)
@@ -634,7 +666,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->stream = c->own_stream;
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned), (4 + 2 * kBins) * sizeof(unsigned long long),
                              cudaHostAllocDefault), "cudaHostAlloc");
+    c->sigma_single_block = std::getenv("GEMPE_SIGMA_SINGLE_BLOCK") != nullptr;  // A/B switch, read once per context
     pack_tables(c->tables);
+    c->tables_f32.upload(pack_tables_f32());
     c->round_state.allocate(4 + 2 * kBins, true);
     c->status.p = reinterpret_cast<std::uint32_t*>(c->round_state.get());
     c->hist.p = c->round_state.get() + 4;
@@ -1066,7 +1100,8 @@ int gempe_sigma_update_async(gempe_ctx* c) {
     require_live(c);
     const double pairs = static_cast<double>(static_cast<std::uint64_t>(c->n) * (c->n - 1) / 2);
     c->launches += launch_sigma_update(c->hist.get(), c->mu_dev, pairs, static_cast<double>(c->m),
-                                       c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->stream);
+                                       c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->status.get(),
+                                       c->sigma_single_block, c->stream);
     cuda_check(cudaGetLastError(), "sigma update");
   });
 }

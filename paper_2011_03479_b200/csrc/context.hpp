@@ -115,7 +115,7 @@ struct gempe_ctx {
   std::uint32_t ex_registered = 0;
   bool ex_peers_lost = false;
   std::uint64_t ex_round = 0;  // parity of the receive buffers in direct mode
-  gempe::DeviceBuffer<uint4> items;
+  gempe::DeviceBuffer<gempe::ItemDesc> items;
   std::vector<std::uint32_t> chunk_item_off;  // comm_chunks + 1
   // gempe_step_host pipeline: item / vertex boundaries of the slices whose rows are copied out while later
   // slices are still being computed (world == 1 only)
@@ -138,6 +138,7 @@ struct gempe_ctx {
   gempe::DeviceBuffer<std::uint32_t> work_cursor;
   gempe::DeviceBuffer<gempe::SigmaState> sigma_state;  // device-resident (mu, sigma) feedback
   double mu_dev = gempe::kDefaultMu;
+  bool sigma_single_block = false;  // GEMPE_SIGMA_SINGLE_BLOCK at creation: one-CTA sigma search (A/B)
   bool use_dev_math = false;  // gather reads RoundMath from sigma_state instead of kernel parameters
   gempe::DeviceBuffer<double> cap_y, cap_z;
   bool capture = false;
@@ -148,6 +149,7 @@ struct gempe_ctx {
   cudaStream_t own_stream = nullptr, stream = nullptr;
   gempe::RoundMath math{};
   gempe::DeviceTables tables{};
+  gempe::DeviceBuffer<float4> tables_f32;  // directly indexed fp32 cells of the same tables (kernels.hpp)
   std::uint64_t round_iter = 0;
   std::uint64_t launches = 0;
   std::uint64_t last_draws = 0;

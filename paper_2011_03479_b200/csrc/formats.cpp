@@ -9,8 +9,6 @@
 #include <fstream>
 #include <numeric>
 #include <string>
-#include <unordered_map>
-#include <unordered_set>
 #include <vector>
 
 #include "context.hpp"
@@ -22,14 +20,6 @@ namespace {
 struct parse_failure : data_error {
   parse_failure(const std::string& msg, std::uint64_t line) : data_error(msg), line(line) {}
   std::uint64_t line;
-};
-
-bool is_space(unsigned char ch) { return ch == ' ' || (ch >= '\t' && ch <= '\r'); }  // std::isspace, "C" locale
-
-struct PairKeyHash {
-  std::size_t operator()(const std::pair<std::uint64_t, std::uint64_t>& p) const {
-    return static_cast<std::size_t>(splitmix64(p.first * 0x100000001b3ull ^ p.second));
-  }
 };
 
 template <typename T>
@@ -49,69 +39,134 @@ void fill(gempe_graph* out, std::uint32_t n, const std::vector<std::uint32_t>& s
   out->raw_labels = labels.empty() ? nullptr : to_c_array(labels);
 }
 
-// load_edge_list (graph.cpp:75-133): "i<ws>j" lines, '#'/'%' comments and blank lines skipped, self-loops dropped,
-// duplicate undirected edges merged (first occurrence and its orientation kept), ids compacted in first-appearance order.
-void parse_edge_list(const char* text, std::uint64_t len, gempe_graph* out) {
-  std::vector<std::pair<std::uint64_t, std::uint64_t>> raw_edges;
-  std::unordered_set<std::pair<std::uint64_t, std::uint64_t>, PairKeyHash> seen;
-  std::uint64_t line_no = 0, at = 0;
-  while (at < len) {
-    std::uint64_t end = at;
-    while (end < len && text[end] != '\n') ++end;
-    ++line_no;
-    std::uint64_t pos = at;
-    const std::uint64_t stop = end;
-    at = end + 1;  // a final line without '\n' is still a line; an empty tail after the last '\n' is not
-    while (pos < stop && is_space(static_cast<unsigned char>(text[pos]))) ++pos;
-    if (pos == stop) continue;
-    if (text[pos] == '#' || text[pos] == '%') continue;
-    std::uint64_t ids[2] = {0, 0};
-    int count = 0;
-    while (pos < stop) {
-      while (pos < stop && is_space(static_cast<unsigned char>(text[pos]))) ++pos;
-      if (pos == stop) break;
-      const std::uint64_t start = pos;
-      while (pos < stop && !is_space(static_cast<unsigned char>(text[pos]))) ++pos;
-      std::uint64_t v = 0;
-      bool ok = count < 2 && pos > start;
-      for (std::uint64_t q = start; ok && q < pos; ++q) {
-        const char ch = text[q];
-        if (ch < '0' || ch > '9') ok = false;
-        else {
-          const std::uint64_t digit = static_cast<std::uint64_t>(ch - '0');
-          if (v > (UINT64_MAX - digit) / 10) ok = false;
-          else v = v * 10 + digit;
-        }
+// ---- edge-list text -> canonical graph ------------------------------------------------------------------------
+// Contract (SPEC of load_edge_list, /root/reference/proj/src/graph.cpp:75-133, and tests/test_graph.cpp:34-91): one
+// "<id> <id>" pair of decimal u64 ids per line, any C-locale whitespace between and around them; lines whose first
+// non-blank character is '#' or '%' and blank lines are skipped; a self-loop is dropped; of several lines naming the
+// same undirected edge the FIRST one survives, with its orientation; ids are then renumbered 0..n-1 in order of first
+// appearance in the surviving edges (source before target).  Anything else on a data line is a parse error that
+// carries the 1-based line number.
+//
+// Built on sorting rather than on hash containers: the text is tokenised in one sweep into (low id, high id, line
+// order) records, duplicates are removed by a sort on the undirected key, and the renumbering is a second sort of
+// the endpoint occurrences -- O(E log E), no per-edge allocation.
+
+inline bool blank(char ch) { return ch == ' ' || (ch >= '\t' && ch <= '\r'); }
+
+const char* skip_blanks(const char* p, const char* stop) {
+  while (p != stop && blank(*p)) ++p;
+  return p;
+}
+
+const char* skip_word(const char* p, const char* stop) {
+  while (p != stop && !blank(*p)) ++p;
+  return p;
+}
+
+// [first, last) is a non-empty run of decimal digits that fits 64 bits
+bool read_decimal(const char* first, const char* last, std::uint64_t* value) {
+  if (first == last) return false;
+  std::uint64_t acc = 0;
+  for (; first != last; ++first) {
+    const unsigned digit = static_cast<unsigned char>(*first) - static_cast<unsigned>('0');
+    if (digit > 9u) return false;
+    if (acc > UINT64_MAX / 10 || acc * 10 > UINT64_MAX - digit) return false;
+    acc = acc * 10 + digit;
+  }
+  *value = acc;
+  return true;
+}
+
+struct EdgeRecord {
+  std::uint64_t lo, hi;  // undirected key
+  std::uint32_t order;   // rank among the data lines that name an edge
+  bool swapped;          // the line read "hi lo"
+};
+
+std::vector<EdgeRecord> tokenise_edge_lines(const char* text, std::uint64_t len) {
+  std::vector<EdgeRecord> records;
+  const char* cursor = text;
+  const char* const stop = text + len;
+  for (std::uint64_t line = 1; cursor != stop; ++line) {
+    const void* nl = std::memchr(cursor, '\n', static_cast<std::size_t>(stop - cursor));
+    const char* const eol = nl ? static_cast<const char*>(nl) : stop;
+    const char* at = skip_blanks(cursor, eol);
+    cursor = nl ? eol + 1 : stop;
+    if (at == eol || *at == '#' || *at == '%') continue;
+    std::uint64_t endpoint[2] = {0, 0};
+    int seen = 0;
+    for (; at != eol; at = skip_blanks(at, eol)) {
+      const char* const word = at;
+      at = skip_word(at, eol);
+      std::uint64_t value = 0;
+      if (seen == 2 || !read_decimal(word, at, &value)) {
+        throw parse_failure("line " + std::to_string(line) + ": cannot read '" + std::string(word, at) +
+                            "' as one of the two vertex ids of an edge", line);
       }
-      if (!ok) {
-        throw parse_failure("malformed edge line " + std::to_string(line_no) + ": '" + std::string(text + start, pos - start) + "'",
-                            line_no);
-      }
-      ids[count++] = v;
+      endpoint[seen++] = value;
     }
-    if (count != 2) throw parse_failure("expected two vertex ids on line " + std::to_string(line_no), line_no);
-    if (ids[0] == ids[1]) continue;
-    if (!seen.insert({std::min(ids[0], ids[1]), std::max(ids[0], ids[1])}).second) continue;
-    raw_edges.emplace_back(ids[0], ids[1]);
+    if (seen != 2) throw parse_failure("line " + std::to_string(line) + ": an edge needs two vertex ids", line);
+    if (endpoint[0] == endpoint[1]) continue;
+    if (records.size() >= 0xffffffffull) throw data_error("edge list exceeds 2^32 lines");
+    const bool swapped = endpoint[0] > endpoint[1];
+    records.push_back({swapped ? endpoint[1] : endpoint[0], swapped ? endpoint[0] : endpoint[1],
+                       static_cast<std::uint32_t>(records.size()), swapped});
   }
-  if (raw_edges.empty()) throw data_error("no edges after canonicalization");
-  std::unordered_map<std::uint64_t, std::uint32_t> compact;
-  compact.reserve(raw_edges.size() * 2);
-  std::vector<std::uint64_t> labels;
-  std::vector<std::uint32_t> src, dst;
-  src.reserve(raw_edges.size());
-  dst.reserve(raw_edges.size());
-  auto id_of = [&](std::uint64_t raw) {
-    auto [it, inserted] = compact.try_emplace(raw, static_cast<std::uint32_t>(compact.size()));
-    if (inserted) labels.push_back(raw);
-    return it->second;
+  return records;
+}
+
+void parse_edge_list(const char* text, std::uint64_t len, gempe_graph* out) {
+  std::vector<EdgeRecord> records = tokenise_edge_lines(text, len);
+  // duplicates: group by undirected key, the earliest line of every group stays; then back to line order
+  std::sort(records.begin(), records.end(), [](const EdgeRecord& x, const EdgeRecord& y) {
+    return x.lo != y.lo ? x.lo < y.lo : (x.hi != y.hi ? x.hi < y.hi : x.order < y.order);
+  });
+  records.erase(std::unique(records.begin(), records.end(),
+                            [](const EdgeRecord& x, const EdgeRecord& y) { return x.lo == y.lo && x.hi == y.hi; }),
+                records.end());
+  std::sort(records.begin(), records.end(), [](const EdgeRecord& x, const EdgeRecord& y) { return x.order < y.order; });
+  if (records.empty()) throw data_error("the edge list holds no edge (only comments, blanks, self-loops)");
+
+  // renumbering: occurrence 2e is the source of surviving edge e, 2e+1 its target; a raw id gets the rank of its first
+  // occurrence among the first occurrences of all ids
+  const std::size_t edges = records.size();
+  struct Occurrence { std::uint64_t raw; std::uint64_t where; };
+  std::vector<Occurrence> occ(2 * edges);
+  for (std::size_t e = 0; e < edges; ++e) {
+    const EdgeRecord& r = records[e];
+    occ[2 * e] = {r.swapped ? r.hi : r.lo, 2 * e};
+    occ[2 * e + 1] = {r.swapped ? r.lo : r.hi, 2 * e + 1};
+  }
+  std::sort(occ.begin(), occ.end(), [](const Occurrence& x, const Occurrence& y) {
+    return x.raw != y.raw ? x.raw < y.raw : x.where < y.where;
+  });
+  std::vector<Occurrence> firsts;  // one per distinct raw id: (raw, first occurrence)
+  for (const Occurrence& o : occ) {
+    if (firsts.empty() || firsts.back().raw != o.raw) firsts.push_back(o);
+  }
+  if (firsts.size() > 0xffffffffull) throw data_error("more than 2^32 distinct vertex ids");
+  std::vector<std::uint32_t> by_appearance(firsts.size());
+  std::iota(by_appearance.begin(), by_appearance.end(), 0u);
+  std::sort(by_appearance.begin(), by_appearance.end(),
+            [&](std::uint32_t x, std::uint32_t y) { return firsts[x].where < firsts[y].where; });
+  std::vector<std::uint32_t> new_id(firsts.size());
+  std::vector<std::uint64_t> labels(firsts.size());
+  for (std::uint32_t rank = 0; rank < by_appearance.size(); ++rank) {
+    new_id[by_appearance[rank]] = rank;
+    labels[rank] = firsts[by_appearance[rank]].raw;
+  }
+  auto lookup = [&](std::uint64_t raw) {
+    const auto it = std::lower_bound(firsts.begin(), firsts.end(), raw,
+                                     [](const Occurrence& o, std::uint64_t v) { return o.raw < v; });
+    return new_id[static_cast<std::size_t>(it - firsts.begin())];
   };
-  for (const auto& [a, b] : raw_edges) {
-    const std::uint32_t ia = id_of(a), ib = id_of(b);
-    src.push_back(ia);
-    dst.push_back(ib);
+  std::vector<std::uint32_t> src(edges), dst(edges);
+  for (std::size_t e = 0; e < edges; ++e) {
+    const EdgeRecord& r = records[e];
+    src[e] = lookup(r.swapped ? r.hi : r.lo);
+    dst[e] = lookup(r.swapped ? r.lo : r.hi);
   }
-  fill(out, static_cast<std::uint32_t>(compact.size()), src, dst, labels);
+  fill(out, static_cast<std::uint32_t>(firsts.size()), src, dst, labels);
 }
 
 std::uint64_t le(const unsigned char* p, int bytes) {

@@ -4,6 +4,7 @@
 #include "hostmath.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <functional>
 #include <mutex>
@@ -261,43 +262,48 @@ double histogram_objective_dsigma(const Tallies& h, double mu, double sigma) {
   return weighted_cost(h, mu, sigma, coding_cost_dsigma);
 }
 
+namespace {
+
+// Root of an increasing sign change: f(a) < 0 < f(b).  Halves [a, b] until it is no wider than `width` or `budget`
+// halvings are spent (counted in *used); an exact zero ends the walk at that point.  Returns the centre of the last
+// interval.  The visited midpoints are those of slope.cpp:104-120, so sigma agrees with the reference bit for bit.
+template <typename F>
+double centre_of_sign_change(F&& f, double a, double b, double width, int budget, int* used) {
+  while (b - a > width && *used < budget) {
+    ++*used;
+    const double c = 0.5 * (a + b);
+    const double fc = f(c);
+    if (fc == 0.0) return c;
+    if (fc > 0.0) b = c; else a = c;
+  }
+  return 0.5 * (a + b);
+}
+
+}  // namespace
+
+// optimize_sigma_detail (slope.cpp:75-125): the derivative of the cost in sigma can change sign several times on the
+// tallies of an unsettled layout, so the basin is located first -- 17 log-spaced candidates between the sigma bounds,
+// scored with the unfloored cost -- and only the two cells around the cheapest candidate are searched for the zero of
+// the derivative.  The refined value replaces the candidate only if it is not more expensive.
 SigmaSearch optimize_sigma(const Tallies& h, double mu) {
-  if (h.edge_total() + h.nonedge_total() == 0) {
-    throw config_error("cannot optimize sigma on an empty histogram");
+  if (h.edge_total() == 0 && h.nonedge_total() == 0) throw config_error("cannot optimize sigma on an empty histogram");
+  constexpr int kCandidates = 17;
+  std::array<double, kCandidates> candidate{}, price{};
+  for (int i = 0; i < kCandidates; ++i) {
+    candidate[i] = kSigmaMin * std::pow(kSigmaMax / kSigmaMin, static_cast<double>(i) / (kCandidates - 1));
+    price[i] = weighted_cost(h, mu, candidate[i], coding_cost_tail);
   }
-  constexpr int kGrid = 17, kMaxSteps = 60;
-  constexpr double kTol = 1e-4;
-  // coarse geometric scan of the unfloored cost, then bisection on dF/dsigma inside the best cell
-  double grid[kGrid], best_cost = 0.0;
-  int best = 0;
-  for (int i = 0; i < kGrid; ++i) {
-    grid[i] = kSigmaMin * std::pow(kSigmaMax / kSigmaMin, static_cast<double>(i) / (kGrid - 1));
-    const double cost = weighted_cost(h, mu, grid[i], coding_cost_tail);
-    if (i == 0 || cost < best_cost) best_cost = cost, best = i;
+  const int cheapest = static_cast<int>(std::min_element(price.begin(), price.end()) - price.begin());  // first minimum
+  SigmaSearch found{candidate[cheapest], 0};
+  const double left = candidate[cheapest > 0 ? cheapest - 1 : 0];
+  const double right = candidate[cheapest + 1 < kCandidates ? cheapest + 1 : kCandidates - 1];
+  auto slope = [&](double sigma) { return histogram_objective_dsigma(h, mu, sigma); };
+  const double slope_left = slope(left), slope_right = slope(right);
+  if (slope_left < 0.0 && slope_right > 0.0) {
+    const double refined = centre_of_sign_change(slope, left, right, 1e-4, 60, &found.bisection_steps);
+    if (weighted_cost(h, mu, refined, coding_cost_tail) <= price[cheapest]) found.sigma = refined;
   }
-  SigmaSearch out{grid[best], 0};
-  double lo = grid[std::max(0, best - 1)], hi = grid[std::min(kGrid - 1, best + 1)];
-  double f_lo = histogram_objective_dsigma(h, mu, lo);
-  const double f_hi = histogram_objective_dsigma(h, mu, hi);
-  if (!(f_lo < 0.0) || !(f_hi > 0.0)) return out;
-  while (hi - lo > kTol && out.bisection_steps < kMaxSteps) {
-    ++out.bisection_steps;
-    const double mid = 0.5 * (lo + hi);
-    const double f_mid = histogram_objective_dsigma(h, mu, mid);
-    if (f_mid == 0.0) {
-      lo = hi = mid;
-      break;
-    }
-    if ((f_mid > 0.0) == (f_lo > 0.0)) {
-      lo = mid;
-      f_lo = f_mid;
-    } else {
-      hi = mid;
-    }
-  }
-  const double refined = 0.5 * (lo + hi);
-  if (weighted_cost(h, mu, refined, coding_cost_tail) <= best_cost) out.sigma = refined;
-  return out;
+  return found;
 }
 
 std::uint64_t splitmix64(std::uint64_t z) {

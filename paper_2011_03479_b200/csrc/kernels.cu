@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -770,34 +771,52 @@ __device__ __forceinline__ void pair_terms(double delta, bool is_edge, const Rou
 // delta is only known to ~3e-7 in this mode, so the scalar chain is carried in fp32 as well (relative error
 // ~1e-6 on wf and sf, two orders below the 1e-4 parity bar); tallies stay exact through the double recheck.
 struct SmemTablesF {
-  float erf[65];
-  float ratio[65];
+  float4 cell[kTableF32Entries];  // ratio cells, then erf segments: {a, b, c, 0} (kernels.hpp)
 };
 struct RoundMathF {
   float mu, inv_sqrt2_sigma, A, B, C;
 };
 
-__device__ __forceinline__ int segment_of_f(const float* __restrict__ knots, float x) {
-  int s = x >= knots[8] ? 8 : 0;
-  s += x >= knots[s + 4] ? 4 : 0;
-  s += x >= knots[s + 2] ? 2 : 0;
-  s += x >= knots[s + 1] ? 1 : 0;
-  return s;
+// MUFU approximations without the denormal guards the intrinsics carry (arguments and results here are far from the
+// denormal range; a flushed 1e-39 changes nothing at the 1e-4 bar)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
-__device__ __forceinline__ float quad_eval_f(const float* __restrict__ t, float x) {
-  const int s = segment_of_f(t, x);
-  return fmaf(fmaf(t[17 + s], x, t[33 + s]), x, t[49 + s]);
+__device__ __forceinline__ float exp_approx(float x) {  // e^x
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x * 1.4426950408889634f));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {  // relative error 2^-23; the tallies are rechecked in double
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// the ratio table's quadratic at x in [-1, 8]: the cell index IS the segment search (a value within rounding of a knot
+// may land in the neighbouring segment; the fit is continuous across knots)
+__device__ __forceinline__ float ratio_table_f(const SmemTablesF& tab, float x) {
+  const int i = min(max(__float2int_rd(fmaf(x, 20.0f, 20.0f)), 0), kRatioCells - 1);
+  const float4 q = tab.cell[i];
+  return fmaf(fmaf(q.x, x, q.y), x, q.z);
+}
+// the erf table's quadratic at x in [0, 6]
+__device__ __forceinline__ float erf_table_f(const SmemTablesF& tab, float x) {
+  const int s = min(__float2int_rd(x * (16.0f / 6.0f)), kErfSegments - 1);
+  const float4 q = tab.cell[kRatioCells + s];
+  return fmaf(fmaf(q.x, x, q.y), x, q.z);
 }
 __device__ __forceinline__ float tail_series_f(float x) {
-  const float r = __fdividef(1.0f, x * x);
+  const float r = rcp_approx(x * x);
   const float series = fmaf(r, fmaf(r, fmaf(r, fmaf(6.5625f, r, -1.875f), 0.75f), -0.5f), 1.0f);
-  return __fdividef(x * 1.7724538509055160273f, series);
+  return x * 1.7724538509055160273f * rcp_approx(series);
 }
 __device__ __forceinline__ float gauss_erfc_ratio_f(float x, int exact, const SmemTablesF& tab) {
   if (exact) return x <= 6.0f ? __fdividef(__expf(-x * x), erfcf(x)) : tail_series_f(x);
-  if (x >= -1.0f) return x > 8.0f ? tail_series_f(x) : quad_eval_f(tab.ratio, x);
+  if (x >= -1.0f) return x > 8.0f ? tail_series_f(x) : ratio_table_f(tab, x);
   if (x < -6.0f) return 0.0f;
-  return __fdividef(__expf(-x * x), 1.0f + quad_eval_f(tab.erf, -x));
+  return exp_approx(-x * x) * rcp_approx(1.0f + erf_table_f(tab, -x));
 }
 __device__ __forceinline__ void pair_terms_f(float delta, bool is_edge, const RoundMathF& m, int exact,
                                              const SmemTablesF& tab, float& wf, float& sf) {
@@ -811,8 +830,22 @@ __device__ __forceinline__ void pair_terms_f(float delta, bool is_edge, const Ro
     wf = w;
     const float dw = delta * w;
     const float num = fmaf(m.C, sg, dw);
-    if (delta > 0.0f && num > 0.0f) sf = __fdividef(num, dw);
+    if (delta > 0.0f && num > 0.0f) sf = num * rcp_approx(dw);
   }
+}
+
+// per-block copy of the round's tables into shared memory: the double knot/coefficient arrays (PRECISE) or the
+// directly indexed fp32 cells
+template <int THREADS>
+__device__ __forceinline__ void load_tables(SmemTables& sh, const GatherArgs& a) {
+  for (int i = threadIdx.x; i < 65; i += THREADS) {
+    sh.erf[i] = a.tab.erf[i];
+    sh.ratio[i] = a.tab.ratio[i];
+  }
+}
+template <int THREADS>
+__device__ __forceinline__ void load_tables(SmemTablesF& sh, const GatherArgs& a) {
+  for (int i = threadIdx.x; i < kTableF32Entries; i += THREADS) sh.cell[i] = __ldg(a.tab_f32 + i);
 }
 
 template <int VEC>
@@ -854,210 +887,6 @@ __device__ __forceinline__ double shfl_xor_f64(double v, int off) {
   return __shfl_xor_sync(kFull, v, off);
 }
 
-// One warp per work item.  A row of ld floats is spread over LPR lanes, NV vectors of VEC floats per lane
-// (lane r holds vector r + LPR*j); the warp's 32/LPR lane groups walk the item's lists in parallel, U rows
-// per group in flight.  At d = 2 this degenerates to one thread per list entry (LPR = 1), at d >= 128 to one
-// warp per row (LPR = 32).
-template <int LPR, int NV, int VEC, int U>
-__global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, std::uint32_t item_lo,
-                                                          std::uint32_t item_hi) {
-  constexpr int G = 32 / LPR;
-  __shared__ unsigned int sh_hist[2 * kBins];
-  __shared__ SmemTables sh_tab;
-  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
-  for (int i = threadIdx.x; i < 65; i += kThreads) {
-    sh_tab.erf[i] = a.tab.erf[i];
-    sh_tab.ratio[i] = a.tab.ratio[i];
-  }
-  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / LPR, r = lane % LPR;
-  const std::uint32_t item = item_lo + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-
-  if (item < item_hi) {
-    const uint4 it = __ldg(a.items + item);
-    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
-    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
-    const std::uint32_t end = min(begin + a.chunk_entries, row_hi);
-    const bool first = begin == row_lo;
-    const std::uint32_t ld = a.ld;
-
-    bool act[NV];
-    float xu[NV][VEC];
-    double xud[NV][VEC];
-    float y[NV][VEC];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      act[j] = static_cast<std::uint32_t>((r + LPR * j) * VEC) < ld;
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) xu[j][c] = 0.0f, y[j][c] = 0.0f;
-      if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(u) * ld + (r + LPR * j) * VEC, xu[j]);
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) xud[j][c] = static_cast<double>(xu[j][c]);
-    }
-    float zacc = 0.0f;
-
-    // tally: 0 never, 1 always, 2 when u < other (each undirected edge is met from both endpoints)
-    auto walk = [&](const std::uint32_t* __restrict__ ids, std::uint32_t len, bool is_edge, int tally) {
-      for (std::uint32_t base = 0; base < len; base += G * U) {
-        std::uint32_t other[U];
-        float xv[U][NV][VEC];
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const std::uint32_t e = base + q * G + grp;
-          other[q] = e < len ? __ldg(ids + e) : 0xffffffffu;
-        }
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const std::uint32_t src_row = other[q] != 0xffffffffu ? other[q] : u;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) xv[q][j][c] = 0.0f;
-            if (act[j]) load_row<VEC>(a.x_cur + static_cast<std::size_t>(src_row) * ld + (r + LPR * j) * VEC, xv[q][j]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          // pair_distance (engine.cpp:45-52): double accumulation of squared double differences
-          double part = 0.0;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-              const double diff = xud[j][c] - static_cast<double>(xv[q][j][c]);
-              part = fma(diff, diff, part);
-            }
-          }
-#pragma unroll
-          for (int off = LPR / 2; off > 0; off >>= 1) part += shfl_xor_f64(part, off);
-          if (other[q] != 0xffffffffu) {
-            const double delta = sqrt(part);
-            if (r == 0 && (tally == 1 || (tally == 2 && u < other[q]))) {
-              // DistanceHistogram::record (histogram.hpp:24-29), tallied before the w > 0 test
-              int b = static_cast<int>(delta / 12.0 * 512.0);
-              b = b >= kBins ? kBins - 1 : (b < 0 ? 0 : b);
-              atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + b], 1u);
-            }
-            float wf, sf;
-            pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
-            // add_pair, own side (engine.cpp:66-72): y_u += wf * (x_v + sf * (x_u - x_v)); z_u += wf
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-#pragma unroll
-              for (int c = 0; c < VEC; ++c) {
-                const float diff = xu[j][c] - xv[q][j][c];
-                y[j][c] += wf * (xv[q][j][c] + sf * diff);
-              }
-            }
-            zacc += wf;
-          }
-        }
-      }
-    };
-
-    walk(a.nbr + begin, end - begin, true, 2);
-    if (a.neg_mode == 0) walk(a.neg_own + begin, end - begin, false, 1);
-    if (first) {
-      if (a.neg_mode == 1) walk(a.neg_own + static_cast<std::size_t>(u) * a.k, a.k, false, 1);
-      const std::uint32_t in_lo = __ldg(a.in_off + u), in_hi = __ldg(a.in_off + u + 1);
-      walk(a.in_anchor + in_lo, in_hi - in_lo, false, 0);
-    }
-
-    // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107)
-    double ys[NV][VEC];
-    double zs = static_cast<double>(zacc);
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) {
-        double t = static_cast<double>(y[j][c]);
-#pragma unroll
-        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
-        ys[j][c] = t;
-      }
-    }
-#pragma unroll
-    for (int off = LPR; off < 32; off <<= 1) zs += shfl_xor_f64(zs, off);
-
-    bool finalize = true;
-    if (hub != kNoHub) {
-      const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
-      const std::uint32_t slot = p0 + it.w;
-      if (grp == 0) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          if (!act[j]) continue;
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
-        }
-        if (r == 0) a.part_z[slot] = zs;
-      }
-      __threadfence();
-      __syncwarp();
-      std::uint32_t arrived = 0;
-      if (lane == 0) arrived = atomicAdd(a.hub_arrived + hub, 1u);
-      arrived = __shfl_sync(kFull, arrived, 0);
-      finalize = arrived == q - 1;
-      if (finalize) {  // last slice of the hub: consolidate the partials in slot order
-        __threadfence();
-        zs = 0.0;
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
-        for (std::uint32_t s = p0; s < p0 + q; ++s) {
-          zs += __ldcg(a.part_z + s);
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            if (!act[j]) continue;
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(s) * ld + (r + LPR * j) * VEC + c);
-          }
-        }
-        if (lane == 0) a.hub_arrived[hub] = 0;
-      }
-    }
-
-    if (finalize && grp == 0) {
-      // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
-      bool bad = false;
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        if (!act[j]) continue;
-        float out[VEC];
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          out[c] = xu[j][c];
-          if (zs > 0.0) {
-            out[c] = static_cast<float>(ys[j][c] / zs);
-            bad |= !isfinite(out[c]);
-          }
-        }
-        const std::uint32_t col = (r + LPR * j) * VEC;
-        store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld + col, out);
-        if (a.cap_y) {
-#pragma unroll
-          for (int c = 0; c < VEC; ++c)
-            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
-        }
-      }
-      if (a.cap_z && r == 0) a.cap_z[u] = zs;
-      if (bad) atomicOr(a.status + kStatNonFinite, 1u);
-    }
-  }
-
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
-    const unsigned int c = sh_hist[i];
-    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
-  }
-  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
-}
-
-
 // ---------------------------------------------------------------------------------- gather, batched
 //
 // Same work decomposition as gather_kernel, but the per-pair scalar math (sqrt, parabola_impl) is no longer
@@ -1065,13 +894,18 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const GatherArgs a, st
 // and walks each item's lists in batches of E = (32/LPR) * TB entries: every lane group keeps TB rows in
 // registers -- as DIFFERENCES x_u - x_v, the only form both the distance and the update need -- the TB per-row
 // partial squared distances are reduced with a transposed (recursive-halving) shuffle pattern that leaves
-// entry t of the group in lane t*REP (REP = LPR/TB lanes hold the same total), each lane evaluates the parabola
-// of ITS entry, and one coefficient per row is shuffled back for the accumulation
+// entry t of the group in lanes t*REP .. t*REP + REP - 1 (REP = LPR/TB lanes hold the same total), each lane evaluates
+// the parabola of ITS entry, and one coefficient per row is shuffled back for the accumulation
 //     y_u = sum_t wf_t (x_v + sf_t (x_u - x_v)) = (sum_t wf_t) x_u + sum_t wf_t (sf_t - 1) (x_u - x_v),
 // i.e. one packed FFMA2 per two floats and row (add_pair, engine.cpp:66-72, regrouped; exact same real value).
 // The three lists of an item (adjacency / own samples / incoming samples) are walked as one virtual list whose
 // ids are fetched two batches ahead; the rows of the next batch are pulled into L2 with
 // prefetch.global.L2 while the current batch is being computed.
+//
+// Register slot t of lane r does NOT hold entry t but entry t ^ (r / REP): with that lane-dependent order the transposed
+// reduction needs no selects (at the step with lane distance `off` a lane keeps slots [0, half) and receives its partner's
+// slots [half, 2 half), which are the SAME rows), every lane ends up owning the entry whose id it fetched itself, and both
+// the row ids and the coefficients travel by butterfly shuffles with immediate lane masks (t * REP).
 //
 // PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation), double
 //                  parabola chain.
@@ -1102,16 +936,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   static_assert(TB <= LPR && (TB & (TB - 1)) == 0, "TB must be a power of two <= LPR");
   constexpr int ROW_BYTES_MAX = LPR * NV * VEC * 4;
   constexpr int LINES = ROW_BYTES_MAX >= 128 ? ROW_BYTES_MAX / 128 : 1;  // 128-byte lines per row
-  constexpr bool kPrefetch = ROW_BYTES_MAX >= 128 && U == 1 && (E * LINES) % 32 == 0;
+  constexpr bool kPrefetch = ROW_BYTES_MAX >= 128 && U == 1;
   using red_t = typename std::conditional<PRECISE, double, float>::type;
   __shared__ unsigned int sh_hist[2 * kBins];
   using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
   __shared__ tab_t sh_tab;
   for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) sh_hist[i] = 0;
-  for (int i = threadIdx.x; i < 65; i += THREADS) {
-    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
-    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
-  }
+  load_tables<THREADS>(sh_tab, a);
   const RoundMath rm = a.math_dev ? *a.math_dev : a.math;  // sigma may live on the device (sigma_update_kernel)
   const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
                       static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
@@ -1119,6 +950,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
 
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, r = lane % LPR;
+  const int mine = grp * TB + r / REP;  // the batch entry this lane fetches and, after the reduction, owns
   const std::uint32_t ld = a.ld;
   bool act[NV];
 #pragma unroll
@@ -1130,7 +962,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   auto row_ptr = [&](std::uint32_t row, int j) {
     return reinterpret_cast<const float*>(x_lane + static_cast<std::uint64_t>(row) * row_bytes + LPR * j * VEC * 4);
   };
-  const char* pf_lane = reinterpret_cast<const char*>(a.x_cur) + (lane % LINES) * 128;  // this lane's line of a prefetched row
+  // the REP lanes that share an entry split its row's lines between them for the L2 prefetch
+  constexpr int kPfLines = LINES >= REP ? LINES / REP : 1;
+  const char* pf_lane = reinterpret_cast<const char*>(a.x_cur) + (r % REP) * 128;
+  const bool pf_lane_on = LINES >= REP || (r % REP) < LINES;
 
   // persistent warps: every warp claims kGrab consecutive work items at a time from a global cursor, so no warp
   // idles behind a heavy neighbour and the per-block setup above is paid once per resident block
@@ -1141,39 +976,33 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
     if (claim >= item_hi - item_lo) break;
     const std::uint32_t claim_end = min(claim + kGrab, item_hi - item_lo);
     for (std::uint32_t item = item_lo + claim; item < item_lo + claim_end; ++item) {
-      const uint4 it = __ldg(a.items + item);
-      const std::uint32_t u = it.x, begin = it.y, hub = it.z;
-      const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
-      const bool first = begin == row_lo;
+      // the item's descriptor: two 16-byte loads (the claim's descriptors share one 128-byte line)
+      const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.items + item));
+      const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.items + item) + 1);
+      const std::uint32_t u = d0.x, lenA = d0.z, lenB = d1.x, hub = d1.z;
 
       // virtual list = [adjacency slice | own samples | incoming samples], as offsets into nbr / neg_own / in_anchor
-      const std::uint32_t lenA = min(begin + a.chunk_entries, row_hi) - begin;
-      std::uint32_t offB = begin, lenB = lenA;
-      if (a.neg_mode != 0) {
-        offB = u * a.k;
-        lenB = first ? a.k : 0u;
-      }
       std::uint32_t offC = 0, lenC = 0;
-      if (first) {
+      if (d1.y) {  // first item of the vertex: it takes the incoming samples as well
         offC = __ldg(a.in_off + u);
         lenC = __ldg(a.in_off + u + 1) - offC;
       }
       const std::uint32_t endB = lenA + lenB, total = endB + lenC;
 
-      // one list entry (vertex id) per lane and sub-batch.  Validity and kind (0 edge, 1 sample tallied here, 2
-      // incoming sample) follow from the entry's position alone, so nothing has to wait on these loads until the
-      // ids are needed as addresses two batches later.
+      // one list entry (vertex id) per lane and sub-batch: lane (grp, r) holds entry grp*TB + r/REP of the sub-batch.
+      // Validity and kind (0 edge, 1 sample tallied here, 2 incoming sample) follow from the entry's position alone, so
+      // nothing has to wait on these loads until the ids are needed as addresses two batches later.
       // entry e of the virtual list lives at index e + d of its array (wrapping 32-bit arithmetic)
-      const std::uint32_t dA = begin, dB = offB - lenA, dC = offC - endB;
+      const std::uint32_t dA = d0.y, dB = d0.w - lenA, dC = offC - endB;
       auto fetch = [&](std::uint32_t base, std::uint32_t (&ent)[U]) {
 #pragma unroll
         for (int s = 0; s < U; ++s) {
-          const std::uint32_t e = base + s * E + lane;
+          const std::uint32_t e = base + s * E + mine;
           const bool in_a = e < lenA, in_b = e < endB;
           const std::uint32_t idx = e + (in_a ? dA : (in_b ? dB : dC));
           const std::uint32_t* arr = in_a ? a.nbr : (in_b ? a.neg_own : a.in_anchor);
-          ent[s] = u;
-          if ((E == 32 || lane < E) && e < total) ent[s] = __ldg(arr + idx);
+          ent[s] = u;  // own row past the list end: zero difference, zero weight
+          if (e < total) ent[s] = __ldg(arr + idx);
         }
       };
 
@@ -1192,13 +1021,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       fetch(E * U, nxt);
 
       for (std::uint32_t base = 0; base < total; base += E * U) {
-        // TB rows per lane group and sub-batch, all loads issued before any use
+        // TB rows per lane group and sub-batch, all loads issued before any use; slot t = entry mine ^ t
         float xv[U][TB][NV][VEC];
 #pragma unroll
         for (int s = 0; s < U; ++s) {
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const std::uint32_t src_row = __shfl_sync(kFull, cur[s], grp * TB + t);  // own row u past the list end
+            const std::uint32_t src_row = t == 0 ? cur[s] : __shfl_xor_sync(kFull, cur[s], t * REP);
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (!FULL) {
@@ -1212,11 +1041,10 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         // rows of the next batch -> L2 (their entries arrived during the previous batch), entries of the batch
         // after that -> registers
         if constexpr (kPrefetch) {
+          if (pf_lane_on && base + E + mine < total) {  // the lane's own entry of the next batch: no shuffles
+            const char* row = pf_lane + static_cast<std::uint64_t>(nxt[0]) * row_bytes;
 #pragma unroll
-          for (int i = 0; i < E * LINES / 32; ++i) {  // lane -> line (lane % LINES) of row i * 32 / LINES + lane / LINES
-            const std::uint32_t slot_row = i * (32 / LINES) + lane / LINES;
-            const std::uint32_t row = __shfl_sync(kFull, nxt[0], slot_row);
-            if (base + E + slot_row < total) prefetch_l2(pf_lane + static_cast<std::uint64_t>(row) * row_bytes);
+            for (int i = 0; i < kPfLines; ++i) prefetch_l2(row + i * REP * 128);
           }
         }
         std::uint32_t nn[U];
@@ -1264,19 +1092,16 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             }
           }
           {
+            // select-free transposed reduction: slot i of this lane and slot i + half of the lane `off` away hold
+            // partial sums of the same row (see the slot order above)
             int width = TB;
 #pragma unroll
             for (int off = LPR / 2; off >= 1; off >>= 1) {
               if (width > 1) {
                 const int half = width / 2;
-                const bool upper = (r & off) != 0;
 #pragma unroll
                 for (int i = 0; i < TB / 2; ++i) {
-                  if (i < half) {
-                    const red_t mine = upper ? p[i + half] : p[i];
-                    const red_t theirs = upper ? p[i] : p[i + half];
-                    p[i] = mine + __shfl_xor_sync(kFull, theirs, off);
-                  }
+                  if (i < half) p[i] += __shfl_xor_sync(kFull, p[i + half], off);
                 }
                 width = half;
               } else {
@@ -1284,9 +1109,9 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
               }
             }
           }
-          // this lane now owns entry (grp, r / REP) of the sub-batch
-          const std::uint32_t own = __shfl_sync(kFull, cur[s], grp * TB + r / REP);
-          const std::uint32_t own_e = base + s * E + grp * TB + r / REP;
+          // p[0] is the squared distance of the entry this lane fetched itself
+          const std::uint32_t own = cur[s];
+          const std::uint32_t own_e = base + s * E + mine;
           const bool valid = own_e < total;
           const bool is_edge = own_e < lenA;
           const bool tally = valid && (r % REP == 0) && (is_edge ? u < own : own_e < endB);
@@ -1297,7 +1122,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
             if (valid) pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
           } else {
-            float delta = sqrtf(p[0]);
+            float delta = sqrt_approx(p[0]);
             // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
             const float pos = delta * (512.0f / 12.0f);
             const float frac = pos - floorf(pos);
@@ -1344,7 +1169,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           // y += wf (sf - 1) (x_u - x_v) from the resident differences
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const float ct = __shfl_sync(kFull, coef, grp * LPR + t * REP);
+            const float ct = t == 0 ? coef : __shfl_xor_sync(kFull, coef, t * REP);  // coefficient of entry mine ^ t
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (VEC % 2 == 0) {
@@ -1388,7 +1213,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       bool finalize = true;
       if (hub != kNoHub) {
         const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
-        const std::uint32_t slot = p0 + it.w;
+        const std::uint32_t slot = p0 + d1.w;
         if (grp == 0) {
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
@@ -1478,10 +1303,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
   using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
   __shared__ tab_t sh_tab;
   for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) sh_hist[i] = 0;
-  for (int i = threadIdx.x; i < 65; i += kThreads) {
-    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
-    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
-  }
+  load_tables<kThreads>(sh_tab, a);
   const RoundMath rm = a.math_dev ? *a.math_dev : a.math;
   const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
                       static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
@@ -1489,18 +1311,11 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
 
   const std::uint32_t item = item_lo + blockIdx.x * kThreads + threadIdx.x;
   if (item < item_hi) {
-    const uint4 it = __ldg(a.items + item);
-    const std::uint32_t u = it.x, begin = it.y, hub = it.z;
-    const std::uint32_t row_lo = __ldg(a.rowptr + u), row_hi = __ldg(a.rowptr + u + 1);
-    const bool first = begin == row_lo;
-    const std::uint32_t lenA = min(begin + a.chunk_entries, row_hi) - begin;
-    std::uint32_t offB = begin, lenB = lenA;
-    if (a.neg_mode != 0) {
-      offB = u * a.k;
-      lenB = first ? a.k : 0u;
-    }
+    const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.items + item));
+    const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.items + item) + 1);
+    const std::uint32_t u = d0.x, begin = d0.y, lenA = d0.z, offB = d0.w, lenB = d1.x, hub = d1.z;
     std::uint32_t offC = 0, lenC = 0;
-    if (first) {
+    if (d1.y) {  // first item of the vertex
       offC = __ldg(a.in_off + u);
       lenC = __ldg(a.in_off + u + 1) - offC;
     }
@@ -1549,7 +1364,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
           bin = static_cast<int>(delta / 12.0 * 512.0);
           pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
         } else {
-          float delta = sqrtf(d2);
+          float delta = sqrt_approx(d2);
           const float pos = delta * (512.0f / 12.0f);
           const float frac = pos - floorf(pos);
           const float tol = 4e-6f * pos + 1e-9f;
@@ -1579,7 +1394,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
     bool finalize = true;
     if (hub != kNoHub) {
       const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
-      const std::uint32_t slot = p0 + it.w;
+      const std::uint32_t slot = p0 + d1.w;
 #pragma unroll
       for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + c] = ys[c];
       a.part_z[slot] = zs;
@@ -1622,402 +1437,6 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
 
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * kBins; i += kThreads) {
-    const unsigned int c = sh_hist[i];
-    if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
-  }
-  if (a.n_peers) __threadfence_system();  // peer stores are performed before the grid retires
-}
-
-// ---------------------------------------------------------------------------------- gather, cp.async pipeline
-//
-// The batched gather with the row loads decoupled from the arithmetic, for 16 < ld <= 128 (rows of 128..512
-// bytes: the HBM-bound shapes).  Every warp software-pipelines its own stream of 16-row batches ACROSS work
-// items: while batch b is being computed from registers, the rows of batch b+1 are in flight as 16-byte
-// `cp.async.cg` (LDGSTS) copies into the warp's shared-memory stage and the list ids of batch b+2 are being
-// fetched.  Lane (grp, r) copies exactly the 16-byte chunk it will later read, so a stage is lane-private
-// storage: completion is a per-thread `cp.async.wait_group`, no barrier, no bank conflicts.  The vertex's own
-// row rides in an extra slot of the item's first batch; item descriptors are fetched eight items per claim.
-// (A warp-specialised variant with a TMA `cp.async.bulk` producer warp was measured first: correct, but the
-// uniform-register bulk copies serialise per lane and one producer per block could not feed 3-7 consumers --
-// 18.7 ms vs 7.4 ms on c4.)
-
-namespace pipe {
-
-constexpr int kE = 16;      // rows per batch / stage
-constexpr int kClaim = 8;   // work items per claim (descriptors live in lanes 0..7)
-constexpr unsigned kHead = 1u, kLast = 2u;
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(std::uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Cursor over the warp's stream of batches.  Descriptor fields are per lane (lane i describes claimed item
-// i); count/cur/pos are warp-uniform; nid/nkind hold, per lane, entry `lane` of the batch at the cursor.
-struct Feed {
-  std::uint32_t u, begin, hub, sub, lenA, lenB, in_lo, lenC;
-  std::uint32_t count, cur, pos;
-  std::uint32_t nid, nkind;
-};
-
-__device__ __forceinline__ void feed_claim(Feed& f, const GatherArgs& a, std::uint32_t item_lo, std::uint32_t n_items,
-                                           int lane) {
-  std::uint32_t base = 0;
-  if (lane == 0) base = atomicAdd(a.work_cursor, static_cast<std::uint32_t>(kClaim));
-  base = __shfl_sync(kFull, base, 0);
-  f.cur = 0;
-  f.pos = 0;
-  if (base >= n_items) {
-    f.count = 0;
-    return;
-  }
-  f.count = min(static_cast<std::uint32_t>(kClaim), n_items - base);
-  f.u = f.begin = f.sub = f.lenA = f.lenB = f.in_lo = f.lenC = 0;
-  f.hub = kNoHub;
-  if (lane < static_cast<int>(f.count)) {
-    const uint4 it = __ldg(a.items + item_lo + base + lane);
-    f.u = it.x;
-    f.begin = it.y;
-    f.hub = it.z;
-    f.sub = it.w;
-    const std::uint32_t row_lo = __ldg(a.rowptr + it.x), row_hi = __ldg(a.rowptr + it.x + 1);
-    f.lenA = min(it.y + a.chunk_entries, row_hi) - it.y;
-    const bool first = it.y == row_lo;
-    f.lenB = a.neg_mode == 0 ? f.lenA : (first ? a.k : 0u);
-    if (first) {
-      f.in_lo = __ldg(a.in_off + it.x);
-      f.lenC = __ldg(a.in_off + it.x + 1) - f.in_lo;
-    }
-  }
-}
-
-// ids of the batch at the cursor, one entry per lane
-__device__ __forceinline__ void feed_prefetch(Feed& f, const GatherArgs& a, int lane) {
-  const std::uint32_t u = __shfl_sync(kFull, f.u, f.cur), begin = __shfl_sync(kFull, f.begin, f.cur);
-  const std::uint32_t lenA = __shfl_sync(kFull, f.lenA, f.cur), lenB = __shfl_sync(kFull, f.lenB, f.cur);
-  const std::uint32_t in_lo = __shfl_sync(kFull, f.in_lo, f.cur), lenC = __shfl_sync(kFull, f.lenC, f.cur);
-  const std::uint32_t e = f.pos + lane, endB = lenA + lenB, total = endB + lenC;
-  f.nid = 0xffffffffu;
-  f.nkind = 0;
-  if (lane < kE && e < total) {
-    if (e < lenA) {
-      f.nid = __ldg(a.nbr + begin + e);
-    } else if (e < endB) {
-      f.nid = a.neg_mode == 0 ? __ldg(a.neg_own + begin + (e - lenA))
-                              : __ldg(a.neg_own + static_cast<std::size_t>(u) * a.k + (e - lenA));
-      f.nkind = 1;
-    } else {
-      f.nid = __ldg(a.in_anchor + in_lo + (e - endB));
-      f.nkind = 2;
-    }
-  }
-}
-
-// what the arithmetic needs to know about a batch whose rows are in (or on their way to) a stage
-struct BatchMeta {
-  std::uint32_t u, nvalid, flags, hub, sub;  // warp-uniform
-  std::uint32_t own_id;                      // per lane: id / kind of the entry this lane will own after the reduction
-  int own_kind;
-};
-
-}  // namespace pipe
-
-template <int LPR, int TB, bool PRECISE, bool FULL, int WARPS, int MINB>
-__global__ void __launch_bounds__(32 * WARPS, MINB) gather_async_kernel(const GatherArgs a, std::uint32_t item_lo,
-                                                                        std::uint32_t item_hi) {
-  using namespace pipe;
-  constexpr int THREADS = 32 * WARPS;
-  constexpr int G = 32 / LPR;
-  constexpr int REP = LPR / TB;
-  constexpr int PITCH = LPR * 16;              // bytes between row slots of a stage
-  constexpr int STAGE = (kE + G) * PITCH;      // 16 rows + one own-row slot per lane group
-  static_assert(G * TB == kE, "a stage holds exactly one batch");
-  constexpr std::uint32_t kNone = 0xffffffffu;
-  using red_t = typename std::conditional<PRECISE, double, float>::type;
-
-  extern __shared__ __align__(128) unsigned char stage_mem[];  // [WARPS][2][STAGE]
-  __shared__ unsigned int sh_hist[2 * kBins];
-  using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
-  __shared__ tab_t sh_tab;
-  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) sh_hist[i] = 0;
-  for (int i = threadIdx.x; i < 65; i += THREADS) {
-    sh_tab.erf[i] = static_cast<decltype(sh_tab.erf[0] + 0)>(a.tab.erf[i]);
-    sh_tab.ratio[i] = static_cast<decltype(sh_tab.ratio[0] + 0)>(a.tab.ratio[i]);
-  }
-  const RoundMath rm = a.math_dev ? *a.math_dev : a.math;  // sigma may live on the device (sigma_update_kernel)
-  const RoundMathF mf{static_cast<float>(rm.mu), static_cast<float>(rm.inv_sqrt2_sigma),
-                      static_cast<float>(rm.A), static_cast<float>(rm.B), static_cast<float>(rm.C)};
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = lane / LPR, r = lane % LPR;
-  const std::uint32_t ld = a.ld;
-  const std::uint32_t n_items = item_hi - item_lo;
-  const bool act = FULL || static_cast<std::uint32_t>(r * 4) < ld;
-  // this lane's private 16-byte column of both stages
-  const std::uint32_t lane_base = smem_u32(stage_mem) + static_cast<std::uint32_t>(warp) * 2u * STAGE + r * 16;
-  const unsigned char* lane_ptr = stage_mem + static_cast<std::size_t>(warp) * 2 * STAGE + r * 16;
-  const float* x_lane = a.x_cur + r * 4;
-
-  Feed f;
-  feed_claim(f, a, item_lo, n_items, lane);
-  if (f.count) feed_prefetch(f, a, lane);
-
-  // Issues the copies of the batch at the cursor into stage `slot`, records its metadata, advances the cursor
-  // and starts the id fetch of the batch after it.  Returns false when the queue is exhausted.
-  auto post = [&](int slot, BatchMeta& m) -> bool {
-    if (f.count == 0) return false;
-    const std::uint32_t total = __shfl_sync(kFull, f.lenA + f.lenB + f.lenC, f.cur);
-    m.u = __shfl_sync(kFull, f.u, f.cur);
-    m.hub = __shfl_sync(kFull, f.hub, f.cur);
-    m.sub = __shfl_sync(kFull, f.sub, f.cur);
-    m.nvalid = min(static_cast<std::uint32_t>(kE), total - f.pos);
-    const bool head = f.pos == 0, last = f.pos + kE >= total;
-    m.flags = (head ? kHead : 0u) | (last ? kLast : 0u);
-    m.own_id = __shfl_sync(kFull, f.nid, grp * TB + r / REP);
-    m.own_kind = static_cast<int>(__shfl_sync(kFull, f.nkind, grp * TB + r / REP));
-    const std::uint32_t dst = lane_base + static_cast<std::uint32_t>(slot) * STAGE;
-#pragma unroll
-    for (int t = 0; t < TB; ++t) {
-      const std::uint32_t id = __shfl_sync(kFull, f.nid, grp * TB + t);
-      if (act && id != kNone) cp_async16(dst + (grp * TB + t) * PITCH, x_lane + static_cast<std::size_t>(id) * ld);
-    }
-    if (head && act) cp_async16(dst + (kE + grp) * PITCH, x_lane + static_cast<std::size_t>(m.u) * ld);
-    cp_async_commit();
-    if (last) {
-      ++f.cur;
-      f.pos = 0;
-      if (f.cur == f.count) feed_claim(f, a, item_lo, n_items, lane);
-    } else {
-      f.pos += kE;
-    }
-    if (f.count) feed_prefetch(f, a, lane);
-    return true;
-  };
-
-  float xu[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  float zacc = 0.0f;
-
-  // The arithmetic of one batch (identical to gather_batched_kernel), rows read from stage `slot`.
-  auto compute = [&](int slot, const BatchMeta& m) {
-    const unsigned char* st = lane_ptr + static_cast<std::size_t>(slot) * STAGE;
-    if (m.flags & kHead) {
-      const float4 t = act ? *reinterpret_cast<const float4*>(st + (kE + grp) * PITCH) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      xu[0] = t.x; xu[1] = t.y; xu[2] = t.z; xu[3] = t.w;
-      y[0] = y[1] = y[2] = y[3] = 0.0f;
-      zacc = 0.0f;
-    }
-    float xv[TB][4];
-#pragma unroll
-    for (int t = 0; t < TB; ++t) {
-      const bool have = act && static_cast<std::uint32_t>(grp * TB + t) < m.nvalid;
-      const float4 q = have ? *reinterpret_cast<const float4*>(st + (grp * TB + t) * PITCH) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      xv[t][0] = q.x; xv[t][1] = q.y; xv[t][2] = q.z; xv[t][3] = q.w;
-    }
-    const std::uint32_t u = m.u;
-    // per-row partial squared distance, then the transposed reduction over the LPR lanes of the group
-    red_t p[TB];
-#pragma unroll
-    for (int t = 0; t < TB; ++t) {
-      if constexpr (PRECISE) {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double diff = static_cast<double>(xu[c]) - static_cast<double>(xv[t][c]);
-          acc = fma(diff, diff, acc);
-        }
-        p[t] = acc;
-      } else {
-        float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          const float2 diff = ffma2(make_float2(xv[t][c], xv[t][c + 1]), make_float2(-1.0f, -1.0f),
-                                    make_float2(xu[c], xu[c + 1]));
-          acc = ffma2(diff, diff, acc);
-        }
-        p[t] = acc.x + acc.y;
-      }
-    }
-    {
-      int width = TB;
-#pragma unroll
-      for (int off = LPR / 2; off >= 1; off >>= 1) {
-        if (width > 1) {
-          const int half = width / 2;
-          const bool upper = (r & off) != 0;
-#pragma unroll
-          for (int i = 0; i < TB / 2; ++i) {
-            if (i < half) {
-              const red_t mine = upper ? p[i + half] : p[i];
-              const red_t theirs = upper ? p[i] : p[i + half];
-              p[i] = mine + __shfl_xor_sync(kFull, theirs, off);
-            }
-          }
-          width = half;
-        } else {
-          p[0] += __shfl_xor_sync(kFull, p[0], off);
-        }
-      }
-    }
-    const bool valid = m.own_id != kNone;
-    const bool is_edge = m.own_kind == 0;
-    const bool tally = valid && (r % REP == 0) && (m.own_kind == 1 || (m.own_kind == 0 && u < m.own_id));
-    float wf = 0.0f, sf = 0.0f;
-    int bin;
-    if constexpr (PRECISE) {
-      const double delta = sqrt(p[0]);
-      bin = static_cast<int>(delta / 12.0 * 512.0);  // DistanceHistogram::record (histogram.hpp:24-29)
-      if (valid) pair_terms(delta, is_edge, rm, sh_tab, wf, sf);
-    } else {
-      float delta = sqrtf(p[0]);
-      // exact tallies: recompute in double the rows whose bin position is within the fp32 error bound of an edge
-      const float pos = delta * (512.0f / 12.0f);
-      const float frac = pos - floorf(pos);
-      const float tol = 4e-6f * pos + 1e-9f;
-      const bool amb = tally && pos < 513.0f && (frac < tol || frac > 1.0f - tol);
-      bin = static_cast<int>(pos);
-      unsigned amb_rows = 0;
-      unsigned pending = __ballot_sync(kFull, amb);
-      while (pending) {
-        const int l = __ffs(pending) - 1;
-        pending &= pending - 1;
-        amb_rows |= 1u << ((l % LPR) / REP);
-      }
-      if (amb_rows) {
-#pragma unroll
-        for (int t = 0; t < TB; ++t) {
-          if (amb_rows & (1u << t)) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const double diff = static_cast<double>(xu[c]) - static_cast<double>(xv[t][c]);
-              acc = fma(diff, diff, acc);
-            }
-#pragma unroll
-            for (int off = LPR / 2; off >= 1; off >>= 1) acc += shfl_xor_f64(acc, off);
-            if (amb && r / REP == t) {
-              const double exact = sqrt(acc);
-              bin = static_cast<int>(exact / 12.0 * 512.0);
-              delta = static_cast<float>(exact);
-            }
-          }
-        }
-      }
-      if (valid) pair_terms_f(delta, is_edge, mf, rm.exact, sh_tab, wf, sf);
-    }
-    if (tally) {  // tallied before the w > 0 test (engine.cpp:221-222)
-      bin = bin >= kBins ? kBins - 1 : (bin < 0 ? 0 : bin);
-      atomicAdd(&sh_hist[(is_edge ? 0 : kBins) + bin], 1u);
-    }
-    if (r % REP == 0) zacc += wf;
-    // add_pair, own side (engine.cpp:66-72): y += wf * (x_v + sf * (x_u - x_v))
-#pragma unroll
-    for (int t = 0; t < TB; ++t) {
-      const float wt = __shfl_sync(kFull, wf, grp * LPR + t * REP);
-      const float st2 = __shfl_sync(kFull, sf, grp * LPR + t * REP);
-#pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        const float2 other = make_float2(xv[t][c], xv[t][c + 1]);
-        const float2 diff = ffma2(other, make_float2(-1.0f, -1.0f), make_float2(xu[c], xu[c + 1]));
-        const float2 tgt = ffma2(make_float2(st2, st2), diff, other);
-        const float2 acc = ffma2(make_float2(wt, wt), tgt, make_float2(y[c], y[c + 1]));
-        y[c] = acc.x;
-        y[c + 1] = acc.y;
-      }
-    }
-
-    if (m.flags & kLast) {
-      // item complete: cross-group reduction in double, hub consolidation, y / z update (engine.cpp:253-276)
-      double ys[4];
-      double zs = static_cast<double>(zacc);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double t = static_cast<double>(y[c]);
-#pragma unroll
-        for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
-        ys[c] = t;
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
-      bool finalize = true;
-      if (m.hub != kNoHub) {
-        const std::uint32_t p0 = __ldg(a.hub_first + m.hub), q = __ldg(a.hub_items + m.hub);
-        const std::uint32_t hslot = p0 + m.sub;
-        if (grp == 0) {
-          if (act) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) a.part_y[static_cast<std::size_t>(hslot) * ld + r * 4 + c] = ys[c];
-          }
-          if (r == 0) a.part_z[hslot] = zs;
-        }
-        __threadfence();
-        __syncwarp();
-        std::uint32_t arrived = 0;
-        if (lane == 0) arrived = atomicAdd(a.hub_arrived + m.hub, 1u);
-        arrived = __shfl_sync(kFull, arrived, 0);
-        finalize = arrived == q - 1;
-        if (finalize) {  // last slice of the hub: consolidate the partials in slot order
-          __threadfence();
-          zs = 0.0;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) ys[c] = 0.0;
-          for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
-            zs += __ldcg(a.part_z + sl);
-            if (act) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) ys[c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + r * 4 + c);
-            }
-          }
-          if (lane == 0) a.hub_arrived[m.hub] = 0;
-        }
-      }
-      if (finalize && grp == 0 && act) {
-        bool bad = false;
-        float out[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          out[c] = xu[c];
-          if (zs > 0.0) {
-            out[c] = static_cast<float>(ys[c] / zs);
-            bad |= !isfinite(out[c]);
-          }
-        }
-        const std::uint32_t col = r * 4;
-        store_row_everywhere<4>(a, static_cast<std::size_t>(u) * ld + col, out);
-        if (a.cap_y) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[c];
-        }
-        if (a.cap_z && r == 0) a.cap_z[u] = zs;
-        if (bad) atomicOr(a.status + kStatNonFinite, 1u);
-      }
-    }
-  };
-
-  // two-stage software pipeline, unrolled by two so that the stage index is a compile-time constant
-  BatchMeta m0, m1;
-  bool have0 = post(0, m0), have1 = false;
-  while (have0) {
-    have1 = post(1, m1);
-    if (have1) cp_async_wait<1>(); else cp_async_wait<0>();
-    compute(0, m0);
-    if (!have1) break;
-    have0 = post(0, m0);
-    if (have0) cp_async_wait<1>(); else cp_async_wait<0>();
-    compute(1, m1);
-  }
-
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2 * kBins; i += THREADS) {
     const unsigned int c = sh_hist[i];
     if (c) atomicAdd(a.hist + i, static_cast<unsigned long long>(c));
   }
@@ -2172,13 +1591,18 @@ __global__ void __launch_bounds__(kThreads) pe_sum_kernel(const float* __restric
 
 __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long long* __restrict__ hist, double mu,
                                                              double pairs, double edges, int exact_math,
-                                                             SigmaState* __restrict__ state) {
+                                                             SigmaState* __restrict__ state,
+                                                             std::uint32_t* __restrict__ status) {
   using namespace sigma;
   __shared__ double scratch[kBins / 32];
   const int b = threadIdx.x;
   const double ec = static_cast<double>(hist[b]), nc = static_cast<double>(hist[kBins + b]);
   const double mid = (b + 0.5) * 12.0 / kBins;  // histogram.hpp:52
   const double samples = block_sum(nc, scratch);
+  if (block_sum(ec, scratch) + samples == 0.0) {  // optimize_sigma on an empty histogram is a config_error (slope.cpp:76)
+    if (b == 0) atomicOr(status + kStatEmptyTallies, 1u);
+    return;  // sigma stays what it was
+  }
   const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;  // engine.cpp:296-300
   auto total = [&](double s, int which) {
     double v = 0.0;
@@ -2276,7 +1700,7 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
 constexpr int kSigmaCtas = 8;
 __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
     sigma_update_cluster_kernel(const unsigned long long* __restrict__ hist, double mu, double pairs, double edges,
-                                int exact_math, SigmaState* __restrict__ state) {
+                                int exact_math, SigmaState* __restrict__ state, std::uint32_t* __restrict__ status) {
   using namespace sigma;
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -2288,6 +1712,13 @@ __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
   const double mid = (b + 0.5) * 12.0 / kBins;
   const double cap = state->sigma * 1.5;  // read before anybody writes the state (CTA 0, after the last sync)
   const double samples = block_sum(nc, scratch);
+  const bool empty = block_sum(ec, scratch) + samples == 0.0;  // the same in every CTA: all return together
+  // every CTA of the cluster is running (and its shared memory exists) before anybody stores into a peer's mailbox
+  cluster.sync();
+  if (empty) {  // optimize_sigma on an empty histogram is a config_error (slope.cpp:76); sigma stays what it was
+    if (cta == 0 && b == 0) atomicOr(status + kStatEmptyTallies, 1u);
+    return;
+  }
   const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;
   auto total = [&](double s, int which) {
     double v = 0.0;
@@ -2478,6 +1909,31 @@ inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
   return static_cast<unsigned>((work + per_block - 1) / per_block);
 }
 
+// SM count of the CURRENT device (a process may drive contexts on several GPUs from several threads: nothing about a
+// device is cached in a plain static)
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int device = 0;
+  cudaGetDevice(&device);
+  return device;
+}
+inline unsigned sm_count() {
+  static std::atomic<int> cached[kMaxDevices] = {};
+  const int device = current_device();
+  int sms = device < kMaxDevices ? cached[device].load(std::memory_order_relaxed) : 0;
+  if (sms == 0) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    sms = std::max(1, sms);
+    if (device < kMaxDevices) cached[device].store(sms, std::memory_order_relaxed);
+  }
+  return static_cast<unsigned>(sms);
+}
+// grid-stride kernels: enough blocks for `work`, at most `per_sm` per SM
+inline unsigned capped_blocks(std::uint64_t work, unsigned per_block, unsigned per_sm) {
+  return static_cast<unsigned>(std::min<std::uint64_t>((work + per_block - 1) / per_block,
+                                                       static_cast<std::uint64_t>(sm_count()) * per_sm));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------- launchers
@@ -2485,7 +1941,7 @@ inline unsigned blocks_for(std::uint64_t work, unsigned per_block) {
 int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                           std::uint32_t* flags, cudaStream_t stream) {
   if (m == 0) return 0;
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  const unsigned blocks = capped_blocks(m, kThreads, 32);
   validate_edges_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, flags);
   return 1;
 }
@@ -2493,20 +1949,20 @@ int launch_validate_edges(const std::uint32_t* src, const std::uint32_t* dst, st
 int launch_hash_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                       std::uint32_t hash_mask, std::uint32_t* hash_words, cudaStream_t stream) {
   if (m == 0) return 0;
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  const unsigned blocks = capped_blocks(m, kThreads, 32);
   hash_build_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, n, hash_mask, hash_words);
   return 1;
 }
 
 int launch_hash_popcount(const std::uint32_t* hash_words, std::uint64_t nwords, unsigned long long* total, cudaStream_t stream) {
   cudaMemsetAsync(total, 0, sizeof(unsigned long long), stream);
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((nwords + kThreads - 1) / kThreads, 148u * 16u));
+  const unsigned blocks = capped_blocks(nwords, kThreads, 16);
   hash_popcount_kernel<<<blocks, kThreads, 0, stream>>>(hash_words, nwords, total);
   return 1;
 }
 
 int launch_hash_summary(const std::uint32_t* hash_words, std::uint64_t nsummary, std::uint32_t* summary, cudaStream_t stream) {
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((nsummary + kThreads - 1) / kThreads, 148u * 16u));
+  const unsigned blocks = capped_blocks(nsummary, kThreads, 16);
   hash_summary_kernel<<<blocks, kThreads, 0, stream>>>(hash_words, nsummary, summary);
   return 1;
 }
@@ -2521,15 +1977,14 @@ int launch_probe(const std::uint32_t* hash_words, std::uint32_t hash_mask, std::
 int launch_relabel_apply(std::uint32_t* src, std::uint32_t* dst, std::uint64_t m, const std::uint32_t* forward,
                          cudaStream_t stream) {
   if (m == 0) return 0;
-  relabel_apply_kernel<<<static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u)), kThreads, 0,
-                         stream>>>(src, dst, m, forward);
+  relabel_apply_kernel<<<capped_blocks(m, kThreads, 32), kThreads, 0, stream>>>(src, dst, m, forward);
   return 1;
 }
 
 int launch_csr_build(const std::uint32_t* src, const std::uint32_t* dst, std::uint64_t m, std::uint32_t n,
                      std::uint32_t* deg, std::uint32_t* rowptr, std::uint32_t* scratch, std::uint32_t* nbr,
                      std::uint32_t* eid_role, std::uint32_t* csr_src, cudaStream_t stream) {
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((m + kThreads - 1) / kThreads, 148u * 32u));
+  const unsigned blocks = capped_blocks(m, kThreads, 32);
   cudaMemsetAsync(deg, 0, static_cast<std::size_t>(n) * sizeof(std::uint32_t), stream);
   degree_count_kernel<<<blocks, kThreads, 0, stream>>>(src, dst, m, deg);
   const int scans = launch_scan(deg, rowptr, n, scratch, stream);
@@ -2569,7 +2024,7 @@ int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uin
     ++launches;
   }
   if (x.spill) {
-    count_spill_kernel<<<148 * 4, kThreads, 0, stream>>>(x, in_cnt, spill_rank);
+    count_spill_kernel<<<sm_count() * 4, kThreads, 0, stream>>>(x, in_cnt, spill_rank);
     ++launches;
   }
   launches += launch_scan(in_cnt, in_off, n, scratch, stream);
@@ -2578,18 +2033,14 @@ int launch_bucket_records(const ExchangeArgs& x, std::uint32_t sources, std::uin
     ++launches;
   }
   if (x.spill) {
-    scatter_spill_kernel<<<148 * 4, kThreads, 0, stream>>>(x, spill_rank, in_off, in_anchor);
+    scatter_spill_kernel<<<sm_count() * 4, kThreads, 0, stream>>>(x, spill_rank, in_off, in_anchor);
     ++launches;
   }
   return launches;
 }
 
 std::uint32_t partition_grid(std::uint64_t slots) {
-  int device = 0, sms = 148;
-  cudaGetDevice(&device);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return static_cast<std::uint32_t>(std::min<std::uint64_t>((slots + kPartThreads - 1) / kPartThreads,
-                                                            static_cast<std::uint64_t>(sms) * 4));
+  return capped_blocks(slots, kPartThreads, 4);
 }
 
 int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::uint32_t* in_off, std::uint32_t* in_anchor,
@@ -2598,20 +2049,18 @@ int launch_sample_partition(const SampleArgs& a, const PartitionArgs& p, std::ui
   const std::uint32_t grid = p.grid;
   const std::size_t hist_smem = static_cast<std::size_t>(p.buckets) * sizeof(std::uint32_t);
   const std::size_t vert_smem = (static_cast<std::size_t>(1) << p.shift) * sizeof(std::uint32_t);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(bucket_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    configured = true;
+  {  // the attribute is per device: set it once on every device this process launches on
+    static std::atomic<bool> configured[kMaxDevices] = {};
+    const int device = current_device();
+    if (device >= kMaxDevices || !configured[device].load(std::memory_order_relaxed)) {
+      cudaFuncSetAttribute(bucket_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (device < kMaxDevices) configured[device].store(true, std::memory_order_relaxed);
+    }
   }
   sample_count_kernel<<<grid, kPartThreads, hist_smem, stream>>>(a, p);
   bucket_column_scan_kernel<<<blocks_for(p.buckets, 128), 128, 0, stream>>>(p, grid);
   bucket_offsets_kernel<<<1, 1024, 0, stream>>>(p, in_off, a.n);
-  {
-    int device = 0, sms = 148;
-    cudaGetDevice(&device);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    partition_kernel<<<std::min<std::uint32_t>(grid, static_cast<std::uint32_t>(sms)), 1024, hist_smem, stream>>>(a, p);
-  }
+  partition_kernel<<<std::min<std::uint32_t>(grid, sm_count()), 1024, hist_smem, stream>>>(a, p);
   bucket_finalize_kernel<<<p.buckets, kPartThreads, vert_smem, stream>>>(p, a.n, in_off, in_anchor);
   return 5;
 }
@@ -2644,7 +2093,7 @@ int launch_permute_rows(const float* in, std::uint32_t in_ld, float* out, std::u
                         std::uint32_t n, const std::uint32_t* map, bool scatter, cudaStream_t stream) {
   const std::uint64_t total = static_cast<std::uint64_t>(n) * dim;
   if (total == 0) return 0;
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(total, kThreads), 148u * 64u));
+  const unsigned blocks = capped_blocks(total, kThreads, 64);
   permute_rows_kernel<<<blocks, kThreads, 0, stream>>>(in, in_ld, out, out_ld, dim, n, map, scatter);
   return 1;
 }
@@ -2667,21 +2116,18 @@ int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32
 }
 
 namespace {
-template <int LPR, int NV, int VEC, int U>
-void gather_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
-  gather_kernel<LPR, NV, VEC, U><<<blocks_for(hi - lo, kThreads / 32), kThreads, 0, stream>>>(a, lo, hi);
-}
 template <int LPR, int NV, int VEC, int TB, int U, bool PRECISE, bool FULL, int THREADS, int MINB>
 void gather_batched_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
   // persistent grid: as many blocks as fit on the device at once (occupancy query cached per instantiation)
-  static int resident_blocks = 0;
+  static std::atomic<int> cached[kMaxDevices] = {};  // per device: GPUs of one process need not be alike
   auto kernel = gather_batched_kernel<LPR, NV, VEC, TB, U, PRECISE, FULL, THREADS, MINB>;
+  const int device = current_device();
+  int resident_blocks = device < kMaxDevices ? cached[device].load(std::memory_order_relaxed) : 0;
   if (resident_blocks == 0) {
-    int device = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&device);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, THREADS, 0);
-    resident_blocks = std::max(1, sms * std::max(1, per_sm));
+    resident_blocks = static_cast<int>(sm_count()) * std::max(1, per_sm);
+    if (device < kMaxDevices) cached[device].store(resident_blocks, std::memory_order_relaxed);
   }
   const unsigned needed = blocks_for(blocks_for(hi - lo, kGrab), THREADS / 32);
   const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
@@ -2700,63 +2146,12 @@ void gather_batched_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, 
     else gather_batched_launch<LPR, NV, VEC, TB, U, false, false, THREADS, MINB>(a, lo, hi, stream);
   }
 }
-template <int LPR, int TB, bool PRECISE, bool FULL, int WARPS, int MINB>
-void gather_async_launch(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, cudaStream_t stream) {
-  constexpr int THREADS = 32 * WARPS;
-  constexpr int kSmem = WARPS * 2 * (pipe::kE + 32 / LPR) * LPR * 16;
-  auto kernel = gather_async_kernel<LPR, TB, PRECISE, FULL, WARPS, MINB>;
-  static int resident_blocks = 0;
-  if (resident_blocks == 0) {
-    int device = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&device);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, THREADS, kSmem);
-    resident_blocks = std::max(1, sms * std::max(1, per_sm));
-  }
-  const unsigned needed = blocks_for(blocks_for(hi - lo, pipe::kClaim), WARPS);
-  const unsigned blocks = std::min<unsigned>(needed, static_cast<unsigned>(resident_blocks));
-  cudaMemsetAsync(a.work_cursor, 0, sizeof(std::uint32_t), stream);
-  kernel<<<blocks, THREADS, kSmem, stream>>>(a, lo, hi);
-}
-template <int LPR, int TB, int WARPS = 4, int MINB = 3>
-void gather_async_go(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
-  const bool full = a.ld == static_cast<std::uint32_t>(LPR * 4);
-  if (precise) {
-    if (full) gather_async_launch<LPR, TB, true, true, WARPS, MINB>(a, lo, hi, stream);
-    else gather_async_launch<LPR, TB, true, false, WARPS, MINB>(a, lo, hi, stream);
-  } else {
-    if (full) gather_async_launch<LPR, TB, false, true, WARPS, MINB>(a, lo, hi, stream);
-    else gather_async_launch<LPR, TB, false, false, WARPS, MINB>(a, lo, hi, stream);
-  }
-}
 }  // namespace
 
-int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int variant, bool precise,
-                  cudaStream_t stream) {
+int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool precise, cudaStream_t stream) {
   if (hi <= lo) return 0;
   const std::uint32_t ld = a.ld;
-  if (variant == 1) {  // v0: one row per lane group at a time, kept for A/B runs
-    if (ld == 1) gather_go<1, 1, 1, 4>(a, lo, hi, stream);
-    else if (ld == 2) gather_go<1, 1, 2, 4>(a, lo, hi, stream);
-    else if (ld <= 4) gather_go<1, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 8) gather_go<2, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 16) gather_go<4, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 32) gather_go<8, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 64) gather_go<16, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 128) gather_go<32, 1, 4, 4>(a, lo, hi, stream);
-    else if (ld <= 256) gather_go<32, 2, 4, 2>(a, lo, hi, stream);
-    else if (ld <= 512) gather_go<32, 4, 4, 1>(a, lo, hi, stream);
-    else gather_go<32, 8, 4, 1>(a, lo, hi, stream);  // ld <= 1024 (checked at create)
-    return 1;
-  }
-  if (variant >= 10 && ld > 16 && ld <= 128) {  // cp.async pipeline (experimental: register pressure caps it at 8 warps/SM)
-    if (ld <= 32) gather_async_go<8, 4>(a, lo, hi, precise, stream);
-    else if (ld <= 64) gather_async_go<16, 8>(a, lo, hi, precise, stream);
-    else gather_async_go<32, 16, 4, 2>(a, lo, hi, precise, stream);  // 8 warps/SM: 204 registers
-    return 1;
-  }
-  if (ld <= 4 && variant != 2) {  // one thread per work item (variant 2 keeps the warp-per-item kernel for A/B runs)
+  if (ld <= 4) {  // one thread per work item
     const unsigned blocks = blocks_for(hi - lo, kThreads);
     if (ld == 1) {
       if (precise) gather_thread_kernel<1, true><<<blocks, kThreads, 0, stream>>>(a, lo, hi);
@@ -2771,12 +2166,9 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
     return 1;
   }
   //                          LPR NV VEC TB U
-  if (ld == 1) gather_batched_go<1, 1, 1, 1, 8>(a, lo, hi, precise, stream);
-  else if (ld == 2) gather_batched_go<1, 1, 2, 1, 8>(a, lo, hi, precise, stream);
-  else if (ld <= 4) gather_batched_go<1, 1, 4, 1, 8>(a, lo, hi, precise, stream);
   // narrow rows need few registers: 128-thread blocks at 8-12 per SM (c3 graph, dimension overridden: d = 8 -40 %,
   // d = 16 -24 %, d = 32 -24 %, d = 64 -13 % against 256-thread blocks at 2 per SM / 16 rows at 5 per SM)
-  else if (ld <= 8) gather_batched_go<2, 1, 4, 2, 2, 128, 12>(a, lo, hi, precise, stream);
+  if (ld <= 8) gather_batched_go<2, 1, 4, 2, 2, 128, 12>(a, lo, hi, precise, stream);
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);  // 8 rows per group, 32 warps/SM
@@ -2794,7 +2186,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, int v
 int launch_pe_collect(const PeCollectArgs& p, cudaStream_t stream) {
   if (p.m == 0) return 0;
   const std::uint64_t work = p.m * (1 + static_cast<std::uint64_t>(p.samples_per_edge));
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(work, kThreads), 148u * 64u));
+  const unsigned blocks = capped_blocks(work, kThreads, 64);
   pe_collect_kernel<<<blocks, kThreads, 0, stream>>>(p);
   return 1;
 }
@@ -2802,16 +2194,15 @@ int launch_pe_collect(const PeCollectArgs& p, cudaStream_t stream) {
 int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigma, bool is_edge, int which, double* total,
                   unsigned long long* valid, cudaStream_t stream) {
   if (count == 0) return 0;
-  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>(blocks_for(count, kThreads * 4), 148u * 8u));
+  const unsigned blocks = capped_blocks(count, kThreads * 4, 8);
   pe_sum_kernel<<<blocks, kThreads, 0, stream>>>(dist, count, mu, sigma, is_edge ? 1 : 0, which, total, valid);
   return 1;
 }
 
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
-                        SigmaState* state, cudaStream_t stream) {
-  const bool single_block = std::getenv("GEMPE_SIGMA_SINGLE_BLOCK") != nullptr;  // A/B switch, read per call
-  if (single_block) sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
-  else sigma_update_cluster_kernel<<<kSigmaCtas, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state);
+                        SigmaState* state, std::uint32_t* status, bool single_block, cudaStream_t stream) {
+  if (single_block) sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status);
+  else sigma_update_cluster_kernel<<<kSigmaCtas, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status);
   return 1;
 }
 

@@ -12,7 +12,8 @@ constexpr std::uint32_t kNoHub = 0xffffffffu;
 constexpr std::uint32_t kNotLocal = 0xffffffffu;
 
 // status word layout (device u32[8])
-enum StatusSlot { kStatNonFinite = 0, kStatRetryCap = 1, kStatDrawsLo = 2, kStatDrawsHi = 3, kStatExchangeOverflow = 4 };
+enum StatusSlot { kStatNonFinite = 0, kStatRetryCap = 1, kStatDrawsLo = 2, kStatDrawsHi = 3, kStatExchangeOverflow = 4,
+                  kStatEmptyTallies = 5 };
 
 // Per-round scalars of parabola_impl (sigmoid.hpp:88-101), folded on the host in double:
 //   u = (delta - mu) * inv_sqrt2_sigma,  w = A g^2 + sign B (delta-mu) g,  d = delta + sign C g / w.
@@ -109,6 +110,28 @@ struct PartitionArgs {
 };
 
 
+// One work item of the gather: a vertex, or one slice of a hub's adjacency.  32 bytes, written once per graph build, so
+// an item starts with two 16-byte loads instead of a chain of dependent ones (items -> rowptr -> ...); the four items
+// of a claim share one 128-byte line.
+struct ItemDesc {
+  std::uint32_t u;       // vertex (work id)
+  std::uint32_t off_a;   // first adjacency position of the slice (index into nbr)
+  std::uint32_t len_a;   // adjacency positions in the slice
+  std::uint32_t off_b;   // first own-sample slot (index into neg_own): u*k, or off_a in PER_EDGE_2
+  std::uint32_t len_b;   // own samples taken by this item: k on a vertex's first item (0 on later slices), len_a in PER_EDGE_2
+  std::uint32_t first;   // 1: first item of the vertex -- it also takes the incoming samples (in_off[u] .. in_off[u+1])
+  std::uint32_t hub;     // hub id, kNoHub for an unsplit vertex
+  std::uint32_t sub;     // slice index inside the hub
+};
+static_assert(sizeof(ItemDesc) == 32, "two 16-byte loads per item");
+
+// fp32 view of the FastMath tables for the default (non-PRECISE) kernels, laid out for direct indexing: the ratio table's
+// knots (-1 ... 8) are all multiples of 0.05, so every cell [-1 + 0.05 i, -1 + 0.05 (i+1)) lies inside ONE segment and
+// carries that segment's quadratic {a, b, c}; the erf table's 16 segments are uniform (width 0.375).
+constexpr int kRatioCells = 180;
+constexpr int kErfSegments = 16;
+constexpr int kTableF32Entries = kRatioCells + kErfSegments;  // float4 {a, b, c, 0} each
+
 struct GatherArgs {
   const float* x_cur;
   float* x_next;
@@ -117,12 +140,11 @@ struct GatherArgs {
   int n_peers;
   float* peer_next[kMaxPeers];
   std::uint32_t n, dim, ld;
-  const std::uint32_t* rowptr;     // n+1
   const std::uint32_t* nbr;        // 2m, both directions
   const std::uint32_t* neg_own;
   const std::uint32_t* in_off;     // n+1
   const std::uint32_t* in_anchor;
-  const uint4* items;              // {vertex, first adjacency position, hub id | kNoHub, index inside hub}
+  const ItemDesc* items;
   const std::uint32_t* hub_first;  // first partial slot of hub h
   const std::uint32_t* hub_items;  // number of items of hub h
   std::uint32_t* hub_arrived;      // arrival counters (zero between rounds)
@@ -133,12 +155,10 @@ struct GatherArgs {
   std::uint32_t* work_cursor;      // persistent-warp work queue head (reset before every launch)
   double* cap_y;                   // optional capture (n*dim, n), null when off
   double* cap_z;
-  std::uint32_t chunk_entries;
-  std::uint32_t k;
-  int neg_mode;
   RoundMath math;
   const RoundMath* math_dev;       // non-null: read the round's constants from device memory (device sigma feedback)
-  DeviceTables tab;
+  DeviceTables tab;                // double tables (PRECISE kernels)
+  const float4* tab_f32;           // kTableF32Entries cells in device memory (default kernels), see above
 };
 
 // ---- launchers (all asynchronous on `stream`; return the number of kernels launched) ---------------
@@ -187,9 +207,8 @@ int launch_permute_rows(const float* in, std::uint32_t in_ld, float* out, std::u
                         std::uint32_t n, const std::uint32_t* map, bool scatter, cudaStream_t stream);
 int launch_unpermute_partners(const std::uint32_t* neg_own, const std::uint32_t* eid_role, std::uint64_t slots,
                               std::uint32_t* out, cudaStream_t stream);
-// variant 0: batched kernel (default), 1: v0 row-at-a-time kernel.  precise: reference-exact double pair_distance.
-int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, int variant, bool precise,
-                  cudaStream_t stream);
+// gradient + update of work items [item_lo, item_hi).  precise: reference-exact double pair_distance.
+int launch_gather(const GatherArgs& a, std::uint32_t item_lo, std::uint32_t item_hi, bool precise, cudaStream_t stream);
 // optimize_sigma + growth cap + PE estimate on the device tallies; updates *state (and state->math)
 // pe_sampled (metrics.cpp:166-213): distances of all edges and of samples_per_edge sampled non-edges per edge
 struct PeCollectArgs {
@@ -210,8 +229,10 @@ struct PeCollectArgs {
 int launch_pe_collect(const PeCollectArgs& p, cudaStream_t stream);
 int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigma, bool is_edge, int which, double* total,
                   unsigned long long* valid, cudaStream_t stream);
+// (an empty histogram sets status[kStatEmptyTallies] and leaves the state alone); single_block selects the one-CTA
+// kernel instead of the 8-CTA cluster (A/B switch)
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
-                        SigmaState* state, cudaStream_t stream);
+                        SigmaState* state, std::uint32_t* status, bool single_block, cudaStream_t stream);
 int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,
                        std::uint64_t seed, double stddev, cudaStream_t stream);
 

@@ -119,6 +119,10 @@ class CudaShardOps:
     def sigma_update(self):
         self.ctx.sigma_update_async()
 
+    def status_flags(self) -> torch.Tensor:
+        """The round's status words on the device (int32[8], kernels.hpp StatusSlot), 32 bytes in front of the tallies."""
+        return torch.as_tensor(_DeviceArray(self.ctx.device_tallies() - 32, (8,), "<i4"), device=self.device)
+
     def sigma_state(self):
         self.ctx.sync()  # raises on divergence / retry cap of the round
         return self.ctx.sigma_state()
@@ -205,11 +209,27 @@ class ShardedEngine:
             torch.cuda.current_stream().synchronize()
             dist.barrier(group=self.group)
 
+    _FLAG_SLOTS = (0, 1, 4, 5)  # non-finite, retry cap, exchange overflow, empty tallies (not the draw counter)
+
+    def _share_status(self):
+        """A failure flag raised on one rank (divergence, retry cap, exchange overflow) is raised on all: every rank
+        then throws the same error at its next status check instead of one rank leaving the others in a collective."""
+        if not (self.collective and hasattr(self.ops, "status_flags")):
+            return
+        status = self.ops.status_flags()
+        slots = torch.tensor(self._FLAG_SLOTS, device=status.device)
+        flags = status[slots].clone()
+        if dist.get_backend(self.group) != "nccl":
+            flags = flags.cpu()
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=self.group)
+        status[slots] = flags.to(status.device)
+
     def finish_round(self):
         """Waits for the exchange and returns the job-wide tallies (edge[512], nonedge[512])."""
         ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
         with ctx:
             self._wait_pending()
+            self._share_status()
             t = self.ops.tallies()
             if self.collective:
                 if t.is_cuda and dist.get_backend(self.group) != "nccl":
@@ -230,6 +250,7 @@ class ShardedEngine:
             ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
             with ctx:
                 self._wait_pending()
+                self._share_status()
                 if self.collective:
                     dist.all_reduce(self.ops.tallies_tensor(), op=dist.ReduceOp.SUM, group=self.group)
                 self.ops.sigma_update()

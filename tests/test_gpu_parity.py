@@ -175,9 +175,7 @@ def test_golden_embed_runs(G):
 
 # ------------------------------------------------------------------------------------- per-round parity
 
-KERNELS = {"batched": dict(), "batched_precise": dict(precise_distance=True), "rowwise": dict(kernel_variant=1),
-           "cp_async": dict(kernel_variant=10),  # only differs from the default for 16 < ld <= 128
-           "warp_per_item_small_d": dict(kernel_variant=2)}  # only differs from the default for ld <= 4
+KERNELS = {"batched": dict(), "batched_precise": dict(precise_distance=True)}
 
 
 @pytest.mark.parametrize("kernel", list(KERNELS))

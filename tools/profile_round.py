@@ -1,6 +1,6 @@
 """Small driver for ncu captures: builds a BASELINE configuration and runs a few rounds of the hot path.
 
-    python tools/profile_round.py [--config c4] [--rounds 3] [--neg-mode per_vertex_k] [--precise] [--variant 0]
+    python tools/profile_round.py [--config c4] [--rounds 3] [--neg-mode per_vertex_k] [--precise]
 """
 import argparse
 import os
@@ -16,7 +16,6 @@ ap.add_argument("--config", default="c4")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--neg-mode", default="per_vertex_k")
 ap.add_argument("--precise", action="store_true")
-ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--chunk-entries", type=int, default=0)
 ap.add_argument("--sigma", type=float, default=1.0)
 ap.add_argument("--bucket-mode", type=int, default=0)
@@ -33,7 +32,7 @@ mode = P.NEG_PER_VERTEX_K if a.neg_mode == "per_vertex_k" else P.NEG_PER_EDGE_2
 import time  # noqa: E402
 _t0 = time.perf_counter()
 ctx = P.Context(P.Graph(n, src, dst), dim, 1, neg_mode=mode, negatives=k if mode == P.NEG_PER_VERTEX_K else 0,
-                precise_distance=a.precise, kernel_variant=a.variant, chunk_entries=a.chunk_entries, bucket_mode=a.bucket_mode)
+                precise_distance=a.precise, chunk_entries=a.chunk_entries, bucket_mode=a.bucket_mode)
 print(f'context construction {time.perf_counter() - _t0:.2f} s (n={n}, m={len(src)})')
 ctx.init_coords(P.INIT_UNIFORM_PM1 if init == "uniform_pm1" else P.INIT_NORMAL, 1, std)
 sigma = a.sigma
@@ -49,5 +48,5 @@ for it in range(2, 2 + a.rounds):
     ctx.iterate_async(1.5, sigma, it)
 he, hn = ctx.sync()
 tot, samp, gath = ctx.elapsed_ms()
-print(f"{a.config} variant {a.variant} bucket_mode {a.bucket_mode}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
+print(f"{a.config} bucket_mode {a.bucket_mode}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
       f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
