@@ -426,6 +426,22 @@ def main():
             line["cuda_graph"] = {"rounds_per_graph": reps, "ms_per_step": g_ms, "value": ctx.pair_terms / (g_ms * 1e-3),
                                   "unit": UNIT, "what": "50 rounds captured into one CUDA graph, one launch"}
             ctx.elapsed_ms()
+            # ... and WHOLE iterations (round + sigma search + PE trace / best-PE / convergence bookkeeping on the device)
+            # replayed the same way: what gempe_engine_run queues per host round trip
+            ctx.run_begin(mu, sigma, it + 400, window=1 << 20, tol=0.0, max_rounds=4 * reps)
+            ctx.run_enqueue(reps, reps, True)
+            ctx.run_poll()
+            ge0.record(stream)
+            ctx.run_enqueue(reps, 2 * reps, True)
+            ge1.record(stream)
+            torch.cuda.synchronize()
+            st = ctx.run_poll()
+            assert st["rounds_done"] == 2 * reps
+            r_ms = ge0.elapsed_time(ge1) / reps
+            line["full_iteration_graph"] = {"rounds_per_graph": reps, "ms_per_step": r_ms,
+                                            "value": ctx.pair_terms / (r_ms * 1e-3), "unit": UNIT,
+                                            "what": "50 whole iterations (sigma feedback, PE trace, best-PE snapshot, convergence "
+                                                    "window on the device) as one CUDA graph launch"}
         ctx.close()
         del ctx
 

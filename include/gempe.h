@@ -171,6 +171,37 @@ int gempe_get_sigma_state(gempe_ctx* ctx, double* sigma, double* pe_estimate, do
 int gempe_sigma_update_async(gempe_ctx* ctx);
 void* gempe_device_tallies(gempe_ctx* ctx);
 
+/* ---- Runs queued without host round trips: the loop of EmbeddingEngine::run (src/engine.cpp:349-373) on the device.
+ * gempe_run_begin arms the device-side bookkeeping for a run that starts at the current coordinates: sigma feedback
+ * (src/engine.cpp:293-314), PE / sigma trace of up to max_rounds rounds, best-PE snapshot (:316-319) and the
+ * convergence window (:353-367).  gempe_run_enqueue queues `rounds` whole iterations -- sampling, gradient + update,
+ * sigma search, bookkeeping, snapshot -- that turn into no-ops once `stop_at` rounds of the run are done, the window
+ * criterion holds or a round failed; with use_graph != 0 the sequence is captured once and replayed as ONE CUDA graph
+ * launch (small graphs are launch-bound).  Round r of the run uses the sample streams of iteration first_iter + r.
+ * gempe_run_poll waits for what was queued, moves the context to the coordinates actually reached, returns the traces
+ * (first min(rounds_done, trace_cap) entries) and the last completed round's tallies, and raises the error of a failed
+ * round (non-finite coordinate -> GEMPE_ERR_DIVERGENCE, ...).  Queue -> poll -> queue ...; single-rank contexts only.
+ * gempe_run_best_snapshot: device pointer to the best-PE coordinates (padded rows x row stride, WORK ids of the
+ * moment they were taken; valid when improved_at > 0).  gempe_run_rebase: call after gempe_relabel inside a run. */
+typedef struct gempe_run_status {
+  uint64_t rounds_done;      /* completed rounds of the run */
+  uint64_t improved_at;      /* rounds_done value after the round that set the best PE (0: none yet) */
+  uint64_t draws;            /* LCG draws of the last completed round */
+  double best_pe;
+  double sigma;              /* after the last completed round */
+  double pe_estimate;        /* of the last completed round */
+  double last_nonedge_weight;
+  int32_t converged;
+  int32_t failed;
+} gempe_run_status;
+int gempe_run_begin(gempe_ctx* ctx, double mu, double sigma, uint64_t first_iter, int32_t window, double tol,
+                    uint32_t max_rounds);
+int gempe_run_enqueue(gempe_ctx* ctx, uint32_t rounds, uint64_t stop_at, int32_t use_graph);
+int gempe_run_poll(gempe_ctx* ctx, gempe_run_status* out, double* pe_trace, double* sigma_trace, uint32_t trace_cap,
+                   uint64_t* hist_edge, uint64_t* hist_nonedge);
+void* gempe_run_best_snapshot(gempe_ctx* ctx);
+int gempe_run_rebase(gempe_ctx* ctx);
+
 /* IterationCapture (include/entropy_embed/engine.hpp:92-96): consolidated y (n*dim) and z (n) of the last
  * round, in double.  Capture must be switched on before the round. */
 int gempe_set_capture(gempe_ctx* ctx, int on);
@@ -244,6 +275,39 @@ int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t 
 int gempe_elapsed_ms(gempe_ctx* ctx, float out3[3]);
 uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels launched so far */
 
+/* ---- Several GPUs in ONE process: the C++ multi-GPU host (`devices[], n_devices` of the proposed
+ * constructor).  A group is one context per listed device (a device may be listed more than once: several ranks on one
+ * GPU, used by the tests), vertices sharded contiguously over the ranks, every rank holding the full X_t, CSR and edge
+ * filter.  A round is driven from the calling thread through the ranks' streams and ordered by CUDA events only.  With
+ * peer access between all listed devices the sample records and the updated rows travel as stores of the pack / gather
+ * kernels into the other ranks' memory (NVLink / NVSwitch); otherwise, or with GEMPE_GROUP_COPY_ENGINES, as
+ * cudaMemcpyPeerAsync copies (all-to-all of the packed regions, all-gather of the owned row blocks).  Results are
+ * bit-identical to a single context in deterministic mode.  gempe_options.device / rank / world / comm_chunks / exchange
+ * of `opt` are set per rank by the group.
+ *   gempe_group_iterate       one sharded round, job-wide tallies           (gempe_iterate)
+ *   gempe_group_iterate_auto  round + sigma search on every rank's device from the summed tallies (gempe_iterate_auto)
+ *   gempe_group_relabel       re-relabel on every rank                        (gempe_relabel)
+ *   gempe_group_replicas_agree  1 when all ranks hold bit-identical coordinates (start-up / test check) */
+typedef struct gempe_group gempe_group;
+#define GEMPE_GROUP_COPY_ENGINES 1 /* flags: move records and rows with copy engines even where peer stores would work */
+int gempe_group_create(gempe_group** out, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                       const gempe_options* opt, const int* devices, int n_devices, int flags);
+void gempe_group_destroy(gempe_group* group);
+const char* gempe_group_last_error(const gempe_group* group);   /* NULL: error of a failed gempe_group_create */
+int gempe_group_world(const gempe_group* group);
+gempe_ctx* gempe_group_context(gempe_group* group, int rank);   /* owned by the group */
+const char* gempe_group_exchange_path(const gempe_group* group);
+int gempe_group_set_coords(gempe_group* group, const float* x_work);
+int gempe_group_init_coords(gempe_group* group, int rule, uint64_t seed, double std);
+int gempe_group_get_coords(gempe_group* group, float* x_work);
+int gempe_group_iterate(gempe_group* group, double mu, double sigma, uint64_t iter_index, uint64_t* hist_edge,
+                        uint64_t* hist_nonedge);
+int gempe_group_set_sigma(gempe_group* group, double mu, double sigma);
+int gempe_group_iterate_auto(gempe_group* group, uint64_t iter_index, double* sigma, double* pe_estimate,
+                             double* nonedge_weight, uint64_t* hist_edge, uint64_t* hist_nonedge);
+int gempe_group_relabel(gempe_group* group, uint64_t relabel_seed);
+int gempe_group_replicas_agree(gempe_group* group);
+
 /* ---- host-side numerics of the path (no GPU needed) ------------------------------------------------ */
 /* FastMath::build tables (src/piecewise.cpp:182-195). which: 0 erf, 1 exp_neg, 2 ratio.
  * out67 = knots[17] a[16] b[16] c[16] lo hi.  Returns odd_mirror (0/1) or a negative error. */
@@ -303,6 +367,11 @@ typedef struct gempe_iteration_config { /* IterationConfig, engine.hpp:29-38 */
   int32_t host_sigma;         /* 1 = run the sigma search on the host (hostmath.cpp) instead of the device kernel */
   int32_t deterministic;      /* 1 = sorted sample buckets: byte-identical results run to run (README.md:41-44 of the
                                  reference promises this for fixed input, seed, workers and lanes) */
+  int32_t batch_rounds;       /* gempe_engine_run with the device sigma search queues this many whole iterations per host
+                                 round trip (gempe_run_enqueue / gempe_run_poll; convergence, best-PE snapshot and PE
+                                 trace are kept on the device): 0 = auto (16, replayed as one CUDA graph, for graphs
+                                 below ~4 M pair-terms per round; 4 plain launches above), 1 = poll after every round,
+                                 < 0 = the host loop of round 1 (one gempe_iterate_auto per round) */
 } gempe_iteration_config;
 
 typedef struct gempe_embed_result { /* EmbedResult, engine.hpp:98-107 */

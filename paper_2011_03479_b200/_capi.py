@@ -25,7 +25,8 @@ SYMBOLS = [
     "gempe_hash_bits", "gempe_sample_slots", "gempe_pair_terms", "gempe_algorithmic_bytes",
     "gempe_get_work_graph", "gempe_set_coords", "gempe_get_coords", "gempe_init_coords", "gempe_relabel",
     "gempe_iterate", "gempe_step_host", "gempe_iterate_async", "gempe_graph_capture", "gempe_graph_launch", "gempe_pe_sampled", "gempe_sync", "gempe_set_sigma", "gempe_iterate_auto",
-    "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_set_capture", "gempe_get_yz", "gempe_get_yz_rows", "gempe_get_coords_rows", "gempe_probe",
+    "gempe_iterate_auto_async", "gempe_get_sigma_state", "gempe_sigma_update_async", "gempe_device_tallies", "gempe_run_begin", "gempe_run_enqueue", "gempe_run_poll", "gempe_run_best_snapshot", "gempe_run_rebase",
+    "gempe_set_capture", "gempe_get_yz", "gempe_get_yz_rows", "gempe_get_coords_rows", "gempe_probe",
     "gempe_sample", "gempe_set_stream", "gempe_device_coords", "gempe_row_stride", "gempe_padded_rows",
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_exchange_layout", "gempe_bucket_received", "gempe_gather_chunk", "gempe_coords_ipc_handles", "gempe_open_peer",
     "gempe_add_peer_pointers", "gempe_clear_peers", "gempe_exchange_ipc_handle", "gempe_open_peer_exchange",
@@ -37,12 +38,22 @@ SYMBOLS = [
     "gempe_engine_sigma", "gempe_engine_run_single_iteration", "gempe_engine_run", "gempe_parse_edge_list",
     "gempe_parse_graph_snapshot", "gempe_load_graph_file", "gempe_write_graph_snapshot", "gempe_graph_free",
     "gempe_write_embedding_tsv",
+    "gempe_group_create", "gempe_group_destroy", "gempe_group_last_error", "gempe_group_world", "gempe_group_context",
+    "gempe_group_exchange_path", "gempe_group_set_coords", "gempe_group_init_coords", "gempe_group_get_coords",
+    "gempe_group_iterate", "gempe_group_set_sigma", "gempe_group_iterate_auto", "gempe_group_relabel",
+    "gempe_group_replicas_agree",
 ]
 
 
 class PeReportC(C.Structure):
     _fields_ = [("pe", C.c_double), ("mu_star", C.c_double), ("sigma_star", C.c_double), ("h_basic", C.c_double),
                 ("compression_ratio", C.c_double), ("grid_pe", C.c_double), ("nonedge_samples", C.c_uint64)]
+
+
+class RunStatusC(C.Structure):
+    _fields_ = [("rounds_done", C.c_uint64), ("improved_at", C.c_uint64), ("draws", C.c_uint64), ("best_pe", C.c_double),
+                ("sigma", C.c_double), ("pe_estimate", C.c_double), ("last_nonedge_weight", C.c_double),
+                ("converged", C.c_int32), ("failed", C.c_int32)]
 
 
 class Options(C.Structure):
@@ -57,7 +68,8 @@ class IterationConfigC(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("lane_width", C.c_uint32), ("workers", C.c_uint32),
                 ("convergence_tol", C.c_double), ("convergence_window", C.c_int32), ("relabel_period", C.c_int32),
                 ("fast_math", C.c_int32), ("hash_bits", C.c_int32), ("neg_mode", C.c_int32),
-                ("negatives", C.c_uint32), ("device", C.c_int32), ("host_sigma", C.c_int32), ("deterministic", C.c_int32)]
+                ("negatives", C.c_uint32), ("device", C.c_int32), ("host_sigma", C.c_int32), ("deterministic", C.c_int32),
+                ("batch_rounds", C.c_int32)]
 
 
 class GraphC(C.Structure):
@@ -120,6 +132,25 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_get_sigma_state": (i32, [vp, C.POINTER(dbl), C.POINTER(dbl), C.POINTER(dbl)]),
         "gempe_sigma_update_async": (i32, [vp]),
         "gempe_device_tallies": (vp, [vp]),
+        "gempe_run_begin": (i32, [vp, dbl, dbl, u64, i32, dbl, u32]),
+        "gempe_run_enqueue": (i32, [vp, u32, u64, i32]),
+        "gempe_run_poll": (i32, [vp, C.POINTER(RunStatusC), vp, vp, u32, vp, vp]),
+        "gempe_run_best_snapshot": (vp, [vp]),
+        "gempe_run_rebase": (i32, [vp]),
+        "gempe_group_create": (i32, [C.POINTER(vp), u32, u64, vp, vp, C.POINTER(Options), vp, i32, i32]),
+        "gempe_group_destroy": (None, [vp]),
+        "gempe_group_last_error": (C.c_char_p, [vp]),
+        "gempe_group_world": (i32, [vp]),
+        "gempe_group_context": (vp, [vp, i32]),
+        "gempe_group_exchange_path": (C.c_char_p, [vp]),
+        "gempe_group_set_coords": (i32, [vp, vp]),
+        "gempe_group_init_coords": (i32, [vp, i32, u64, dbl]),
+        "gempe_group_get_coords": (i32, [vp, vp]),
+        "gempe_group_iterate": (i32, [vp, dbl, dbl, u64, vp, vp]),
+        "gempe_group_set_sigma": (i32, [vp, dbl, dbl]),
+        "gempe_group_iterate_auto": (i32, [vp, u64, C.POINTER(dbl), C.POINTER(dbl), C.POINTER(dbl), vp, vp]),
+        "gempe_group_relabel": (i32, [vp, u64]),
+        "gempe_group_replicas_agree": (i32, [vp]),
         "gempe_set_capture": (i32, [vp, i32]),
         "gempe_get_yz": (i32, [vp, vp, vp]),
         "gempe_get_yz_rows": (i32, [vp, vp, u64, vp, vp]),

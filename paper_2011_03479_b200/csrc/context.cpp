@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <exception>
 #include <chrono>
@@ -137,6 +138,7 @@ void host_work_graph(gempe_ctx* c) {
 
 // Builds every graph-derived device structure from the work graph on the device.
 void build_structures(gempe_ctx* c) {
+  ++c->structure_generation;  // captured launch sequences hold pointers into what is rebuilt here
   const std::uint32_t n = c->n;
   const std::uint64_t m = c->m;
 
@@ -439,6 +441,8 @@ SampleArgs sample_args(gempe_ctx* c, std::uint64_t iter) {
   a.rng = c->opt.rng;
   a.stream_base = c->opt.rng == GEMPE_RNG_REFERENCE ? mix_seed(c->opt.seed, iter) : c->opt.seed;
   a.iter = iter;
+  a.seed = c->opt.seed;
+  a.iter_dev = c->run_queued ? &c->run_state.get()->count : nullptr;  // a queued run: the round index lives on the device
   a.csr_src = c->csr_src.get();
   a.eid_role = c->eid_role.get();
   a.hash_words = c->hash_words.get();
@@ -535,6 +539,7 @@ void gather_items(gempe_ctx* c, std::uint32_t item_lo, std::uint32_t item_hi) {
   g.cap_z = c->capture ? c->cap_z.get() : nullptr;
   g.math = c->math;
   g.math_dev = c->use_dev_math ? &c->sigma_state.get()->math : nullptr;
+  g.run = c->run_queued ? c->run_state.get() : nullptr;
   g.tab = c->tables;
   g.tab_f32 = c->tables_f32.get();
   c->launches += launch_gather(g, item_lo, item_hi, c->opt.precise_distance != 0, c->stream);
@@ -597,6 +602,9 @@ using namespace gempe;
 
 gempe_ctx::~gempe_ctx() {
   if (round_graph) cudaGraphExecDestroy(round_graph);
+  for (cudaGraphExec_t g : run_graph) {
+    if (g) cudaGraphExecDestroy(g);
+  }
   for (const ExchangePeer& p : ex_peers) {
     if (p.ipc) cudaIpcCloseMemHandle(p.recv);
   }
@@ -1072,6 +1080,172 @@ int gempe_graph_launch(gempe_ctx* c) {
   });
 }
 
+// ---- runs queued without host round trips (EmbeddingEngine::run, engine.cpp:349-373) --------------------------------
+namespace {
+
+// one whole iteration of a queued run on the stream: round, sigma search + bookkeeping, best-PE snapshot
+void enqueue_run_round(gempe_ctx* c, int parity) {
+  const int saved = c->cur;
+  c->cur = parity;
+  c->use_dev_math = true;
+  c->run_queued = true;
+  try {
+    sampling_passes(c, c->run_first_iter);
+    gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
+    const double pairs = static_cast<double>(static_cast<std::uint64_t>(c->n) * (c->n - 1) / 2);
+    c->launches += launch_sigma_update(c->hist.get(), c->mu_dev, pairs, static_cast<double>(c->m),
+                                       c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->status.get(),
+                                       c->sigma_single_block, c->run_state.get(), c->run_pe_trace.get(),
+                                       c->run_sigma_trace.get(), c->stream);
+    c->launches += launch_snapshot_if_improved(c->x[0].get(), c->x[1].get(), c->run_best_x.get(), c->run_best_x.size(),
+                                               c->run_state.get(), c->stream);
+    cuda_check(cudaGetLastError(), "queued round");
+  } catch (...) {
+    c->use_dev_math = false;
+    c->run_queued = false;
+    c->cur = saved;
+    throw;
+  }
+  c->use_dev_math = false;
+  c->run_queued = false;
+  c->cur = saved;
+}
+
+void drop_run_graphs(gempe_ctx* c) {
+  for (auto& g : c->run_graph) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
+
+}  // namespace
+
+int gempe_run_begin(gempe_ctx* c, double mu, double sigma, std::uint64_t first_iter, std::int32_t window, double tol,
+                    std::uint32_t max_rounds) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (c->opt.world != 1 || (c->pack_path && c->exchange.recv != c->exchange.send)) {
+      throw config_error("queued runs are for single-rank contexts (the tallies of a sharded round need a reduction)");
+    }
+    if (window < 1 || max_rounds < 1) throw config_error("run needs window >= 1 and max_rounds >= 1");
+    if (gempe_set_sigma(c, mu, sigma) != GEMPE_OK) throw config_error(c->error);
+    cuda_check(cudaStreamSynchronize(c->stream), "run begin");
+    c->run_first_iter = first_iter;
+    c->run_state.allocate(1, true);
+    c->run_pe_trace.allocate(max_rounds, true);
+    c->run_sigma_trace.allocate(max_rounds, true);
+    c->run_best_x.allocate(static_cast<std::size_t>(c->n_pad) * c->ld, true);
+    RunState head{};
+    head.best_pe = std::numeric_limits<double>::infinity();
+    head.tol = tol;
+    head.window = window;
+    head.parity_base = c->cur;
+    head.trace_cap = max_rounds;
+    cuda_check(cudaMemcpy(c->run_state.get(), &head, offsetof(RunState, last_hist), cudaMemcpyHostToDevice), "run state");
+    c->run_rounds_seen = 0;
+    c->run_armed = true;
+    drop_run_graphs(c);
+  });
+}
+
+int gempe_run_enqueue(gempe_ctx* c, std::uint32_t rounds, std::uint64_t stop_at, std::int32_t use_graph) {
+  return guarded(c, [&] {
+    require_live(c);
+    if (!c->run_armed) throw config_error("gempe_run_enqueue without gempe_run_begin");
+    if (rounds < 1) throw config_error("enqueue at least one round");
+    // the device skips rounds once `stop_at` are done; the coordinates' parity follows the rounds actually done, so the
+    // host learns it at the next poll -- until then nothing else may be queued on this context
+    if (c->run_in_flight) throw config_error("poll the queued rounds (gempe_run_poll) before queueing more");
+    cuda_check(cudaMemcpyAsync(&c->run_state.get()->stop_at, &stop_at, sizeof stop_at, cudaMemcpyHostToDevice, c->stream),
+               "stop_at");
+    const int parity = c->cur;
+    if (use_graph) {
+      if (c->run_graph_generation != c->structure_generation || c->run_graph_rounds != rounds) {
+        drop_run_graphs(c);
+        c->run_graph_generation = c->structure_generation;
+        c->run_graph_rounds = rounds;
+      }
+      if (!c->run_graph[parity]) {
+        const std::uint64_t launches0 = c->launches;
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+          for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1);
+        } catch (...) {
+          cudaStreamEndCapture(c->stream, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        cuda_check(cudaStreamEndCapture(c->stream, &graph), "end capture");
+        c->run_graph_launches = c->launches - launches0;
+        c->launches = launches0;
+        const cudaError_t inst = cudaGraphInstantiate(&c->run_graph[parity], graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(inst, "graph instantiate");
+      }
+      cuda_check(cudaGraphLaunch(c->run_graph[parity], c->stream), "graph launch");
+      c->launches += c->run_graph_launches;
+    } else {
+      for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1);
+    }
+    c->run_in_flight = true;
+  });
+}
+
+int gempe_run_poll(gempe_ctx* c, gempe_run_status* out, double* pe_trace, double* sigma_trace, std::uint32_t trace_cap,
+                   std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
+  return guarded(c, [&] {
+    if (!c->run_armed) throw config_error("gempe_run_poll without gempe_run_begin");
+    RunState head{};
+    cuda_check(cudaMemcpyAsync(&head, c->run_state.get(), offsetof(RunState, last_hist), cudaMemcpyDeviceToHost, c->stream),
+               "run state D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "queued rounds");
+    c->run_in_flight = false;
+    c->cur = static_cast<int>((head.parity_base + head.count) & 1ull);
+    c->round_iter = c->run_first_iter + (head.count ? head.count - 1 : 0);
+    c->last_draws = head.draws;
+    SigmaState st{};
+    cuda_check(cudaMemcpy(&st, c->sigma_state.get(), sizeof st, cudaMemcpyDeviceToHost), "sigma D2H");
+    const std::uint64_t have = std::min<std::uint64_t>(head.count, head.trace_cap);
+    const std::uint64_t copy = std::min<std::uint64_t>(have, trace_cap);
+    if (pe_trace && copy) cuda_check(cudaMemcpy(pe_trace, c->run_pe_trace.get(), copy * sizeof(double), cudaMemcpyDeviceToHost), "trace");
+    if (sigma_trace && copy) cuda_check(cudaMemcpy(sigma_trace, c->run_sigma_trace.get(), copy * sizeof(double), cudaMemcpyDeviceToHost), "trace");
+    if (hist_edge) cuda_check(cudaMemcpy(hist_edge, &c->run_state.get()->last_hist[0], kBins * sizeof(std::uint64_t), cudaMemcpyDeviceToHost), "tallies");
+    if (hist_nonedge) cuda_check(cudaMemcpy(hist_nonedge, &c->run_state.get()->last_hist[kBins], kBins * sizeof(std::uint64_t), cudaMemcpyDeviceToHost), "tallies");
+    if (out) {
+      out->rounds_done = head.count;
+      out->converged = head.converged;
+      out->failed = head.failed;
+      out->improved_at = head.improved_at;
+      out->best_pe = head.best_pe;
+      out->sigma = st.sigma;
+      out->pe_estimate = st.pe_estimate;
+      out->last_nonedge_weight = head.last_nonedge_weight;
+      out->draws = head.draws;
+    }
+    if (head.failed) {
+      const std::uint32_t* s = head.sticky_status;
+      if (s[kStatRetryCap]) throw near_complete_graph_error("no non-edge partner found after 10^4 draws; graph is near-complete");
+      if (s[kStatExchangeOverflow]) throw data_error("sample exchange region overflowed");
+      if (s[kStatEmptyTallies]) throw config_error("cannot optimize sigma on an empty histogram");
+      throw divergence_error("non-finite coordinate after update", static_cast<int>(c->run_first_iter + head.fail_iter) + 1);
+    }
+  });
+}
+
+void* gempe_run_best_snapshot(gempe_ctx* c) { return c->run_best_x.get(); }
+
+int gempe_run_rebase(gempe_ctx* c) {
+  // after the coordinates moved to the other buffer outside a round (gempe_relabel): the parity relation of the run
+  return guarded(c, [&] {
+    if (!c->run_armed || c->run_in_flight) throw config_error("no idle run to rebase");
+    RunState head{};
+    cuda_check(cudaMemcpy(&head, c->run_state.get(), offsetof(RunState, last_hist), cudaMemcpyDeviceToHost), "run state D2H");
+    const int base = static_cast<int>((static_cast<unsigned long long>(c->cur) + head.count) & 1ull);
+    cuda_check(cudaMemcpy(&c->run_state.get()->parity_base, &base, sizeof base, cudaMemcpyHostToDevice), "parity base");
+  });
+}
+
 int gempe_sync(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
   return guarded(c, [&] { fetch_status(c, hist_edge, hist_nonedge); });
 }
@@ -1101,7 +1275,8 @@ int gempe_sigma_update_async(gempe_ctx* c) {
     const double pairs = static_cast<double>(static_cast<std::uint64_t>(c->n) * (c->n - 1) / 2);
     c->launches += launch_sigma_update(c->hist.get(), c->mu_dev, pairs, static_cast<double>(c->m),
                                        c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->status.get(),
-                                       c->sigma_single_block, c->stream);
+                                       c->sigma_single_block, c->run_queued ? c->run_state.get() : nullptr,
+                                       c->run_pe_trace.get(), c->run_sigma_trace.get(), c->stream);
     cuda_check(cudaGetLastError(), "sigma update");
   });
 }

@@ -97,6 +97,16 @@ struct gempe_ctx {
   cudaGraphExec_t round_graph = nullptr;
   int graph_rounds = 0, graph_start_parity = 0;
   std::uint64_t graph_launches_per_replay = 0, graph_last_iter = 0;
+  // a run queued without host round trips (gempe_run_begin / enqueue / poll): device bookkeeping, traces, best-PE snapshot
+  gempe::DeviceBuffer<gempe::RunState> run_state;
+  gempe::DeviceBuffer<double> run_pe_trace, run_sigma_trace;
+  gempe::DeviceBuffer<float> run_best_x;
+  cudaGraphExec_t run_graph[2] = {nullptr, nullptr};  // by the parity of the coordinate buffers at the first round
+  std::uint64_t run_graph_generation = 0, run_graph_launches = 0, run_first_iter = 0, run_rounds_seen = 0;
+  std::uint32_t run_graph_rounds = 0;
+  std::uint64_t structure_generation = 0;  // bumped by every (re)build of the graph-derived structures
+  bool run_armed = false, run_in_flight = false;
+  bool run_queued = false;  // while a queued round's launches are being issued: kernels get the run state
   bool pack_path = false;       // sampling goes through sample_pack + bucket_records (opt.exchange, or bucket_mode 3)
   bool bucket_pending = false;  // records packed, gempe_bucket_received not yet called
   // fused update + broadcast: X buffers (both parities, indexed like x[]) of the other ranks, in this rank's address space

@@ -24,6 +24,7 @@ struct gempe_engine {
   Tallies last_hist;
   bool have_hist = false;
   bool sigma_seeded = false;
+  bool queued_converged = false, queued_best = false;  // outcome of a run queued on the device (run_queued)
   double best_pe = std::numeric_limits<double>::infinity();
   DeviceBuffer<float> best_x;               // device snapshot, WORK indexing of the moment it was taken
   std::vector<std::uint32_t> best_to_work;
@@ -120,6 +121,50 @@ void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {
   if (sigma_out) *sigma_out = e->sigma;
 }
 
+// EmbeddingEngine::run (engine.cpp:349-373) with the loop on the device: whole iterations are queued in batches, the
+// device keeps the PE trace, the best-PE snapshot and the convergence window, the host looks every `batch` rounds (and at
+// every re-relabel boundary, which needs the host).  Returns false when the run has to fall back to the host loop.
+bool run_queued(gempe_engine* e, int batch, bool use_graph) {
+  gempe_ctx* c = e->ctx;
+  const int max_iters = e->cfg.max_iters;
+  if (e->iter != 0 || max_iters <= 0) return false;  // a run that continues manual steps keeps the host loop
+  const std::uint32_t max_rounds = static_cast<std::uint32_t>(max_iters);
+  rethrow(c, gempe_run_begin(c, e->mu, e->sigma, 0, e->cfg.convergence_window, e->cfg.convergence_tol, max_rounds));
+  e->sigma_seeded = true;
+  const int period = e->cfg.relabel_period;
+  gempe_run_status st{};
+  std::uint64_t improved_seen = 0;
+  std::vector<double> trace(max_rounds);
+  while (true) {
+    std::uint64_t stop_at = max_rounds;
+    if (period > 0) stop_at = std::min<std::uint64_t>(stop_at, (static_cast<std::uint64_t>(e->iter) / period + 1) * period);
+    const std::uint64_t todo = stop_at - static_cast<std::uint64_t>(e->iter);
+    // a graph always replays `batch` rounds (the surplus ones are no-ops); plain launches queue only what is left
+    const std::uint32_t rounds = use_graph ? static_cast<std::uint32_t>(batch)
+                                           : static_cast<std::uint32_t>(std::min<std::uint64_t>(batch, todo));
+    rethrow(c, gempe_run_enqueue(c, rounds, stop_at, use_graph ? 1 : 0));
+    rethrow(c, gempe_run_poll(c, &st, trace.data(), nullptr, max_rounds, e->last_hist.edge.data(), e->last_hist.nonedge.data()));
+    e->iter = static_cast<int>(st.rounds_done);
+    if (st.improved_at != improved_seen) {  // the snapshot on the device was taken under the current relabelling
+      improved_seen = st.improved_at;
+      e->best_to_work = c->to_work;
+    }
+    if (st.converged || e->iter >= max_iters) break;
+    if (period > 0 && e->iter > 0 && e->iter % period == 0) {  // engine.cpp:281-283
+      rethrow(c, gempe_relabel(c, mix_seed(mix_seed(e->seed, 0xA11BE11), static_cast<std::uint64_t>(e->iter))));
+      rethrow(c, gempe_run_rebase(c));
+    }
+  }
+  e->pe_trace.assign(trace.begin(), trace.begin() + e->iter);
+  e->sigma = st.sigma;
+  e->best_pe = st.best_pe;
+  e->last_hist.nonedge_weight = st.last_nonedge_weight;
+  e->have_hist = e->iter > 0;
+  e->queued_converged = st.converged != 0;
+  e->queued_best = st.improved_at > 0;
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -139,6 +184,7 @@ void gempe_default_iteration_config(gempe_iteration_config* cfg) {
   cfg->device = 0;
   cfg->host_sigma = 0;
   cfg->deterministic = 0;
+  cfg->batch_rounds = 0;
 }
 
 int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
@@ -204,10 +250,25 @@ int gempe_engine_run(gempe_engine* e, gempe_embed_result* r) {
       if (r->relabel_forward) std::copy(c->to_work.begin(), c->to_work.end(), r->relabel_forward);
       return;
     }
+    // device sigma search: the whole loop runs on the device, the host looks every few rounds
+    bool queued = false;
+    if (!e->cfg.host_sigma && e->cfg.batch_rounds >= 0) {
+      const bool small = gempe_pair_terms(c) < 4000000ull;  // launch-bound rounds: replay them as one CUDA graph
+      const int batch = e->cfg.batch_rounds > 0 ? e->cfg.batch_rounds : (small ? 16 : 4);
+      queued = run_queued(e, batch, small && batch > 1);
+    }
+    if (queued) {
+      r->converged = e->queued_converged ? 1 : 0;
+      if (!r->converged && e->queued_best) {
+        map_back(e, static_cast<const float*>(gempe_run_best_snapshot(c)), e->best_to_work, r->embedding);
+      } else {
+        map_back(e, c->x[c->cur].get(), c->to_work, r->embedding);
+      }
+    }
     // converged when the last `window` rounds brought no new PE minimum beating the earlier best by tol
     // (engine.cpp:353-367)
     const int window = e->cfg.convergence_window;
-    while (e->iter < e->cfg.max_iters) {
+    while (!queued && e->iter < e->cfg.max_iters) {
       single_iteration(e, nullptr, nullptr);
       const int k = static_cast<int>(e->pe_trace.size());
       if (k > window) {
@@ -219,7 +280,9 @@ int gempe_engine_run(gempe_engine* e, gempe_embed_result* r) {
         }
       }
     }
-    if (!r->converged && e->best_x.size()) {
+    if (queued) {
+      // exported above
+    } else if (!r->converged && e->best_x.size()) {
       map_back(e, e->best_x.get(), e->best_to_work, r->embedding);
     } else {
       map_back(e, c->x[c->cur].get(), c->to_work, r->embedding);

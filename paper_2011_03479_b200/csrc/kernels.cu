@@ -176,8 +176,11 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
     unit = anchor;
     draw = t - static_cast<std::uint64_t>(anchor) * a.k;
   }
+  // the round's index may live on the device (a queued run): the stream base follows it
+  const std::uint64_t iter = a.iter + (a.iter_dev ? static_cast<std::uint64_t>(*a.iter_dev) : 0ull);
+  const std::uint64_t stream_base = a.iter_dev ? (a.rng == 0 ? mix(a.seed, iter) : a.seed) : a.stream_base;
   if (a.rng == 0) {
-    std::uint32_t s = static_cast<std::uint32_t>(mix(mix(a.stream_base, unit), draw) >> 16);
+    std::uint32_t s = static_cast<std::uint32_t>(mix(mix(stream_base, unit), draw) >> 16);
     for (int tries = 0; tries < kMaxRetries; ++tries) {
       s = s * kLcgMul + 1u;
       ++draws;
@@ -190,8 +193,8 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
     const std::uint64_t slot = a.neg_mode == 0 ? ((unit << 1) | draw) : t;
     for (int tries = 0; tries < kMaxRetries; tries += 4) {
       std::uint32_t ctr[4] = {static_cast<std::uint32_t>(slot), static_cast<std::uint32_t>(slot >> 32),
-                              static_cast<std::uint32_t>(tries >> 2), static_cast<std::uint32_t>(a.iter)};
-      philox4x32(ctr, static_cast<std::uint32_t>(a.stream_base), static_cast<std::uint32_t>(a.stream_base >> 32));
+                              static_cast<std::uint32_t>(tries >> 2), static_cast<std::uint32_t>(iter)};
+      philox4x32(ctr, static_cast<std::uint32_t>(stream_base), static_cast<std::uint32_t>(stream_base >> 32));
       for (int q = 0; q < 4; ++q) {
         ++draws;
         const std::uint32_t g = static_cast<std::uint32_t>((static_cast<std::uint64_t>(ctr[q]) * a.n) >> 32);
@@ -902,10 +905,14 @@ __device__ __forceinline__ double shfl_xor_f64(double v, int off) {
 // ids are fetched two batches ahead; the rows of the next batch are pulled into L2 with
 // prefetch.global.L2 while the current batch is being computed.
 //
-// Register slot t of lane r does NOT hold entry t but entry t ^ (r / REP): with that lane-dependent order the transposed
-// reduction needs no selects (at the step with lane distance `off` a lane keeps slots [0, half) and receives its partner's
-// slots [half, 2 half), which are the SAME rows), every lane ends up owning the entry whose id it fetched itself, and both
-// the row ids and the coefficients travel by butterfly shuffles with immediate lane masks (t * REP).
+// Lane (grp, r) fetches the id of entry grp*TB + r/REP of a batch, which is also the entry it owns after the reduction;
+// ids and coefficients travel by sub-group shuffles (width LPR) with immediate source lanes.  Slot t of every lane of a
+// group holds the SAME row (entry grp*TB + t), so one load instruction reads whole 128-byte lines of G rows.  (A
+// lane-dependent slot order makes the reduction select-free, but then one load instruction touches TB different rows
+// with 32 bytes each: measured 10.5 ms instead of 4.6 ms on c4, profiles/r02_gather_permuted_slots.md.)  The shape that
+// minimises shuffles and selects is FEW lanes per row: LPR = 8 at d = 128 (a lane holds four 16-byte vectors of a row,
+// 128 bytes apart), four rows per group -- 4 id shuffles, 4 coefficient shuffles and a 4 -> 1 transposed reduction per
+// batch of 16 rows, instead of 16 / 16 / 16 -> 1 with one warp per row.
 //
 // PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation), double
 //                  parabola chain.
@@ -938,6 +945,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
   constexpr int LINES = ROW_BYTES_MAX >= 128 ? ROW_BYTES_MAX / 128 : 1;  // 128-byte lines per row
   constexpr bool kPrefetch = ROW_BYTES_MAX >= 128 && U == 1;
   using red_t = typename std::conditional<PRECISE, double, float>::type;
+  if (a.run && run_stopped(a.run)) return;  // a queued round after the run has stopped
   __shared__ unsigned int sh_hist[2 * kBins];
   using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
   __shared__ tab_t sh_tab;
@@ -1021,13 +1029,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       fetch(E * U, nxt);
 
       for (std::uint32_t base = 0; base < total; base += E * U) {
-        // TB rows per lane group and sub-batch, all loads issued before any use; slot t = entry mine ^ t
+        // TB rows per lane group and sub-batch, all loads issued before any use; slot t = entry grp*TB + t
         float xv[U][TB][NV][VEC];
 #pragma unroll
         for (int s = 0; s < U; ++s) {
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const std::uint32_t src_row = t == 0 ? cur[s] : __shfl_xor_sync(kFull, cur[s], t * REP);
+            const std::uint32_t src_row = __shfl_sync(kFull, cur[s], t * REP, LPR);
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (!FULL) {
@@ -1092,16 +1100,21 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
             }
           }
           {
-            // select-free transposed reduction: slot i of this lane and slot i + half of the lane `off` away hold
-            // partial sums of the same row (see the slot order above)
+            // transposed (recursive-halving) reduction: at lane distance `off` the lower lane keeps the first half of the
+            // rows and takes the partner's partial sums of them, the upper lane the second half
             int width = TB;
 #pragma unroll
             for (int off = LPR / 2; off >= 1; off >>= 1) {
               if (width > 1) {
                 const int half = width / 2;
+                const bool upper = (r & off) != 0;
 #pragma unroll
                 for (int i = 0; i < TB / 2; ++i) {
-                  if (i < half) p[i] += __shfl_xor_sync(kFull, p[i + half], off);
+                  if (i < half) {
+                    const red_t keep = upper ? p[i + half] : p[i];
+                    const red_t give = upper ? p[i] : p[i + half];
+                    p[i] = keep + __shfl_xor_sync(kFull, give, off);
+                  }
                 }
                 width = half;
               } else {
@@ -1169,7 +1182,7 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           // y += wf (sf - 1) (x_u - x_v) from the resident differences
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const float ct = t == 0 ? coef : __shfl_xor_sync(kFull, coef, t * REP);  // coefficient of entry mine ^ t
+            const float ct = __shfl_sync(kFull, coef, t * REP, LPR);  // coefficient of entry grp*TB + t
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               if constexpr (VEC % 2 == 0) {
@@ -1193,20 +1206,60 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
         }
       }
 
-      // cross-group reduction in double (the reference consolidates replicas in double, engine.cpp:88-107);
-      // y_u = z_u x_u + sum of the weighted differences
-      double ys[NV][VEC];
+      // Consolidation (the reference sums its replicas in double, engine.cpp:88-107) and the update, spread over the
+      // WHOLE warp: vector j of the row is finalised by lane group j % G, so every lane handles JF = ceil(NV / G) vectors
+      // instead of group 0 handling all NV.  The groups' fp32 partial sums (and the own row) change hands through shared
+      // memory; y_u = z_u x_u + sum of the weighted differences.
+      constexpr int JF = (NV + G - 1) / G;
       double zs = static_cast<double>(zacc);
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) zs += shfl_xor_f64(zs, off);
+      double ys[JF][VEC];
+      float xo[JF][VEC];
+      bool fin[JF];
+      std::uint32_t fcol[JF];
+      if constexpr (G == 1) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
+        for (int j = 0; j < NV; ++j) {
+          fin[j] = act[j];
+          fcol[j] = static_cast<std::uint32_t>((r + LPR * j) * VEC);
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          double t = static_cast<double>(y[j][c]);
+          for (int c = 0; c < VEC; ++c) {
+            xo[j][c] = xu[j][c];
+            ys[j][c] = fma(zs, static_cast<double>(xu[j][c]), static_cast<double>(y[j][c]));
+          }
+        }
+      } else {
+        static_assert(G == 1 || VEC == 4, "the exchange moves 16-byte vectors");
+        __shared__ float4 sh_part[THREADS / 32][G][NV * LPR];
+        __shared__ float4 sh_own[THREADS / 32][NV * LPR];
+        const int w = threadIdx.x >> 5;
+        __syncwarp();  // the previous item's readers are done
 #pragma unroll
-          for (int off = LPR; off < 32; off <<= 1) t += shfl_xor_f64(t, off);
-          ys[j][c] = fma(zs, static_cast<double>(xu[j][c]), t);
+        for (int j = 0; j < NV; ++j) {
+          sh_part[w][grp][j * LPR + r] = make_float4(y[j][0], y[j][1], y[j][2], y[j][3]);
+          if (grp == 0) sh_own[w][j * LPR + r] = make_float4(xu[j][0], xu[j][1], xu[j][2], xu[j][3]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int jj = 0; jj < JF; ++jj) {
+          const int j = grp + jj * G;
+          fcol[jj] = static_cast<std::uint32_t>((r + LPR * j) * VEC);
+          fin[jj] = j < NV && (FULL || fcol[jj] < ld);
+          const int at = (j < NV ? j : 0) * LPR + r;
+          double sum[VEC] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float4 v = sh_part[w][g][at];
+            sum[0] += static_cast<double>(v.x);
+            sum[1] += static_cast<double>(v.y);
+            sum[2] += static_cast<double>(v.z);
+            sum[3] += static_cast<double>(v.w);
+          }
+          const float4 own = sh_own[w][at];
+          xo[jj][0] = own.x; xo[jj][1] = own.y; xo[jj][2] = own.z; xo[jj][3] = own.w;
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) ys[jj][c] = fma(zs, static_cast<double>(xo[jj][c]), sum[c]);
         }
       }
 
@@ -1214,15 +1267,13 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       if (hub != kNoHub) {
         const std::uint32_t p0 = __ldg(a.hub_first + hub), q = __ldg(a.hub_items + hub);
         const std::uint32_t slot = p0 + d1.w;
-        if (grp == 0) {
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            if (!act[j]) continue;
+        for (int jj = 0; jj < JF; ++jj) {
+          if (!fin[jj]) continue;
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + (r + LPR * j) * VEC + c] = ys[j][c];
-          }
-          if (r == 0) a.part_z[slot] = zs;
+          for (int c = 0; c < VEC; ++c) a.part_y[static_cast<std::size_t>(slot) * ld + fcol[jj] + c] = ys[jj][c];
         }
+        if (lane == 0) a.part_z[slot] = zs;
         __threadfence();
         __syncwarp();
         std::uint32_t arrived = 0;
@@ -1233,46 +1284,48 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
           __threadfence();
           zs = 0.0;
 #pragma unroll
-          for (int j = 0; j < NV; ++j)
+          for (int jj = 0; jj < JF; ++jj)
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) ys[j][c] = 0.0;
+            for (int c = 0; c < VEC; ++c) ys[jj][c] = 0.0;
           for (std::uint32_t sl = p0; sl < p0 + q; ++sl) {
             zs += __ldcg(a.part_z + sl);
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-              if (!act[j]) continue;
+            for (int jj = 0; jj < JF; ++jj) {
+              if (!fin[jj]) continue;
 #pragma unroll
-              for (int c = 0; c < VEC; ++c) ys[j][c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + (r + LPR * j) * VEC + c);
+              for (int c = 0; c < VEC; ++c) ys[jj][c] += __ldcg(a.part_y + static_cast<std::size_t>(sl) * ld + fcol[jj] + c);
             }
           }
           if (lane == 0) a.hub_arrived[hub] = 0;
         }
       }
 
-      if (finalize && grp == 0) {
-        // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z)
+      if (finalize) {
+        // reduce_and_update (engine.cpp:261-272): z <= 0 holds position, else x = float(y / z) -- as y * (1 / z) in
+        // double, one division per item (the quotient differs from y / z by at most one double ulp before the rounding
+        // to float)
         bool bad = false;
+        const double inv_z = zs > 0.0 ? 1.0 / zs : 0.0;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          if (!act[j]) continue;
+        for (int jj = 0; jj < JF; ++jj) {
+          if (!fin[jj]) continue;
           float out[VEC];
 #pragma unroll
           for (int c = 0; c < VEC; ++c) {
-            out[c] = xu[j][c];
+            out[c] = xo[jj][c];
             if (zs > 0.0) {
-              out[c] = static_cast<float>(ys[j][c] / zs);
+              out[c] = static_cast<float>(ys[jj][c] * inv_z);
               bad |= !isfinite(out[c]);
             }
           }
-          const std::uint32_t col = (r + LPR * j) * VEC;
-          store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld + col, out);
+          store_row_everywhere<VEC>(a, static_cast<std::size_t>(u) * ld + fcol[jj], out);
           if (a.cap_y) {
 #pragma unroll
             for (int c = 0; c < VEC; ++c)
-              if (col + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + col + c] = ys[j][c];
+              if (fcol[jj] + c < a.dim) a.cap_y[static_cast<std::size_t>(u) * a.dim + fcol[jj] + c] = ys[jj][c];
           }
         }
-        if (a.cap_z && r == 0) a.cap_z[u] = zs;
+        if (a.cap_z && lane == 0) a.cap_z[u] = zs;
         if (bad) atomicOr(a.status + kStatNonFinite, 1u);
       }
     }
@@ -1299,6 +1352,7 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
 #define GEMPE_INFLIGHT 4
 #endif
   constexpr int kInflight = GEMPE_INFLIGHT;
+  if (a.run && run_stopped(a.run)) return;  // a queued round after the run has stopped
   __shared__ unsigned int sh_hist[2 * kBins];
   using tab_t = typename std::conditional<PRECISE, SmemTables, SmemTablesF>::type;
   __shared__ tab_t sh_tab;
@@ -1490,6 +1544,48 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
+// Run bookkeeping after a completed round (one block; see RunState): PE / sigma trace, best PE, the convergence window of
+// EmbeddingEngine::run (engine.cpp:353-367: the last `window` rounds brought no minimum beating the earlier best by
+// tol), failure flags, the round's tallies.
+__device__ __forceinline__ void record_round(RunState* run, double* pe_trace, double* sigma_trace, double pe, double sigma_new,
+                                             double nonedge_weight, const std::uint32_t* status,
+                                             const unsigned long long* hist) {
+  for (int i = threadIdx.x; i < 2 * kBins; i += blockDim.x) run->last_hist[i] = hist[i];
+  if (threadIdx.x != 0) return;
+  const unsigned long long k = run->count;
+  std::uint32_t bad = 0;
+  for (int i = 0; i < 8; ++i) {
+    const std::uint32_t w = status[i];
+    if (i == kStatDrawsLo || i == kStatDrawsHi) continue;
+    run->sticky_status[i] |= w;
+    bad |= w;
+  }
+  run->draws = static_cast<unsigned long long>(status[kStatDrawsLo]) | (static_cast<unsigned long long>(status[kStatDrawsHi]) << 32);
+  run->last_nonedge_weight = nonedge_weight;
+  if (k < run->trace_cap) {
+    pe_trace[k] = pe;
+    sigma_trace[k] = sigma_new;
+  }
+  if (pe < run->best_pe) {
+    run->best_pe = pe;
+    run->improved_at = k + 1;
+  }
+  const unsigned long long have = k + 1;
+  const unsigned long long window = static_cast<unsigned long long>(run->window);
+  if (have > window && have <= run->trace_cap) {
+    double best_before = pe_trace[0], best_recent = pe_trace[have - window];
+    for (unsigned long long i = 1; i < have - window; ++i) best_before = fmin(best_before, pe_trace[i]);
+    for (unsigned long long i = have - window + 1; i < have; ++i) best_recent = fmin(best_recent, pe_trace[i]);
+    if (best_before - best_recent < run->tol * fabs(best_before)) run->converged = 1;
+  }
+  if (bad && !run->failed) {
+    run->failed = 1;
+    run->fail_iter = k;
+  }
+  __threadfence();
+  run->count = have;
+}
+
 }  // namespace sigma
 
 // ---------------------------------------------------------------------------------- quality scoring: pe_sampled
@@ -1592,8 +1688,10 @@ __global__ void __launch_bounds__(kThreads) pe_sum_kernel(const float* __restric
 __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long long* __restrict__ hist, double mu,
                                                              double pairs, double edges, int exact_math,
                                                              SigmaState* __restrict__ state,
-                                                             std::uint32_t* __restrict__ status) {
+                                                             std::uint32_t* __restrict__ status, RunState* run,
+                                                             double* pe_trace, double* sigma_trace) {
   using namespace sigma;
+  if (run && run_stopped(run)) return;  // a queued round after the run has stopped
   __shared__ double scratch[kBins / 32];
   const int b = threadIdx.x;
   const double ec = static_cast<double>(hist[b]), nc = static_cast<double>(hist[kBins + b]);
@@ -1601,6 +1699,10 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
   const double samples = block_sum(nc, scratch);
   if (block_sum(ec, scratch) + samples == 0.0) {  // optimize_sigma on an empty histogram is a config_error (slope.cpp:76)
     if (b == 0) atomicOr(status + kStatEmptyTallies, 1u);
+    if (run) {
+      __syncthreads();
+      record_round(run, pe_trace, sigma_trace, 0.0, state->sigma, 1.0, status, hist);
+    }
     return;  // sigma stays what it was
   }
   const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;  // engine.cpp:296-300
@@ -1689,6 +1791,7 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
     state->math.C = c2 / sigma_new;
     state->math.exact = exact_math;
   }
+  if (run) record_round(run, pe_trace, sigma_trace, pe, sigma_new, nw, status, hist);
 }
 
 // The same search on a cluster of 8 CTAs (8 SMs): one evaluation of the objective is bound by the FP64 throughput of
@@ -1700,9 +1803,13 @@ __global__ void __launch_bounds__(kBins) sigma_update_kernel(const unsigned long
 constexpr int kSigmaCtas = 8;
 __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
     sigma_update_cluster_kernel(const unsigned long long* __restrict__ hist, double mu, double pairs, double edges,
-                                int exact_math, SigmaState* __restrict__ state, std::uint32_t* __restrict__ status) {
+                                int exact_math, SigmaState* __restrict__ state, std::uint32_t* __restrict__ status,
+                                RunState* run, double* pe_trace, double* sigma_trace) {
   using namespace sigma;
   namespace cg = cooperative_groups;
+  // a queued round after the run has stopped: every CTA sees the same state (it only changes at the very end of this
+  // kernel, after the last cluster.sync), so the whole cluster leaves together
+  if (run && run_stopped(run)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int cta = static_cast<int>(cluster.block_rank());
   __shared__ double scratch[kBins / 32];
@@ -1717,6 +1824,10 @@ __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
   cluster.sync();
   if (empty) {  // optimize_sigma on an empty histogram is a config_error (slope.cpp:76); sigma stays what it was
     if (cta == 0 && b == 0) atomicOr(status + kStatEmptyTallies, 1u);
+    if (cta == 0 && run) {
+      __syncthreads();
+      record_round(run, pe_trace, sigma_trace, 0.0, state->sigma, 1.0, status, hist);
+    }
     return;
   }
   const double nw = samples > 0.0 ? (pairs - edges) / samples : 1.0;
@@ -1839,6 +1950,31 @@ __global__ void __cluster_dims__(kSigmaCtas, 1, 1) __launch_bounds__(kBins)
     state->math.C = c2 / sigma_new;
     state->math.exact = exact_math;
   }
+  if (cta == 0 && run) record_round(run, pe_trace, sigma_trace, pe_sum / pairs, sigma_new, nw, status, hist);
+}
+
+// best-PE snapshot (engine.cpp:316-319) without the host: see launch_snapshot_if_improved
+__global__ void __launch_bounds__(kThreads) snapshot_if_improved_kernel(const float4* __restrict__ x0,
+                                                                        const float4* __restrict__ x1,
+                                                                        float4* __restrict__ dst, std::size_t floats,
+                                                                        const RunState* __restrict__ run) {
+  const unsigned long long count = run->count;
+  if (run->improved_at != count) return;
+  const float4* src = ((run->parity_base + count) & 1ull) ? x1 : x0;
+  const std::size_t count4 = floats / 4, stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  const std::size_t t = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (std::size_t i = t; i < count4; i += stride) dst[i] = src[i];
+  if (t < floats % 4) {  // tail of a buffer whose length is not a multiple of four floats (d <= 2)
+    reinterpret_cast<float*>(dst)[4 * count4 + t] = reinterpret_cast<const float*>(src)[4 * count4 + t];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) sum_tallies_kernel(const TallySources srcs, unsigned long long* __restrict__ dst) {
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= 2 * kBins) return;
+  unsigned long long total = 0;
+  for (int r = 0; r < srcs.count; ++r) total += srcs.hist[r][i];
+  dst[i] = total;
 }
 
 __global__ void __launch_bounds__(kThreads) permute_rows_kernel(const float* __restrict__ in, std::uint32_t in_ld,
@@ -2172,7 +2308,16 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool 
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);  // 8 rows per group, 32 warps/SM
-  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);  // 16 rows/warp, 20 warps/SM (96 regs)
+#ifndef GEMPE_D128_ROW_LANES
+#define GEMPE_D128_ROW_LANES 8
+#endif
+#if GEMPE_D128_ROW_LANES == 32  // one warp per row (round 1)
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);
+#elif GEMPE_D128_ROW_LANES == 16
+  else if (ld <= 128) gather_batched_go<16, 2, 4, 8, 1, 128, 5>(a, lo, hi, precise, stream);
+#else  // 8 lanes per row, 4 rows per group, 16 rows per warp and batch; own row + accumulator take 32 registers: 16 warps/SM
+  else if (ld <= 128) gather_batched_go<8, 4, 4, 4, 1, 128, 4>(a, lo, hi, precise, stream);
+#endif
   // wider rows: 64 row registers per lane as well (8 / 4 rows per batch), 16 warps/SM (d = 256: -19 %, d = 512: -10 %
   // against 4 / 2 rows in 256-thread blocks)
   else if (ld <= 192) gather_batched_go<16, 3, 4, 8, 1, 128, 4>(a, lo, hi, precise, stream);  // 2 half-warps x 8 rows
@@ -2200,9 +2345,27 @@ int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigm
 }
 
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
-                        SigmaState* state, std::uint32_t* status, bool single_block, cudaStream_t stream) {
-  if (single_block) sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status);
-  else sigma_update_cluster_kernel<<<kSigmaCtas, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status);
+                        SigmaState* state, std::uint32_t* status, bool single_block, RunState* run, double* pe_trace,
+                        double* sigma_trace, cudaStream_t stream) {
+  if (single_block) {
+    sigma_update_kernel<<<1, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status, run, pe_trace, sigma_trace);
+  } else {
+    sigma_update_cluster_kernel<<<kSigmaCtas, kBins, 0, stream>>>(hist, mu, pairs, edges, exact_math, state, status, run,
+                                                                  pe_trace, sigma_trace);
+  }
+  return 1;
+}
+
+int launch_sum_tallies(const TallySources& srcs, unsigned long long* dst, cudaStream_t stream) {
+  sum_tallies_kernel<<<blocks_for(2 * kBins, kThreads), kThreads, 0, stream>>>(srcs, dst);
+  return 1;
+}
+
+int launch_snapshot_if_improved(const float* x0, const float* x1, float* dst, std::size_t floats, const RunState* run,
+                                cudaStream_t stream) {
+  if (floats == 0) return 0;
+  snapshot_if_improved_kernel<<<capped_blocks(floats / 4 + 1, kThreads, 8), kThreads, 0, stream>>>(
+      reinterpret_cast<const float4*>(x0), reinterpret_cast<const float4*>(x1), reinterpret_cast<float4*>(dst), floats, run);
   return 1;
 }
 

@@ -36,6 +36,35 @@ struct SigmaState {
   RoundMath math;  // folded constants of `sigma` for the next round's gather
 };
 
+// Device-resident bookkeeping of a run of iterations queued without host round trips (EmbeddingEngine::run,
+// engine.cpp:349-373): the sigma kernel of every completed round appends the PE estimate, tracks the best PE and evaluates
+// the convergence window; a round whose turn comes after the run has stopped (converged, failed, or `stop_at` rounds
+// done) does nothing.  One instance per context, read back by the host every few rounds.
+struct RunState {
+  unsigned long long count;        // rounds completed == PE values recorded == index of the next round's sample streams
+  unsigned long long stop_at;      // rounds with count >= stop_at are skipped (max_iters / relabel boundary / batch end)
+  unsigned long long fail_iter;    // round that raised the first failure flag
+  unsigned long long draws;        // LCG draws of the last completed round
+  double best_pe;                  // minimum of the trace so far (engine.cpp:316-319)
+  double tol;                      // convergence_tol
+  int window;                      // convergence_window
+  int converged;                   // engine.cpp:353-367 held after some round
+  int failed;                      // a completed round left a failure flag in sticky_status
+  int parity_base;                 // the current coordinates are buffer (parity_base + count) & 1
+  unsigned long long improved_at;  // value of `count` after the latest round that set a new PE minimum (0: none yet)
+  std::uint32_t sticky_status[8];  // OR of the rounds' status words
+  std::uint32_t trace_cap;         // capacity of pe_trace / sigma_trace
+  std::uint32_t pad;
+  double last_nonedge_weight;      // of the last completed round
+  unsigned long long last_hist[2 * kBins];  // tallies of the last completed round
+};
+// true when the round whose kernels read this must not run
+#if defined(__CUDACC__)
+__device__ __forceinline__ bool run_stopped(const RunState* r) {
+  return r->converged || r->failed || r->count >= r->stop_at;
+}
+#endif
+
 // knots[17] a[16] b[16] c[16] per table (the lo/hi clamps are the first/last knot).
 struct DeviceTables {
   double erf[65];
@@ -58,6 +87,10 @@ struct SampleArgs {
   int rng;                        // 0 reference replay, 1 philox
   std::uint64_t stream_base;      // mix(seed, iter)  (reference) / seed (philox)
   std::uint64_t iter;
+  // iteration index on the device (RunState::count): when non-null the round's index is iter + *iter_dev and the
+  // stream base is derived from `seed` in the kernel, so one captured launch sequence serves every round
+  std::uint64_t seed;
+  const unsigned long long* iter_dev;
   const std::uint32_t* csr_src;   // PER_EDGE_2: anchor of each CSR position
   const std::uint32_t* eid_role;  // PER_EDGE_2: 2*edge + role (role 0: anchor is src[e], 1: dst[e])
   const std::uint32_t* hash_words;  // bit-packed direct-mapped table, 2^bits bits
@@ -157,6 +190,7 @@ struct GatherArgs {
   double* cap_z;
   RoundMath math;
   const RoundMath* math_dev;       // non-null: read the round's constants from device memory (device sigma feedback)
+  const RunState* run;             // non-null: the launch does nothing once the run has stopped
   DeviceTables tab;                // double tables (PRECISE kernels)
   const float4* tab_f32;           // kTableF32Entries cells in device memory (default kernels), see above
 };
@@ -231,8 +265,21 @@ int launch_pe_sum(const float* dist, std::uint64_t count, double mu, double sigm
                   unsigned long long* valid, cudaStream_t stream);
 // (an empty histogram sets status[kStatEmptyTallies] and leaves the state alone); single_block selects the one-CTA
 // kernel instead of the 8-CTA cluster (A/B switch)
+// run / pe_trace / sigma_trace (optional): device-side run bookkeeping, see RunState
 int launch_sigma_update(const unsigned long long* hist, double mu, double pairs, double edges, int exact_math,
-                        SigmaState* state, std::uint32_t* status, bool single_block, cudaStream_t stream);
+                        SigmaState* state, std::uint32_t* status, bool single_block, RunState* run, double* pe_trace,
+                        double* sigma_trace, cudaStream_t stream);
+// best-PE snapshot on the device (engine.cpp:316-319): when the latest completed round set a new PE minimum, copies the
+// current coordinates -- buffer (parity_base + count) & 1 of {x0, x1} -- to dst.  `floats` is a multiple of 4.
+int launch_snapshot_if_improved(const float* x0, const float* x1, float* dst, std::size_t floats, const RunState* run,
+                                cudaStream_t stream);
+// job-wide tallies of a sharded round inside one process: dst[i] = sum over `count` ranks of srcs[r][i] (2*kBins counters;
+// the sources are the ranks' device tallies, peer memory included)
+struct TallySources {
+  const unsigned long long* hist[kMaxPeers + 1];
+  int count;
+};
+int launch_sum_tallies(const TallySources& srcs, unsigned long long* dst, cudaStream_t stream);
 int launch_init_coords(float* x, std::uint32_t n, std::uint32_t dim, std::uint32_t ld, int rule,
                        std::uint64_t seed, double stddev, cudaStream_t stream);
 

@@ -88,6 +88,7 @@ class IterationConfig:
     device: int = 0
     host_sigma: bool = False  # True: sigma search on the host instead of the device kernel
     deterministic: bool = False  # True: sorted sample buckets, byte-identical results run to run
+    batch_rounds: int = 0  # run(): whole iterations queued per host round trip (0 auto, 1 every round, < 0 host loop)
 
 
 @dataclass
@@ -262,6 +263,30 @@ class Context:
         self._check(self._L.gempe_pe_sampled(self._h, samples_per_edge, seed, C.byref(rep)))
         return {name: getattr(rep, name) for name, _ in rep._fields_}
 
+    # -- runs queued without host round trips ----------------------------------------------------------
+    def run_begin(self, mu: float, sigma: float, first_iter: int = 0, window: int = 5, tol: float = 1e-4,
+                  max_rounds: int = 100):
+        self._run_cap = int(max_rounds)
+        self._check(self._L.gempe_run_begin(self._h, mu, sigma, first_iter, window, tol, max_rounds))
+
+    def run_enqueue(self, rounds: int, stop_at: int, use_graph: bool = True):
+        self._check(self._L.gempe_run_enqueue(self._h, rounds, stop_at, int(use_graph)))
+
+    def run_poll(self) -> dict:
+        """Waits for the queued rounds; dict(rounds_done, converged, failed, improved_at, best_pe, sigma, pe_estimate,
+        last_nonedge_weight, draws, pe_trace, sigma_trace, hist_edge, hist_nonedge)."""
+        st = _capi.RunStatusC()
+        pe = np.zeros(self._run_cap, np.float64)
+        sg = np.zeros(self._run_cap, np.float64)
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        self._check(self._L.gempe_run_poll(self._h, C.byref(st), _capi.ptr(pe), _capi.ptr(sg), self._run_cap, _capi.ptr(he),
+                                           _capi.ptr(hn)))
+        out = {name: getattr(st, name) for name, _ in st._fields_}
+        k = min(int(st.rounds_done), self._run_cap)
+        out.update(pe_trace=pe[:k], sigma_trace=sg[:k], hist_edge=he, hist_nonedge=hn)
+        return out
+
     def graph_capture(self, mu: float, sigma: float, first_iter: int, count: int):
         """Captures `count` rounds into a CUDA graph (replayed by graph_launch)."""
         self._check(self._L.gempe_graph_capture(self._h, mu, sigma, first_iter, count))
@@ -392,6 +417,96 @@ class Context:
         self._check(self._L.gempe_end_round(self._h))
 
 
+class Group:
+    """Several GPUs in one process (gempe_group): one context per listed device, vertices sharded over them.  A device
+    may be listed more than once (several ranks on one GPU: what the tests use)."""
+
+    GROUP_COPY_ENGINES = 1
+
+    def __init__(self, g: Graph, dim: int, seed: int = 1, *, devices=(0,), copy_engines=False, neg_mode=NEG_PER_EDGE_2,
+                 negatives=0, math=MATH_TABLES, rng=RNG_REFERENCE, hash_bits=0, relabel=True, chunk_entries=0,
+                 deterministic=False, precise_distance=False, bucket_mode=0):
+        self._L = _capi.load()
+        self._h = C.c_void_p()
+        opt = _capi.Options()
+        self._L.gempe_default_options(C.byref(opt))
+        opt.dim, opt.seed, opt.neg_mode, opt.negatives = dim, seed, neg_mode, negatives
+        opt.math, opt.rng, opt.hash_bits, opt.relabel = math, rng, hash_bits or 0, int(relabel)
+        opt.chunk_entries, opt.deterministic = chunk_entries, int(deterministic)
+        opt.precise_distance, opt.bucket_mode = int(precise_distance), bucket_mode
+        self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
+        dev = (C.c_int * len(devices))(*[int(d) for d in devices])
+        rc = self._L.gempe_group_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), C.byref(opt),
+                                        C.cast(dev, C.c_void_p), len(devices),
+                                        self.GROUP_COPY_ENGINES if copy_engines else 0)
+        if rc != _capi.OK:
+            self._h = C.c_void_p()
+            _raise(rc, self._L.gempe_group_last_error(None).decode())
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._L.gempe_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != _capi.OK:
+            _raise(rc, self._L.gempe_group_last_error(self._h).decode())
+
+    @property
+    def world(self) -> int:
+        return self._L.gempe_group_world(self._h)
+
+    @property
+    def exchange_path(self) -> str:
+        return self._L.gempe_group_exchange_path(self._h).decode()
+
+    def set_coords(self, x_work: np.ndarray):
+        x = np.ascontiguousarray(x_work, np.float32)
+        if x.shape != (self.n, self.dim):
+            raise ConfigError(f"coordinates must be {self.n}x{self.dim}")
+        self._check(self._L.gempe_group_set_coords(self._h, _capi.ptr(x)))
+
+    def init_coords(self, rule=INIT_REFERENCE, seed=1, std=0.01):
+        self._check(self._L.gempe_group_init_coords(self._h, rule, seed, std))
+
+    def get_coords(self) -> np.ndarray:
+        out = np.empty((self.n, self.dim), np.float32)
+        self._check(self._L.gempe_group_get_coords(self._h, _capi.ptr(out)))
+        return out
+
+    def iterate(self, mu: float, sigma: float, iter_index: int):
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        self._check(self._L.gempe_group_iterate(self._h, mu, sigma, iter_index, _capi.ptr(he), _capi.ptr(hn)))
+        return he, hn
+
+    def set_sigma(self, mu: float, sigma: float):
+        self._check(self._L.gempe_group_set_sigma(self._h, mu, sigma))
+
+    def iterate_auto(self, iter_index: int):
+        he = np.zeros(HIST_BINS, np.uint64)
+        hn = np.zeros(HIST_BINS, np.uint64)
+        s, pe, nw = C.c_double(), C.c_double(), C.c_double()
+        self._check(self._L.gempe_group_iterate_auto(self._h, iter_index, C.byref(s), C.byref(pe), C.byref(nw),
+                                                     _capi.ptr(he), _capi.ptr(hn)))
+        return s.value, pe.value, nw.value, he, hn
+
+    def relabel(self, relabel_seed: int):
+        self._check(self._L.gempe_group_relabel(self._h, relabel_seed))
+
+    def replicas_agree(self) -> bool:
+        rc = self._L.gempe_group_replicas_agree(self._h)
+        if rc < 0:
+            _raise(-rc, self._L.gempe_group_last_error(self._h).decode())
+        return rc == 1
+
+
 class EmbeddingEngine:
     """engine.hpp:112-134 (run-level facade, gempe_engine)."""
 
@@ -409,6 +524,7 @@ class EmbeddingEngine:
         c.neg_mode, c.negatives, c.device = cfg.neg_mode, cfg.negatives, cfg.device
         c.host_sigma = int(cfg.host_sigma)
         c.deterministic = int(cfg.deterministic)
+        c.batch_rounds = int(cfg.batch_rounds)
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         self._pe_trace = []
         rc = self._L.gempe_engine_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,

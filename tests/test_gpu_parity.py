@@ -749,3 +749,70 @@ def test_many_rounds_async_then_sync_matches_stepwise(G):
     assert a.kernel_launches > 12 * 5
     a.close()
     b.close()
+
+
+# ------------------------------------------------------------------------------------- runs queued on the device
+
+def _stepwise_run(G, g, dim, cfg, seed):
+    """EmbeddingEngine::run driven from the host, one round trip per iteration (the round-1 loop)."""
+    from dataclasses import replace
+    return G.embed(g, dim, replace(cfg, batch_rounds=-1), seed)
+
+
+@pytest.mark.parametrize("batch", [1, 3, 16])
+def test_queued_run_is_bit_identical_to_the_stepwise_loop(G, batch):
+    """gempe_engine_run with the loop on the device (sigma feedback, PE trace, best-PE snapshot, convergence window; 16
+    rounds per CUDA-graph replay) against the host loop: same PE trace, sigma, iteration count, outcome and embedding,
+    bit for bit (deterministic bucket order)."""
+    cases = [(er_graph(600, 3000, 8), 2, dict(max_iters=37)),                      # stops at max_iters: best snapshot
+             (er_graph(300, 900, 3), 3, dict(max_iters=400, convergence_tol=5e-3)),  # converges mid-batch
+             (star_plus_ring(400, hubs=2), 8, dict(max_iters=20, neg_mode=1, negatives=6)),
+             (er_graph(500, 2500, 4), 2, dict(max_iters=23, relabel_period=5))]      # host work at relabel boundaries
+    for (n, src, dst), dim, kw in cases:
+        cfg = G.IterationConfig(deterministic=True, **kw)
+        g = G.Graph(n, src, dst)
+        want = _stepwise_run(G, g, dim, cfg, 5)
+        from dataclasses import replace
+        got = G.embed(g, dim, replace(cfg, batch_rounds=batch), 5)
+        assert got.iterations == want.iterations and got.converged == want.converged
+        assert np.array_equal(got.pe_trace, want.pe_trace)
+        assert got.final_sigma == want.final_sigma and got.last_nonedge_weight == want.last_nonedge_weight
+        assert np.array_equal(got.last_hist_edge, want.last_hist_edge)
+        assert np.array_equal(got.last_hist_nonedge, want.last_hist_nonedge)
+        assert np.array_equal(got.relabel_forward, want.relabel_forward)
+        assert np.array_equal(got.embedding.view(np.uint32), want.embedding.view(np.uint32))
+    assert any(True for _ in cases)
+
+
+def test_queued_run_hooks_directly(G):
+    """gempe_run_begin / enqueue / poll: rounds past stop_at are no-ops, the context lands on the coordinates reached,
+    and a failing round (non-finite coordinates) surfaces as DivergenceError at the poll."""
+    n, src, dst = er_graph(800, 4000, 6)
+    ref = G.Context(G.Graph(n, src, dst), 4, 9, deterministic=True)
+    ref.set_sigma(1.5, 1.0)
+    trace = [ref.iterate_auto(it)[:2] for it in range(7)]
+    for use_graph in (False, True):
+        ctx = G.Context(G.Graph(n, src, dst), 4, 9, deterministic=True)
+        ctx.run_begin(1.5, 1.0, 0, window=50, tol=0.0, max_rounds=64)
+        ctx.run_enqueue(5, 3, use_graph)       # only 3 of the 5 queued rounds may run
+        st = ctx.run_poll()
+        assert st["rounds_done"] == 3 and not st["converged"]
+        ctx.run_enqueue(5, 7, use_graph)       # 4 more
+        st = ctx.run_poll()
+        assert st["rounds_done"] == 7
+        assert st["pe_trace"].tolist() == [pe for _, pe in trace]
+        assert st["sigma_trace"].tolist() == [s for s, _ in trace]
+        assert st["best_pe"] == min(pe for _, pe in trace)
+        assert np.array_equal(ctx.get_coords().view(np.uint32), ref.get_coords().view(np.uint32))
+        assert st["hist_edge"].sum() == len(src) and st["hist_nonedge"].sum() == 2 * len(src)
+        ctx.close()
+    ref.close()
+    ctx = G.Context(G.Graph(n, src, dst), 4, 9)
+    x = ctx.get_coords()
+    x[5, 1] = np.inf
+    ctx.set_coords(x)
+    ctx.run_begin(1.5, 1.0, 0, max_rounds=8)
+    ctx.run_enqueue(4, 8, False)
+    with pytest.raises(G.DivergenceError):
+        ctx.run_poll()
+    ctx.close()
