@@ -71,7 +71,11 @@ typedef struct gempe_options {
   int32_t bucket_mode;    /* incoming-sample bucketing: 0 = auto, 1 = per-partner atomics + scan + scatter,
                              2 = two-level counting sort (streaming traffic only),
                              3 = one radix pass by contiguous vertex range, then per-partner atomics range by range
-                                 (auto for n >= 2^22 on one rank) */
+                                 (auto for n >= 2^22 on one rank),
+                             4 = slotted buckets: S/n + 6 sigma + 8 slots per vertex, the sampler places each anchor at
+                                 its arrival rank itself (no scan, no scatter pass; overflow goes to an indexed spill
+                                 list).  Auto on one rank while the slot array fits L2 (<= 48 MB), unless `deterministic`
+                                 (sorted buckets: mode 1) */
   int32_t exchange;       /* sharded sampling: 0 = every rank enumerates all sample streams and keeps the partners it
                              owns (no exchange step); 1 = a rank samples only the streams of its own anchors, packs
                              (partner, anchor) records per destination rank and the ranks exchange them with one
@@ -393,6 +397,11 @@ void gempe_default_iteration_config(gempe_iteration_config* cfg);
 int gempe_engine_create(gempe_engine** out, uint32_t n, uint64_t m, const uint32_t* src,
                         const uint32_t* dst, uint32_t dim, const gempe_iteration_config* cfg,
                         uint64_t seed);
+/* The same engine sharded over several GPUs of this process (`devices[], n_devices` of SURVEY.md 8b; a gempe_group
+ * inside): n_devices <= 1 is gempe_engine_create on devices[0] / cfg->device.  gempe_engine_context returns rank 0. */
+int gempe_engine_create_multi(gempe_engine** out, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                              uint32_t dim, const gempe_iteration_config* cfg, uint64_t seed, const int* devices,
+                              int n_devices);
 void gempe_engine_destroy(gempe_engine* e);
 const char* gempe_engine_last_error(const gempe_engine* e);
 gempe_ctx* gempe_engine_context(gempe_engine* e);                   /* borrowed */

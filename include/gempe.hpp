@@ -125,6 +125,7 @@ struct IterationConfig {
   std::uint32_t negatives_per_vertex = 0;  // > 0: BASELINE sampling, k draws per vertex instead of 2 per edge
   int device = 0;
   bool deterministic = false;
+  std::vector<int> devices;  // more than one entry: vertices sharded over these GPUs of the process (gempe_group)
 };
 
 struct IterationStats {
@@ -172,7 +173,9 @@ class EmbeddingEngine {
     c.negatives = cfg.negatives_per_vertex;
     c.device = cfg.device;
     c.deterministic = cfg.deterministic ? 1 : 0;
-    const int rc = gempe_engine_create(&handle_, g.n, g.edge_count(), g.src.data(), g.dst.data(), dim, &c, seed);
+    const int rc = gempe_engine_create_multi(&handle_, g.n, g.edge_count(), g.src.data(), g.dst.data(), dim, &c, seed,
+                                             cfg.devices.empty() ? nullptr : cfg.devices.data(),
+                                             static_cast<int>(cfg.devices.size()));
     detail::check(rc, gempe_last_error(nullptr));  // two statements: the message must be read AFTER the call
   }
   ~EmbeddingEngine() { gempe_engine_destroy(handle_); }

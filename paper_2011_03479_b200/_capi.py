@@ -33,7 +33,7 @@ SYMBOLS = [
     "gempe_add_peer_exchange_pointer", "gempe_exchange_recv_area", "gempe_device_coords_parity", "gempe_coords_parity", "gempe_end_round", "gempe_elapsed_ms",
     "gempe_kernel_launches", "gempe_host_fastmath_table", "gempe_host_optimize_sigma",
     "gempe_host_histogram_objective", "gempe_host_histogram_objective_dsigma", "gempe_host_random_relabel",
-    "gempe_host_mix_seed", "gempe_default_iteration_config", "gempe_engine_create", "gempe_engine_destroy",
+    "gempe_host_mix_seed", "gempe_default_iteration_config", "gempe_engine_create", "gempe_engine_create_multi", "gempe_engine_destroy",
     "gempe_engine_last_error", "gempe_engine_context", "gempe_engine_degenerate", "gempe_engine_iteration",
     "gempe_engine_sigma", "gempe_engine_run_single_iteration", "gempe_engine_run", "gempe_parse_edge_list",
     "gempe_parse_graph_snapshot", "gempe_load_graph_file", "gempe_write_graph_snapshot", "gempe_graph_free",
@@ -191,6 +191,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_host_mix_seed": (u64, [u64, u64]),
         "gempe_default_iteration_config": (None, [C.POINTER(IterationConfigC)]),
         "gempe_engine_create": (i32, [C.POINTER(vp), u32, u64, vp, vp, u32, C.POINTER(IterationConfigC), u64]),
+        "gempe_engine_create_multi": (i32, [C.POINTER(vp), u32, u64, vp, vp, u32, C.POINTER(IterationConfigC), u64, vp, i32]),
         "gempe_engine_destroy": (None, [vp]),
         "gempe_engine_last_error": (C.c_char_p, [vp]),
         "gempe_engine_context": (vp, [vp]),

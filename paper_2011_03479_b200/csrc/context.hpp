@@ -84,6 +84,10 @@ struct gempe_ctx {
   gempe::DeviceBuffer<std::uint32_t> tmp_src, tmp_dst;  // the work edge arrays (work ids, input edge order)
   gempe::DeviceBuffer<std::uint32_t> hash_words, hash_summary;
   gempe::DeviceBuffer<std::uint32_t> neg_own, in_cnt, in_off, in_rank, in_anchor, scan_scratch;
+  // slotted buckets (bucket_mode 4): slots per vertex in in_anchor (0 = off), and the overflow side
+  std::uint32_t in_stride = 0;
+  gempe::DeviceBuffer<uint2> spill;
+  gempe::DeviceBuffer<std::uint32_t> spill_cnt, spill_off, spill_anchor;
   // large-n bucketing (two-level counting sort); partition.buckets == 0 selects the atomic method
   gempe::PartitionArgs partition{};
   gempe::DeviceBuffer<std::uint32_t> block_hist, bucket_off;

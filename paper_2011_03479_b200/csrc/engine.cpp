@@ -13,7 +13,8 @@
 using namespace gempe;
 
 struct gempe_engine {
-  gempe_ctx* ctx = nullptr;
+  gempe_ctx* ctx = nullptr;      // the engine's context; rank 0 of `group` (and owned by it) when the engine is sharded
+  gempe_group* group = nullptr;  // several GPUs (gempe_engine_create_multi)
   gempe_iteration_config cfg{};
   std::uint64_t seed = 0;
   std::uint32_t n = 0, dim = 0;
@@ -30,7 +31,10 @@ struct gempe_engine {
   std::vector<std::uint32_t> best_to_work;
   std::string error;
 
-  ~gempe_engine() { gempe_destroy(ctx); }
+  ~gempe_engine() {
+    if (group) gempe_group_destroy(group);
+    else gempe_destroy(ctx);
+  }
 };
 
 namespace {
@@ -55,9 +59,16 @@ int guarded(gempe_engine* e, Fn&& fn) {
   }
 }
 
+void rethrow_message(int rc, const std::string& msg);
 void rethrow(gempe_ctx* c, int rc) {
   if (rc == GEMPE_OK) return;
-  const std::string msg = gempe_last_error(c);
+  rethrow_message(rc, gempe_last_error(c));
+}
+void rethrow(gempe_group* g, int rc) {
+  if (rc == GEMPE_OK) return;
+  rethrow_message(rc, gempe_group_last_error(g));
+}
+void rethrow_message(int rc, const std::string& msg) {
   switch (rc) {
     case GEMPE_ERR_CONFIG: throw config_error(msg);
     case GEMPE_ERR_DIVERGENCE: throw divergence_error(msg, 0);
@@ -84,13 +95,20 @@ void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {
   gempe_ctx* c = e->ctx;
   if (c->degenerate) throw config_error("cannot iterate a degenerate graph");
   if (e->cfg.relabel_period > 0 && e->iter > 0 && e->iter % e->cfg.relabel_period == 0) {  // engine.cpp:281-283
-    rethrow(c, gempe_relabel(c, mix_seed(mix_seed(e->seed, 0xA11BE11), static_cast<std::uint64_t>(e->iter))));
+    const std::uint64_t relabel_seed = mix_seed(mix_seed(e->seed, 0xA11BE11), static_cast<std::uint64_t>(e->iter));
+    if (e->group) rethrow(e->group, gempe_group_relabel(e->group, relabel_seed));
+    else rethrow(c, gempe_relabel(c, relabel_seed));
   }
   Tallies t;
   double pe = 0.0;
   const std::uint64_t pairs = static_cast<std::uint64_t>(e->n) * (e->n > 0 ? e->n - 1 : 0) / 2;
   if (e->cfg.host_sigma) {
-    rethrow(c, gempe_iterate(c, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(), t.nonedge.data()));
+    if (e->group) {
+      rethrow(e->group, gempe_group_iterate(e->group, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(),
+                                            t.nonedge.data()));
+    } else {
+      rethrow(c, gempe_iterate(c, e->mu, e->sigma, static_cast<std::uint64_t>(e->iter), t.edge.data(), t.nonedge.data()));
+    }
     const std::uint64_t samples = t.nonedge_total();
     t.nonedge_weight = samples > 0 ? static_cast<double>(pairs - e->m) / static_cast<double>(samples) : 1.0;
     // growth-capped sigma update (engine.cpp:302-307)
@@ -99,11 +117,17 @@ void single_iteration(gempe_engine* e, double* pe_out, double* sigma_out) {
   } else {
     // sigma search, growth cap and PE estimate on the device (sigma_update_kernel)
     if (!e->sigma_seeded) {
-      rethrow(c, gempe_set_sigma(c, e->mu, e->sigma));
+      if (e->group) rethrow(e->group, gempe_group_set_sigma(e->group, e->mu, e->sigma));
+      else rethrow(c, gempe_set_sigma(c, e->mu, e->sigma));
       e->sigma_seeded = true;
     }
-    rethrow(c, gempe_iterate_auto(c, static_cast<std::uint64_t>(e->iter), &e->sigma, &pe, &t.nonedge_weight,
-                                  t.edge.data(), t.nonedge.data()));
+    if (e->group) {  // every rank searches sigma on its own device from the summed tallies
+      rethrow(e->group, gempe_group_iterate_auto(e->group, static_cast<std::uint64_t>(e->iter), &e->sigma, &pe,
+                                                 &t.nonedge_weight, t.edge.data(), t.nonedge.data()));
+    } else {
+      rethrow(c, gempe_iterate_auto(c, static_cast<std::uint64_t>(e->iter), &e->sigma, &pe, &t.nonedge_weight,
+                                    t.edge.data(), t.nonedge.data()));
+    }
   }
   e->pe_trace.push_back(pe);
   e->last_hist = t;
@@ -190,7 +214,13 @@ void gempe_default_iteration_config(gempe_iteration_config* cfg) {
 int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
                         const std::uint32_t* dst, std::uint32_t dim, const gempe_iteration_config* cfg,
                         std::uint64_t seed) {
-  if (!out || !cfg) return GEMPE_ERR_CONFIG;
+  return gempe_engine_create_multi(out, n, m, src, dst, dim, cfg, seed, nullptr, 0);
+}
+
+int gempe_engine_create_multi(gempe_engine** out, std::uint32_t n, std::uint64_t m, const std::uint32_t* src,
+                              const std::uint32_t* dst, std::uint32_t dim, const gempe_iteration_config* cfg,
+                              std::uint64_t seed, const int* devices, int n_devices) {
+  if (!out || !cfg || (n_devices > 0 && !devices)) return GEMPE_ERR_CONFIG;
   *out = nullptr;
   auto e = std::make_unique<gempe_engine>();
   e->cfg = *cfg;
@@ -213,7 +243,14 @@ int gempe_engine_create(gempe_engine** out, std::uint32_t n, std::uint64_t m, co
   opt.device = cfg->device;
   opt.deterministic = cfg->deterministic;
   int rc = GEMPE_ERR_CONFIG;
-  if (!bad) rc = gempe_create(&e->ctx, n, m, src, dst, &opt);
+  if (!bad && n_devices > 1) {  // vertices sharded over the listed devices, one rank each (group.cpp)
+    rc = gempe_group_create(&e->group, n, m, src, dst, &opt, devices, n_devices, 0);
+    if (rc == GEMPE_OK) e->ctx = gempe_group_context(e->group, 0);
+    else set_create_error(gempe_group_last_error(nullptr));
+  } else if (!bad) {
+    if (n_devices == 1) opt.device = devices[0];
+    rc = gempe_create(&e->ctx, n, m, src, dst, &opt);
+  }
   if (bad) set_create_error(bad);
   if (bad || rc != GEMPE_OK) return rc;  // message: gempe_last_error(NULL)
   *out = e.release();
@@ -252,7 +289,7 @@ int gempe_engine_run(gempe_engine* e, gempe_embed_result* r) {
     }
     // device sigma search: the whole loop runs on the device, the host looks every few rounds
     bool queued = false;
-    if (!e->cfg.host_sigma && e->cfg.batch_rounds >= 0) {
+    if (!e->cfg.host_sigma && e->cfg.batch_rounds >= 0 && !e->group) {
       const bool small = gempe_pair_terms(c) < 4000000ull;  // launch-bound rounds: replay them as one CUDA graph
       const int batch = e->cfg.batch_rounds > 0 ? e->cfg.batch_rounds : (small ? 16 : 4);
       queued = run_queued(e, batch, small && batch > 1);

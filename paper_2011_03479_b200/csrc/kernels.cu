@@ -232,9 +232,73 @@ __global__ void __launch_bounds__(kThreads, 8) sample_kernel(const SampleArgs a)
     std::uint32_t anchor;
     const std::uint32_t partner = sample_slot(a, t, anchor, draws);
     a.neg_own[t] = partner;
-    a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
+    if (a.in_stride) {  // slotted buckets: the arrival rank is the slot
+      if (is_local(a.own, partner)) {
+        const std::uint32_t rank = atomicAdd(a.in_cnt + partner, 1u);
+        if (rank < a.in_stride) {
+          a.in_anchor[static_cast<std::size_t>(partner) * a.in_stride + rank] = anchor;
+        } else {
+          const std::uint32_t at = atomicAdd(a.spill_count, 1u);
+          if (at < a.spill_capacity) a.spill[at] = make_uint2(partner, anchor);
+          else atomicOr(a.status + kStatExchangeOverflow, 1u);
+        }
+      }
+    } else {
+      a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
+    }
   }
   add_draws(a, draws);
+}
+
+// Slotted buckets, overflow side (rare: a partner drew more samples than its slots hold).  ONE block: leaves at once when
+// nothing spilled; otherwise counts the spilled records per partner, scans the n counters with a running carry and
+// groups the anchors by partner -- O(n + spill) work for one SM, the price of a round that overflowed.
+__global__ void __launch_bounds__(1024) spill_index_kernel(const SpillIndexArgs a) {
+  const std::uint32_t count = min(*a.spill_count, a.spill_capacity);
+  if (count == 0) return;
+  __shared__ std::uint32_t warp_tot[32];
+  __shared__ std::uint32_t carry;
+  for (std::uint32_t i = threadIdx.x; i < count; i += 1024) atomicAdd(a.cnt + a.spill[i].x, 1u);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (std::uint32_t base = 0; base < a.n; base += 1024) {
+    const std::uint32_t i = base + threadIdx.x;
+    const std::uint32_t v = i < a.n ? a.cnt[i] : 0u;
+    std::uint32_t inc = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, inc, off);
+      if (lane >= off) inc += o;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const std::uint32_t w = warp_tot[lane];
+      std::uint32_t winc = w;
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, winc, off);
+        if (lane >= off) winc += o;
+      }
+      warp_tot[lane] = winc - w;
+    }
+    __syncthreads();
+    const std::uint32_t excl = carry + warp_tot[warp] + inc - v;
+    if (i < a.n) {
+      a.off[i] = excl;
+      a.cnt[i] = 0;  // becomes the placement cursor below, and is zero again afterwards
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.off[a.n] = carry;
+  __syncthreads();
+  for (std::uint32_t i = threadIdx.x; i < count; i += 1024) {
+    const uint2 rec = a.spill[i];
+    a.anchor[a.off[rec.x] + atomicAdd(a.cnt + rec.x, 1u)] = rec.y;
+  }
+  __syncthreads();
+  for (std::uint32_t i = threadIdx.x; i < count; i += 1024) a.cnt[a.spill[i].x] = 0;
 }
 
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, const std::uint32_t* __restrict__ in_off,
@@ -990,25 +1054,34 @@ __global__ void __launch_bounds__(THREADS, MINB) gather_batched_kernel(const Gat
       const std::uint32_t u = d0.x, lenA = d0.z, lenB = d1.x, hub = d1.z;
 
       // virtual list = [adjacency slice | own samples | incoming samples], as offsets into nbr / neg_own / in_anchor
-      std::uint32_t offC = 0, lenC = 0;
+      std::uint32_t offC = 0, lenC = 0, offD = 0, lenD = 0;
       if (d1.y) {  // first item of the vertex: it takes the incoming samples as well
-        offC = __ldg(a.in_off + u);
-        lenC = __ldg(a.in_off + u + 1) - offC;
+        if (a.in_stride) {  // slotted buckets: the vertex's own slots, then what spilled (normally nothing)
+          offC = u * a.in_stride;
+          lenC = min(a.in_cnt[u], a.in_stride);
+          if (*a.spill_count) {
+            offD = a.spill_off[u];
+            lenD = a.spill_off[u + 1] - offD;
+          }
+        } else {
+          offC = __ldg(a.in_off + u);
+          lenC = __ldg(a.in_off + u + 1) - offC;
+        }
       }
-      const std::uint32_t endB = lenA + lenB, total = endB + lenC;
+      const std::uint32_t endB = lenA + lenB, endC = endB + lenC, total = endC + lenD;
 
       // one list entry (vertex id) per lane and sub-batch: lane (grp, r) holds entry grp*TB + r/REP of the sub-batch.
       // Validity and kind (0 edge, 1 sample tallied here, 2 incoming sample) follow from the entry's position alone, so
       // nothing has to wait on these loads until the ids are needed as addresses two batches later.
       // entry e of the virtual list lives at index e + d of its array (wrapping 32-bit arithmetic)
-      const std::uint32_t dA = d0.y, dB = d0.w - lenA, dC = offC - endB;
+      const std::uint32_t dA = d0.y, dB = d0.w - lenA, dC = offC - endB, dD = offD - endC;
       auto fetch = [&](std::uint32_t base, std::uint32_t (&ent)[U]) {
 #pragma unroll
         for (int s = 0; s < U; ++s) {
           const std::uint32_t e = base + s * E + mine;
-          const bool in_a = e < lenA, in_b = e < endB;
-          const std::uint32_t idx = e + (in_a ? dA : (in_b ? dB : dC));
-          const std::uint32_t* arr = in_a ? a.nbr : (in_b ? a.neg_own : a.in_anchor);
+          const bool in_a = e < lenA, in_b = e < endB, in_c = e < endC;
+          const std::uint32_t idx = e + (in_a ? dA : (in_b ? dB : (in_c ? dC : dD)));
+          const std::uint32_t* arr = in_a ? a.nbr : (in_b ? a.neg_own : (in_c ? a.in_anchor : a.spill_anchor));
           ent[s] = u;  // own row past the list end: zero difference, zero weight
           if (e < total) ent[s] = __ldg(arr + idx);
         }
@@ -1368,12 +1441,21 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
     const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.items + item));
     const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.items + item) + 1);
     const std::uint32_t u = d0.x, begin = d0.y, lenA = d0.z, offB = d0.w, lenB = d1.x, hub = d1.z;
-    std::uint32_t offC = 0, lenC = 0;
+    std::uint32_t offC = 0, lenC = 0, offD = 0, lenD = 0;
     if (d1.y) {  // first item of the vertex
-      offC = __ldg(a.in_off + u);
-      lenC = __ldg(a.in_off + u + 1) - offC;
+      if (a.in_stride) {  // slotted buckets (see gather_batched_kernel)
+        offC = u * a.in_stride;
+        lenC = min(a.in_cnt[u], a.in_stride);
+        if (*a.spill_count) {
+          offD = a.spill_off[u];
+          lenD = a.spill_off[u + 1] - offD;
+        }
+      } else {
+        offC = __ldg(a.in_off + u);
+        lenC = __ldg(a.in_off + u + 1) - offC;
+      }
     }
-    const std::uint32_t endB = lenA + lenB, total = endB + lenC;
+    const std::uint32_t endB = lenA + lenB, endC = endB + lenC, total = endC + lenD;
     const std::uint32_t ld = a.ld;
 
     float xu[VEC], y[VEC];
@@ -1390,7 +1472,9 @@ __global__ void __launch_bounds__(kThreads) gather_thread_kernel(const GatherArg
         const std::uint32_t e = base + q;
         other[q] = u;
         if (e < total) {
-          other[q] = __ldg(e < lenA ? a.nbr + begin + e : (e < endB ? a.neg_own + offB + (e - lenA) : a.in_anchor + offC + (e - endB)));
+          other[q] = __ldg(e < lenA ? a.nbr + begin + e
+                                    : (e < endB ? a.neg_own + offB + (e - lenA)
+                                                : (e < endC ? a.in_anchor + offC + (e - endB) : a.spill_anchor + offD + (e - endC))));
         }
       }
 #pragma unroll
@@ -2132,6 +2216,11 @@ int launch_csr_build(const std::uint32_t* src, const std::uint32_t* dst, std::ui
 int launch_sample(const SampleArgs& a, cudaStream_t stream) {
   if (a.slots == 0) return 0;
   sample_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a);
+  return 1;
+}
+
+int launch_spill_index(const SpillIndexArgs& a, cudaStream_t stream) {
+  spill_index_kernel<<<1, 1024, 0, stream>>>(a);
   return 1;
 }
 

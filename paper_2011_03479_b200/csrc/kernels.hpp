@@ -101,7 +101,27 @@ struct SampleArgs {
   std::uint32_t* in_rank;         // out: arrival rank of the slot inside its partner's bucket
   std::uint32_t* status;
   Ownership own;
+  // slotted buckets (bucket_mode 4): every vertex owns `in_stride` slots of in_anchor; the sampler stores the anchor at
+  // slot (partner * in_stride + arrival rank) itself -- no scan, no scatter pass.  The few samples whose partner's slots are
+  // full go to the spill list, indexed afterwards by launch_spill_index.  in_stride == 0: off.
+  std::uint32_t in_stride;
+  std::uint32_t* in_anchor;
+  uint2* spill;                   // (partner, anchor)
+  std::uint32_t* spill_count;
+  std::uint32_t spill_capacity;
 };
+
+// Slotted buckets, overflow side: `spill_count` records (partner, anchor) that did not fit their partner's slots.
+struct SpillIndexArgs {
+  std::uint32_t n;
+  const uint2* spill;
+  const std::uint32_t* spill_count;
+  std::uint32_t spill_capacity;
+  std::uint32_t* cnt;     // [n] scratch, zero on entry and on exit
+  std::uint32_t* off;     // [n + 1] exclusive offsets of the spilled anchors per partner (valid when spill_count > 0)
+  std::uint32_t* anchor;  // [spill_capacity] spilled anchors grouped by partner
+};
+int launch_spill_index(const SpillIndexArgs& a, cudaStream_t stream);
 
 constexpr int kMaxPeers = 15;  // other ranks whose X_{t+1} copy this rank writes directly (world <= 16)
 
@@ -177,6 +197,13 @@ struct GatherArgs {
   const std::uint32_t* neg_own;
   const std::uint32_t* in_off;     // n+1
   const std::uint32_t* in_anchor;
+  // slotted buckets (in_stride != 0): incoming samples of u are in_anchor[u*in_stride .. + min(in_cnt[u], in_stride)), plus,
+  // when *spill_count != 0, spill_anchor[spill_off[u] .. spill_off[u+1])
+  std::uint32_t in_stride;
+  const std::uint32_t* in_cnt;
+  const std::uint32_t* spill_count;
+  const std::uint32_t* spill_off;
+  const std::uint32_t* spill_anchor;
   const ItemDesc* items;
   const std::uint32_t* hub_first;  // first partial slot of hub h
   const std::uint32_t* hub_items;  // number of items of hub h

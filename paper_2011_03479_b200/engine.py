@@ -89,6 +89,7 @@ class IterationConfig:
     host_sigma: bool = False  # True: sigma search on the host instead of the device kernel
     deterministic: bool = False  # True: sorted sample buckets, byte-identical results run to run
     batch_rounds: int = 0  # run(): whole iterations queued per host round trip (0 auto, 1 every round, < 0 host loop)
+    devices: Optional[list] = None  # several GPUs of this process: vertices sharded over them (gempe_engine_create_multi)
 
 
 @dataclass
@@ -527,8 +528,11 @@ class EmbeddingEngine:
         c.batch_rounds = int(cfg.batch_rounds)
         self.n, self.m, self.dim = int(g.n), g.edge_count(), int(dim)
         self._pe_trace = []
-        rc = self._L.gempe_engine_create(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,
-                                         C.byref(c), seed)
+        devices = list(cfg.devices) if cfg.devices else []
+        dev = (C.c_int * max(1, len(devices)))(*devices)
+        rc = self._L.gempe_engine_create_multi(C.byref(self._h), g.n, self.m, _capi.ptr(g.src), _capi.ptr(g.dst), dim,
+                                               C.byref(c), seed, C.cast(dev, C.c_void_p) if devices else None,
+                                               len(devices))
         if rc != _capi.OK:
             self._h = C.c_void_p()
             _raise(rc, self._L.gempe_last_error(None).decode())

@@ -91,6 +91,17 @@ int main() {
     CHECK(intra / ci < inter / cx);
     CHECK(res.relabel.forward.size() == 20 && res.relabel.inverse[res.relabel.forward[7]] == 7);
   }
+  {  // the engine sharded over a device list (two ranks on device 0) reproduces the single-GPU engine bit for bit
+    Graph g = clique_pair(12);
+    IterationConfig cfg;
+    cfg.max_iters = 12;
+    cfg.deterministic = true;
+    EmbedResult one = embed(g, 4, cfg, 9);
+    cfg.devices = {0, 0};
+    EmbedResult two = embed(g, 4, cfg, 9);
+    CHECK(one.iterations == two.iterations && one.final_sigma == two.final_sigma);
+    CHECK(one.embedding.coords == two.embedding.coords);
+  }
   {  // two-body system settles (one edge inside a 3-vertex graph)
     Graph g = graph_from_edges(3, {{0, 1}});
     IterationConfig cfg;

@@ -90,3 +90,17 @@ def test_group_of_one_and_errors(G):
     with pytest.raises(G.DivergenceError):
         grp.iterate(1.5, 1.0, 0)
     grp.close()
+
+
+def test_engine_sharded_over_a_device_list_equals_the_single_gpu_engine(G):
+    """gempe_engine_create_multi (the `devices[], n_devices` constructor): embed() on three ranks == embed() on one."""
+    from dataclasses import replace
+    n, src, dst = er_graph(600, 3500, 9)
+    g = G.Graph(n, src, dst)
+    cfg = G.IterationConfig(max_iters=25, deterministic=True, relabel_period=10, batch_rounds=-1)
+    one = G.embed(g, 8, cfg, 4)
+    many = G.embed(g, 8, replace(cfg, devices=[0, 0, 0]), 4)
+    assert many.iterations == one.iterations and many.converged == one.converged
+    assert np.array_equal(many.pe_trace, one.pe_trace) and many.final_sigma == one.final_sigma
+    assert np.array_equal(many.embedding.view(np.uint32), one.embedding.view(np.uint32))
+    assert np.array_equal(many.last_hist_nonedge, one.last_hist_nonedge)

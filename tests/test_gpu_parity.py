@@ -186,7 +186,7 @@ def test_round_parity_across_dimensions(G, oracle, golden_fastmath, dim, kernel)
                 **KERNELS[kernel])
 
 
-@pytest.mark.parametrize("bucket_mode", [1, 2, 3])
+@pytest.mark.parametrize("bucket_mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("neg_mode,k", [(0, 0), (1, 5), (1, 20)])
 def test_round_parity_modes(G, oracle, golden_fastmath, exact, neg_mode, k, bucket_mode):
@@ -815,4 +815,32 @@ def test_queued_run_hooks_directly(G):
     ctx.run_enqueue(4, 8, False)
     with pytest.raises(G.DivergenceError):
         ctx.run_poll()
+    ctx.close()
+
+
+def test_slotted_buckets_overflow_into_the_spill_list(G, oracle, golden_fastmath, monkeypatch):
+    """bucket_mode 4 with 2 slots per vertex (test hook): most incoming samples overflow, go through the spill list and
+    its one-block index, and the round still equals the oracle (tallies exact, y / z / X to 1e-4)."""
+    monkeypatch.setenv("GEMPE_IN_STRIDE", "2")
+    for dim in (2, 64, 128):
+        check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, iters=3, bucket_mode=4)
+        check_round(G, oracle, golden_fastmath, star_plus_ring(300, hubs=2), dim, seed=2, neg_mode=1, k=9, iters=2,
+                    bucket_mode=4)
+    # a clique plus one isolated vertex: every anchor's only legal partner is that vertex, whose bucket receives ALL samples
+    # (far beyond S/n + 6 sigma slots) -- with the natural stride, no test hook
+    monkeypatch.delenv("GEMPE_IN_STRIDE")
+    n = 40
+    src = np.array([a for a in range(n - 1) for b in range(a + 1, n - 1)], np.uint32)
+    dst = np.array([b for a in range(n - 1) for b in range(a + 1, n - 1)], np.uint32)
+    ctx = G.Context(G.Graph(n, src, dst), 3, 5, hash_bits=24, bucket_mode=4)  # 2^24 cells: no false positive blocks a pair
+    ctx.set_capture(True)
+    ws, wd, to_work = ctx.work_graph()
+    table = oracle.hash_build(n, ws, wd, 24)
+    x = ctx.get_coords()
+    he, hn = ctx.iterate(1.5, 1.0, 0)
+    y, z = ctx.get_yz()
+    want = oracle.iterate(n, ws, wd, x, 0, 0, 5, 0, 1.5, 1.0, golden_fastmath, table)
+    assert want["rc"] == 0 and (want["partners"] == to_work[n - 1]).all()
+    assert np.array_equal(he, want["hist_edge"]) and np.array_equal(hn, want["hist_nonedge"])
+    assert rel_l2(y, want["y"]) <= TOL and rel_l2(z, want["z"]) <= TOL and rel_l2(ctx.get_coords(), want["x_next"]) <= TOL
     ctx.close()
