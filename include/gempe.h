@@ -278,6 +278,9 @@ int gempe_end_round(gempe_ctx* ctx);                               /* swaps X_t 
  * (CUDA events on the context's stream), split as {total, sampling passes, gather+update}. */
 int gempe_elapsed_ms(gempe_ctx* ctx, float out3[3]);
 uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels launched so far */
+/* slotted buckets (bucket_mode 4): samples of the last round that did not fit their partner's slots and took the
+ * indexed spill list (waits for the stream); -1 when the context does not use slotted buckets.  Diagnostics / tests. */
+int64_t gempe_bucket_spills(gempe_ctx* ctx);
 
 /* ---- Several GPUs in ONE process: the C++ multi-GPU host (`devices[], n_devices` of the proposed
  * constructor).  A group is one context per listed device (a device may be listed more than once: several ranks on one

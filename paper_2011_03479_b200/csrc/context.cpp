@@ -1446,6 +1446,16 @@ int gempe_elapsed_ms(gempe_ctx* c, float out3[3]) {
 
 std::uint64_t gempe_kernel_launches(const gempe_ctx* c) { return c->launches; }
 
+std::int64_t gempe_bucket_spills(gempe_ctx* c) {
+  if (!c->in_stride) return -1;
+  std::uint32_t count = 0;
+  if (cudaSetDevice(c->opt.device) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess ||
+      cudaMemcpy(&count, c->in_cnt.get() + c->n, sizeof count, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    return -2;
+  }
+  return count;
+}
+
 int gempe_probe(gempe_ctx* c, const std::uint32_t* i, const std::uint32_t* j, std::uint64_t count, std::uint8_t* out) {
   return guarded(c, [&] {
     require_live(c);

@@ -179,6 +179,10 @@ class Context:
         return self._L.gempe_kernel_launches(self._h)
 
     @property
+    def bucket_spills(self) -> int:
+        return self._L.gempe_bucket_spills(self._h)
+
+    @property
     def row_stride(self) -> int:
         return self._L.gempe_row_stride(self._h)
 

@@ -822,6 +822,10 @@ def test_slotted_buckets_overflow_into_the_spill_list(G, oracle, golden_fastmath
     """bucket_mode 4 with 2 slots per vertex (test hook): most incoming samples overflow, go through the spill list and
     its one-block index, and the round still equals the oracle (tallies exact, y / z / X to 1e-4)."""
     monkeypatch.setenv("GEMPE_IN_STRIDE", "2")
+    probe = G.Context(G.Graph(*er_graph(400, 1000, 23)), 2, 9, bucket_mode=4)
+    probe.iterate(1.5, 1.0, 0)
+    assert probe.bucket_spills > 500  # the hook does force the overflow path
+    probe.close()
     for dim in (2, 64, 128):
         check_round(G, oracle, golden_fastmath, er_graph(400, 1000, 23), dim, seed=9, iters=3, bucket_mode=4)
         check_round(G, oracle, golden_fastmath, star_plus_ring(300, hubs=2), dim, seed=2, neg_mode=1, k=9, iters=2,

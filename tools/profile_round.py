@@ -48,5 +48,6 @@ for it in range(2, 2 + a.rounds):
     ctx.iterate_async(1.5, sigma, it)
 he, hn = ctx.sync()
 tot, samp, gath = ctx.elapsed_ms()
+print('slot spills of the last round:', ctx.bucket_spills)
 print(f"{a.config} bucket_mode {a.bucket_mode}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
       f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
