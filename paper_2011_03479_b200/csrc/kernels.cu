@@ -973,10 +973,11 @@ __device__ __forceinline__ double shfl_xor_f64(double v, int off) {
 // ids and coefficients travel by sub-group shuffles (width LPR) with immediate source lanes.  Slot t of every lane of a
 // group holds the SAME row (entry grp*TB + t), so one load instruction reads whole 128-byte lines of G rows.  (A
 // lane-dependent slot order makes the reduction select-free, but then one load instruction touches TB different rows
-// with 32 bytes each: measured 10.5 ms instead of 4.6 ms on c4, profiles/r02_gather_permuted_slots.md.)  The shape that
-// minimises shuffles and selects is FEW lanes per row: LPR = 8 at d = 128 (a lane holds four 16-byte vectors of a row,
-// 128 bytes apart), four rows per group -- 4 id shuffles, 4 coefficient shuffles and a 4 -> 1 transposed reduction per
-// batch of 16 rows, instead of 16 / 16 / 16 -> 1 with one warp per row.
+// with 32 bytes each: measured 10.5 ms instead of 4.6 ms on c4.)  FEW lanes per row minimise shuffles and selects: LPR = 8 at
+// d = 128 (a lane holds four 16-byte vectors of a row, 128 bytes apart), four rows per group -- 4 id shuffles, 4 coefficient
+// shuffles and a 4 -> 1 transposed reduction per batch of 16 rows, instead of 16 / 16 / 16 -> 1 with one warp per row: 1.75 G
+// instead of 2.19 G warp instructions on c4.  But the own row and the accumulator then take 32 registers, the kernel
+// needs 128 and runs 16 instead of 20 warps per SM, which costs more than the instructions save (launch_gather).
 //
 // PRECISE = true : pair_distance exactly as the reference (double differences, double accumulation), double
 //                  parabola chain.
@@ -2398,13 +2399,21 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool 
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);  // 8 rows per group, 32 warps/SM
 #ifndef GEMPE_D128_ROW_LANES
-#define GEMPE_D128_ROW_LANES 8
+#define GEMPE_D128_ROW_LANES 32
 #endif
-#if GEMPE_D128_ROW_LANES == 32  // one warp per row (round 1)
-  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);
+  // d = 128 on c4 / c5 (40-round / 3-round runs under the power cap, gather ms): one warp per row at 96 registers and 20
+  // warps/SM 4.43 / 86.5 (alone: 4.17, 2.19 G warp instructions); 8 lanes per row at 128 registers and 16 warps/SM 4.59 /
+  // 89.3 (alone: 4.26, 1.75 G); 16 lanes per row 5.12 / 97.8.  The kernel wants warps more than it wants fewer
+  // instructions (3 instead of 4 resident blocks of the 8-lane shape: 5.12), so one warp per row is the default.
+#if GEMPE_D128_ROW_LANES == 32
+#ifndef GEMPE_D128_THREADS
+#define GEMPE_D128_THREADS 128
+#define GEMPE_D128_MINB 5
+#endif
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, GEMPE_D128_THREADS, GEMPE_D128_MINB>(a, lo, hi, precise, stream);
 #elif GEMPE_D128_ROW_LANES == 16
   else if (ld <= 128) gather_batched_go<16, 2, 4, 8, 1, 128, 5>(a, lo, hi, precise, stream);
-#else  // 8 lanes per row, 4 rows per group, 16 rows per warp and batch; own row + accumulator take 32 registers: 16 warps/SM
+#else  // 8 lanes per row, 4 rows per group: fewest instructions, but own row + accumulator take 32 registers -> 16 warps/SM
   else if (ld <= 128) gather_batched_go<8, 4, 4, 4, 1, 128, 4>(a, lo, hi, precise, stream);
 #endif
   // wider rows: 64 row registers per lane as well (8 / 4 rows per batch), 16 warps/SM (d = 256: -19 %, d = 512: -10 %
