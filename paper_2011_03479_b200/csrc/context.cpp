@@ -478,7 +478,7 @@ SampleArgs sample_args(gempe_ctx* c, std::uint64_t iter) {
   a.stream_base = c->opt.rng == GEMPE_RNG_REFERENCE ? mix_seed(c->opt.seed, iter) : c->opt.seed;
   a.iter = iter;
   a.seed = c->opt.seed;
-  a.iter_dev = c->run_queued ? &c->run_state.get()->count : nullptr;  // a queued run: the round index lives on the device
+  a.iter_dev = c->run_queued ? &c->run_state.get()->batch_base : nullptr;  // a queued run: the batch's first round index lives on the device
   a.csr_src = c->csr_src.get();
   a.eid_role = c->eid_role.get();
   a.hash_words = c->hash_words.get();
@@ -516,7 +516,7 @@ void bucket_received(gempe_ctx* c) {
 }
 
 void sampling_passes(gempe_ctx* c, std::uint64_t iter) {
-  cuda_check(cudaMemsetAsync(c->round_state.get(), 0, (4 + 2 * kBins) * sizeof(unsigned long long), c->stream),
+  cuda_check(cudaMemsetAsync(c->status.get(), 0, (4 + 2 * kBins) * sizeof(unsigned long long), c->stream),
              "memset status + tallies");
   const SampleArgs a = sample_args(c, iter);
   if (c->pack_path) {
@@ -619,7 +619,7 @@ cudaEvent_t next_event(gempe_ctx* c) {
 }
 
 void fetch_status(gempe_ctx* c, std::uint64_t* hist_edge, std::uint64_t* hist_nonedge) {
-  cuda_check(cudaMemcpyAsync(c->pinned, c->round_state.get(), (4 + 2 * kBins) * sizeof(unsigned long long),
+  cuda_check(cudaMemcpyAsync(c->pinned, c->status.get(), (4 + 2 * kBins) * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, c->stream), "status + tallies D2H");
   cuda_check(cudaStreamSynchronize(c->stream), "round");
   std::uint32_t st[8];
@@ -664,6 +664,9 @@ void validate(std::uint32_t n, std::uint64_t m, const std::uint32_t* src, const 
 using namespace gempe;
 
 gempe_ctx::~gempe_ctx() {
+  if (ev_gathered) cudaEventDestroy(ev_gathered);
+  if (ev_sigma) cudaEventDestroy(ev_sigma);
+  if (side_stream) cudaStreamDestroy(side_stream);
   if (round_graph) cudaGraphExecDestroy(round_graph);
   for (cudaGraphExec_t g : run_graph) {
     if (g) cudaGraphExecDestroy(g);
@@ -740,7 +743,7 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
     c->sigma_single_block = std::getenv("GEMPE_SIGMA_SINGLE_BLOCK") != nullptr;  // A/B switch, read once per context
     pack_tables(c->tables);
     c->tables_f32.upload(pack_tables_f32());
-    c->round_state.allocate(4 + 2 * kBins, true);
+    c->round_state.allocate(2 * (4 + 2 * kBins), true);  // two sets: see gempe_ctx::rs
     c->status.p = reinterpret_cast<std::uint32_t*>(c->round_state.get());
     c->hist.p = c->round_state.get() + 4;
     c->work_cursor.allocate(1, true);
@@ -1146,33 +1149,48 @@ int gempe_graph_launch(gempe_ctx* c) {
 // ---- runs queued without host round trips (EmbeddingEngine::run, engine.cpp:349-373) --------------------------------
 namespace {
 
-// one whole iteration of a queued run on the stream: round, sigma search + bookkeeping, best-PE snapshot
-void enqueue_run_round(gempe_ctx* c, int parity) {
+// One whole iteration of a queued run: sampling passes and gather + update on the context's stream, sigma search +
+// bookkeeping + best-PE snapshot on the side stream.  Round r + 1's sampling passes need neither X nor sigma, so they run
+// BESIDE round r's sigma search (a serial chain of ~9 cluster rounds, 30 us: as long as a whole round on graph-drawing
+// sizes); the gather of round r + 1 waits for it.  The status / tally words alternate between two sets so that the
+// memset of round r + 1 does not race the search that still reads round r's tallies.
+void enqueue_run_round(gempe_ctx* c, int parity, std::uint32_t round_in_batch, bool first_in_batch) {
   const int saved = c->cur;
   c->cur = parity;
   c->use_dev_math = true;
   c->run_queued = true;
+  auto restore = [&] {
+    c->use_dev_math = false;
+    c->run_queued = false;
+    c->cur = saved;
+  };
   try {
-    sampling_passes(c, c->run_first_iter);
+    c->rs ^= 1;
+    c->status.p = reinterpret_cast<std::uint32_t*>(c->round_state.get() + c->rs * (4 + 2 * kBins));
+    c->hist.p = c->round_state.get() + c->rs * (4 + 2 * kBins) + 4;
+    sampling_passes(c, c->run_first_iter + round_in_batch);
+    if (!first_in_batch) cuda_check(cudaStreamWaitEvent(c->stream, c->ev_sigma, 0), "wait sigma");  // sigma of the round before
     gather_items(c, c->chunk_item_off.front(), c->chunk_item_off.back());
+    cuda_check(cudaEventRecord(c->ev_gathered, c->stream), "event");
+    cuda_check(cudaStreamWaitEvent(c->side_stream, c->ev_gathered, 0), "wait gather");
     const double pairs = static_cast<double>(static_cast<std::uint64_t>(c->n) * (c->n - 1) / 2);
     c->launches += launch_sigma_update(c->hist.get(), c->mu_dev, pairs, static_cast<double>(c->m),
                                        c->opt.math == GEMPE_MATH_EXACT, c->sigma_state.get(), c->status.get(),
                                        c->sigma_single_block, c->run_state.get(), c->run_pe_trace.get(),
-                                       c->run_sigma_trace.get(), c->stream);
+                                       c->run_sigma_trace.get(), c->side_stream);
     c->launches += launch_snapshot_if_improved(c->x[0].get(), c->x[1].get(), c->run_best_x.get(), c->run_best_x.size(),
-                                               c->run_state.get(), c->stream);
+                                               c->run_state.get(), c->side_stream);
+    cuda_check(cudaEventRecord(c->ev_sigma, c->side_stream), "event");
     cuda_check(cudaGetLastError(), "queued round");
   } catch (...) {
-    c->use_dev_math = false;
-    c->run_queued = false;
-    c->cur = saved;
+    restore();
     throw;
   }
-  c->use_dev_math = false;
-  c->run_queued = false;
-  c->cur = saved;
+  restore();
 }
+
+// the side stream's work of a batch flows back into the context's stream (and, under capture, into the graph)
+void join_run_batch(gempe_ctx* c) { cuda_check(cudaStreamWaitEvent(c->stream, c->ev_sigma, 0), "join sigma"); }
 
 void drop_run_graphs(gempe_ctx* c) {
   for (auto& g : c->run_graph) {
@@ -1208,6 +1226,11 @@ int gempe_run_begin(gempe_ctx* c, double mu, double sigma, std::uint64_t first_i
     c->run_rounds_seen = 0;
     c->run_armed = true;
     drop_run_graphs(c);
+    if (!c->side_stream) {
+      cuda_check(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking), "side stream");
+      cuda_check(cudaEventCreateWithFlags(&c->ev_gathered, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&c->ev_sigma, cudaEventDisableTiming), "event");
+    }
   });
 }
 
@@ -1219,8 +1242,10 @@ int gempe_run_enqueue(gempe_ctx* c, std::uint32_t rounds, std::uint64_t stop_at,
     // the device skips rounds once `stop_at` are done; the coordinates' parity follows the rounds actually done, so the
     // host learns it at the next poll -- until then nothing else may be queued on this context
     if (c->run_in_flight) throw config_error("poll the queued rounds (gempe_run_poll) before queueing more");
-    cuda_check(cudaMemcpyAsync(&c->run_state.get()->stop_at, &stop_at, sizeof stop_at, cudaMemcpyHostToDevice, c->stream),
-               "stop_at");
+    const unsigned long long limits[2] = {stop_at, c->run_rounds_seen};  // RunState::stop_at, batch_base (adjacent)
+    static_assert(offsetof(RunState, batch_base) == offsetof(RunState, stop_at) + sizeof(unsigned long long), "layout");
+    cuda_check(cudaMemcpyAsync(&c->run_state.get()->stop_at, limits, sizeof limits, cudaMemcpyHostToDevice, c->stream),
+               "stop_at + batch_base");
     const int parity = c->cur;
     if (use_graph) {
       if (c->run_graph_generation != c->structure_generation || c->run_graph_rounds != rounds) {
@@ -1233,7 +1258,8 @@ int gempe_run_enqueue(gempe_ctx* c, std::uint32_t rounds, std::uint64_t stop_at,
         cudaGraph_t graph = nullptr;
         cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
         try {
-          for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1);
+          for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1, r, r == 0);
+          join_run_batch(c);
         } catch (...) {
           cudaStreamEndCapture(c->stream, &graph);
           if (graph) cudaGraphDestroy(graph);
@@ -1249,7 +1275,8 @@ int gempe_run_enqueue(gempe_ctx* c, std::uint32_t rounds, std::uint64_t stop_at,
       cuda_check(cudaGraphLaunch(c->run_graph[parity], c->stream), "graph launch");
       c->launches += c->run_graph_launches;
     } else {
-      for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1);
+      for (std::uint32_t r = 0; r < rounds; ++r) enqueue_run_round(c, (parity + r) & 1, r, r == 0);
+      join_run_batch(c);
     }
     c->run_in_flight = true;
   });
@@ -1264,6 +1291,7 @@ int gempe_run_poll(gempe_ctx* c, gempe_run_status* out, double* pe_trace, double
                "run state D2H");
     cuda_check(cudaStreamSynchronize(c->stream), "queued rounds");
     c->run_in_flight = false;
+    c->run_rounds_seen = head.count;
     c->cur = static_cast<int>((head.parity_base + head.count) & 1ull);
     c->round_iter = c->run_first_iter + (head.count ? head.count - 1 : 0);
     c->last_draws = head.draws;

@@ -161,6 +161,11 @@ struct gempe_ctx {
   unsigned long long* pinned = nullptr;
 
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  // queued runs: the sigma search + bookkeeping of round t run on a side stream beside the sampling passes of round t + 1
+  // (which need neither X nor sigma); the status / tally words are double-buffered for that (round_state holds two sets)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_gathered = nullptr, ev_sigma = nullptr;
+  int rs = 0;  // which half of round_state the status / hist views point at
   gempe::RoundMath math{};
   gempe::DeviceTables tables{};
   gempe::DeviceBuffer<float4> tables_f32;  // directly indexed fp32 cells of the same tables (kernels.hpp)

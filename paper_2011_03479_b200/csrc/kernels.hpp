@@ -43,6 +43,8 @@ struct SigmaState {
 struct RunState {
   unsigned long long count;        // rounds completed == PE values recorded == index of the next round's sample streams
   unsigned long long stop_at;      // rounds with count >= stop_at are skipped (max_iters / relabel boundary / batch end)
+  unsigned long long batch_base;   // rounds done when the current batch was queued: round r of the batch samples the streams
+                                   // of iteration first_iter + batch_base + r (set by the host, stable while the batch runs)
   unsigned long long fail_iter;    // round that raised the first failure flag
   unsigned long long draws;        // LCG draws of the last completed round
   double best_pe;                  // minimum of the trace so far (engine.cpp:316-319)
