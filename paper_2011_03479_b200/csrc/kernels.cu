@@ -2406,11 +2406,7 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool 
   // 89.3 (alone: 4.26, 1.75 G); 16 lanes per row 5.12 / 97.8.  The kernel wants warps more than it wants fewer
   // instructions (3 instead of 4 resident blocks of the 8-lane shape: 5.12), so one warp per row is the default.
 #if GEMPE_D128_ROW_LANES == 32
-#ifndef GEMPE_D128_THREADS
-#define GEMPE_D128_THREADS 128
-#define GEMPE_D128_MINB 5
-#endif
-  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, GEMPE_D128_THREADS, GEMPE_D128_MINB>(a, lo, hi, precise, stream);
+  else if (ld <= 128) gather_batched_go<32, 1, 4, 16, 1, 128, 5>(a, lo, hi, precise, stream);
 #elif GEMPE_D128_ROW_LANES == 16
   else if (ld <= 128) gather_batched_go<16, 2, 4, 8, 1, 128, 5>(a, lo, hi, precise, stream);
 #else  // 8 lanes per row, 4 rows per group: fewest instructions, but own row + accumulator take 32 registers -> 16 warps/SM
