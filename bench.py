@@ -54,6 +54,8 @@ def parse():
                    help="CPU budget on rank 0 for the cpu_baseline leg of the GPU arm (default 30 s)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sub-records", action="store_true", help="skip per_edge_2 and largest_config")
+    p.add_argument("--largest-cpu-baseline", action="store_true",
+                   help="time the CPU reference on config 5 inside the largest_config record (adds ~3 minutes)")
     p.add_argument("--peer-broadcast", default="auto", choices=["auto", "off"],
                    help="N > 1: gather kernel stores updated rows into the peers' buffers (auto) or NCCL all-gather (off)")
     return p.parse_args()
@@ -476,12 +478,15 @@ def main():
                                                       min(args.steps, 5), 3, sampler_index=local_rank, peaks=peaks)
                 bctx.close()
                 big["config"] = config_record("c5", n5, len(s5), dim5)
-                per_worker = n5 * (dim5 + 1) * 4
-                big["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                                       "sample": "DNF (memory/time): one accumulator replica of the reference is %.1f GB plus a "
-                                                 "2.1 GB edge table; at the %.1f M pair-terms/s per core measured on config 4 "
-                                                 "one round of 3m = %.0f M pair-terms is tens of minutes -- not extrapolated "
-                                                 "(BASELINE.md section 3)" % (per_worker / 1e9, 0.5, 3 * len(s5) / 1e6)}
+                if args.largest_cpu_baseline:  # one round of the reference on c5 is about a minute after a minute of construction
+                    big["cpu_baseline"] = cpu_reference_arm(n5, s5, d5, dim5, steps=1, warmup=1)
+                else:
+                    big["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                           "sample": "not timed in the default run: one round of the reference on this graph is ~60 s "
+                                                     "after ~66 s of engine construction (13 workers x 8.7 GB of accumulators fit this "
+                                                     "host).  `bench.py --impl reference --config c5` times it on the full graph: "
+                                                     "12.98 M pair-terms/s on this pool's 16-core host (profiles/r02_reference_c5.json); "
+                                                     "`--largest-cpu-baseline` runs it inside this record"}
                 line["largest_config"] = big
             except Exception as e:  # noqa: BLE001
                 line["largest_config"] = {"unavailable": str(e)[:300]}
