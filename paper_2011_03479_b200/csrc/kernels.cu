@@ -161,6 +161,12 @@ __global__ void csr_fill_kernel(const std::uint32_t* __restrict__ src, const std
 
 // ---------------------------------------------------------------------------------- sampler
 
+// PER_VERTEX_K: slot t belongs to anchor t / k.  The slot count fits 32 bits (checked when the context is created), so
+// this is one 32-bit division instead of the 64-bit software routine
+__device__ __forceinline__ std::uint32_t slot_anchor(std::uint64_t t, std::uint32_t k) {
+  return static_cast<std::uint32_t>(t) / k;
+}
+
 // One sample stream: replays expand_seed32(seed, iter, unit, draw) followed by the LCG "advance, then use" loop
 // of sample_non_edges (reference mode), or a Philox4x32-10 stream.  Returns the accepted partner.
 __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::uint64_t t, std::uint32_t& anchor,
@@ -172,7 +178,7 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
     unit = er >> 1;
     draw = er & 1u;
   } else {
-    anchor = static_cast<std::uint32_t>(t / a.k);
+    anchor = slot_anchor(t, a.k);
     unit = anchor;
     draw = t - static_cast<std::uint64_t>(anchor) * a.k;
   }
@@ -209,6 +215,91 @@ __device__ __forceinline__ std::uint32_t sample_slot(const SampleArgs& a, std::u
   return anchor + 1 < a.n ? anchor + 1 : 0;
 }
 
+// Q independent streams per thread (reference LCG mode only): the draw of every open stream is made, then the probes
+// of all of them are issued before any answer is consumed -- the chain seed -> draw -> summary word -> table word is
+// latency, and one chain per thread leaves the memory system idle (the sampling kernel ran at 40 % issue activity).
+// Same streams, same draws, same partners as sample_slot; `draws` is the sum over the Q streams.
+template <int Q>
+__device__ __forceinline__ void sample_slots_lcg(const SampleArgs& a, const std::uint64_t (&t)[Q], const bool (&on)[Q],
+                                                 std::uint32_t (&anchor)[Q], std::uint32_t (&partner)[Q],
+                                                 std::uint32_t& draws) {
+  const std::uint64_t iter = a.iter + (a.iter_dev ? static_cast<std::uint64_t>(*a.iter_dev) : 0ull);
+  const std::uint64_t stream_base = a.iter_dev ? mix(a.seed, iter) : a.stream_base;
+  std::uint32_t s[Q];
+  bool open[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    open[q] = on[q];
+    anchor[q] = 0;
+    partner[q] = 0;
+    s[q] = 0;
+    if (!on[q]) continue;
+    std::uint64_t unit, draw;
+    if (a.neg_mode == 0) {
+      anchor[q] = __ldg(a.csr_src + t[q]);
+      const std::uint32_t er = __ldg(a.eid_role + t[q]);
+      unit = er >> 1;
+      draw = er & 1u;
+    } else {
+      anchor[q] = slot_anchor(t[q], a.k);
+      unit = anchor[q];
+      draw = t[q] - static_cast<std::uint64_t>(anchor[q]) * a.k;
+    }
+    s[q] = static_cast<std::uint32_t>(mix(mix(stream_base, unit), draw) >> 16);
+  }
+  for (int tries = 0; tries < kMaxRetries; ++tries) {
+    std::uint32_t g[Q], h[Q];
+    bool probe[Q], hit[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      probe[q] = false;
+      g[q] = h[q] = 0;
+      if (open[q]) {
+        s[q] = s[q] * kLcgMul + 1u;
+        ++draws;
+        g[q] = uniform_index(s[q], a.n);
+        probe[q] = g[q] != anchor[q];
+        h[q] = pair_hash(anchor[q], g[q], a.n, a.hash_mask);
+      }
+    }
+    if (a.hash_summary) {  // first the small "any cell of the group set" bitmap, all streams at once
+      std::uint32_t sw[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) sw[q] = probe[q] ? __ldg(a.hash_summary + (h[q] >> (kSummaryShift + 5))) : 0u;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) hit[q] = probe[q] && ((sw[q] >> ((h[q] >> kSummaryShift) & 31u)) & 1u);
+    } else {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) hit[q] = probe[q];
+    }
+    {
+      std::uint32_t tw[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) tw[q] = hit[q] ? __ldg(a.hash_words + (h[q] >> 5)) : 0u;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) hit[q] = hit[q] && ((tw[q] >> (h[q] & 31u)) & 1u);
+    }
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (open[q] && probe[q] && !hit[q]) {
+        partner[q] = g[q];
+        open[q] = false;
+      }
+      any |= open[q];
+    }
+    if (!any) return;
+  }
+  // near_complete_graph_error (sampler.cpp:18-21); keep memory-safe output
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (open[q]) {
+      atomicOr(a.status + kStatRetryCap, 1u);
+      partner[q] = anchor[q] + 1 < a.n ? anchor[q] + 1 : 0;
+    }
+  }
+}
+
 // Total draw count (test hook / p-bar of the roofline formula).  Called by every thread of the block: one global
 // atomic per block -- per-warp atomics on this single address serialise in L2 and dominated the sampling kernel.
 __device__ __forceinline__ void add_draws(const SampleArgs& a, std::uint32_t draws) {
@@ -225,26 +316,48 @@ __device__ __forceinline__ void add_draws(const SampleArgs& a, std::uint32_t dra
 
 // ---- bucketing by partner, method A (small n): one returning atomic per sample on the partner's counter, then
 // scan + scatter.  Every array it touches at random (in_cnt, in_off) fits L2 for n up to a few million.
-__global__ void __launch_bounds__(kThreads, 8) sample_kernel(const SampleArgs a) {
-  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+constexpr int kSampleIlp = 2;  // sample streams per thread (sample_slots_lcg)
+__global__ void __launch_bounds__(kThreads, 6) sample_kernel(const SampleArgs a) {
+  const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * (kThreads * kSampleIlp) + threadIdx.x;
   std::uint32_t draws = 0;
-  if (t < a.slots) {
-    std::uint32_t anchor;
-    const std::uint32_t partner = sample_slot(a, t, anchor, draws);
-    a.neg_own[t] = partner;
+  std::uint64_t t[kSampleIlp];
+  bool on[kSampleIlp];
+  std::uint32_t anchor[kSampleIlp], partner[kSampleIlp];
+#pragma unroll
+  for (int q = 0; q < kSampleIlp; ++q) {
+    t[q] = t0 + q * kThreads;
+    on[q] = t[q] < a.slots;
+  }
+  if (a.rng == 0) {
+    sample_slots_lcg<kSampleIlp>(a, t, on, anchor, partner, draws);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kSampleIlp; ++q)
+      if (on[q]) partner[q] = sample_slot(a, t[q], anchor[q], draws);
+  }
+  // the returning atomics of all streams before any of their answers is stored
+  std::uint32_t rank[kSampleIlp];
+#pragma unroll
+  for (int q = 0; q < kSampleIlp; ++q) {
+    rank[q] = kNotLocal;
+    if (on[q] && is_local(a.own, partner[q])) rank[q] = atomicAdd(a.in_cnt + partner[q], 1u);
+  }
+#pragma unroll
+  for (int q = 0; q < kSampleIlp; ++q) {
+    if (!on[q]) continue;
     if (a.in_stride) {  // slotted buckets: the arrival rank is the slot
-      if (is_local(a.own, partner)) {
-        const std::uint32_t rank = atomicAdd(a.in_cnt + partner, 1u);
-        if (rank < a.in_stride) {
-          a.in_anchor[static_cast<std::size_t>(partner) * a.in_stride + rank] = anchor;
-        } else {
-          const std::uint32_t at = atomicAdd(a.spill_count, 1u);
-          if (at < a.spill_capacity) a.spill[at] = make_uint2(partner, anchor);
-          else atomicOr(a.status + kStatExchangeOverflow, 1u);
-        }
+      a.neg_own[t[q]] = partner[q];
+      if (rank[q] == kNotLocal) continue;
+      if (rank[q] < a.in_stride) {
+        a.in_anchor[static_cast<std::size_t>(partner[q]) * a.in_stride + rank[q]] = anchor[q];
+      } else {
+        const std::uint32_t at = atomicAdd(a.spill_count, 1u);
+        if (at < a.spill_capacity) a.spill[at] = make_uint2(partner[q], anchor[q]);
+        else atomicOr(a.status + kStatExchangeOverflow, 1u);
       }
-    } else {
-      a.in_rank[t] = is_local(a.own, partner) ? atomicAdd(a.in_cnt + partner, 1u) : kNotLocal;
+    } else {  // large graphs: both arrays are read once by later kernels and must not displace the counters / summary
+      __stcs(a.neg_own + t[q], partner[q]);
+      __stcs(a.in_rank + t[q], rank[q]);
     }
   }
   add_draws(a, draws);
@@ -301,14 +414,36 @@ __global__ void __launch_bounds__(1024) spill_index_kernel(const SpillIndexArgs 
   for (std::uint32_t i = threadIdx.x; i < count; i += 1024) a.cnt[a.spill[i].x] = 0;
 }
 
+constexpr int kScatterIlp = 4;  // samples per thread: rank / partner -> offset -> store is a chain of dependent accesses
+// blockIdx.y = part: the samples are walked gridDim.y times, each walk placing only the partners of one contiguous vertex
+// range, so the window of in_anchor that receives random 4-byte stores (S * 4 bytes in all) stays in L2 while the index
+// streams pass through (launch_scatter sizes the parts).  A window beyond L2 is written back half-filled and fetched
+// again: 277 MB of DRAM writes for 84 MB of anchors on c4.
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const SampleArgs a, const std::uint32_t* __restrict__ in_off,
-                                                           std::uint32_t* __restrict__ in_anchor) {
-  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= a.slots) return;
-  const std::uint32_t rank = a.in_rank[t];
-  if (rank == kNotLocal) return;
-  const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t) : static_cast<std::uint32_t>(t / a.k);
-  in_anchor[in_off[a.neg_own[t]] + rank] = anchor;
+                                                           std::uint32_t* __restrict__ in_anchor, std::uint32_t part_rows) {
+  const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * (kThreads * kScatterIlp) + threadIdx.x;
+  const std::uint32_t lo = blockIdx.y * part_rows, hi = lo + part_rows;  // part_rows * gridDim.y >= n
+  std::uint32_t rank[kScatterIlp], partner[kScatterIlp], off[kScatterIlp];
+  bool mine[kScatterIlp];
+#pragma unroll
+  for (int q = 0; q < kScatterIlp; ++q) {
+    const std::uint64_t t = t0 + q * kThreads;
+    partner[q] = 0xffffffffu;
+    if (t < a.slots) partner[q] = __ldcs(a.neg_own + t);  // read once per walk: must not push the window out of L2
+  }
+#pragma unroll
+  for (int q = 0; q < kScatterIlp; ++q) {
+    mine[q] = partner[q] >= lo && partner[q] < hi;  // 0xffffffff (no slot) is in no part: hi <= n + part_rows < 2^32
+    rank[q] = mine[q] ? __ldcs(a.in_rank + t0 + q * kThreads) : kNotLocal;
+    off[q] = mine[q] ? in_off[partner[q]] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < kScatterIlp; ++q) {
+    if (mine[q] && rank[q] != kNotLocal) {
+      const std::uint64_t t = t0 + q * kThreads;
+      in_anchor[off[q] + rank[q]] = a.neg_mode == 0 ? __ldg(a.csr_src + t) : slot_anchor(t, a.k);
+    }
+  }
 }
 
 // ---- sharded sampling with an exchange step (world > 1): every rank samples ONLY the streams of the anchors it owns,
@@ -328,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
     }
     const std::uint64_t t = x.first_slot[c] + (i - x.prefix[c]);
     partner = sample_slot(a, t, anchor, draws);
-    a.neg_own[t] = partner;
+    __stcs(a.neg_own + t, partner);  // streamed: read again by the gather only
     dest = x.region_rows ? partner / x.region_rows : (partner / a.own.block_rows) % a.own.world;
     have = true;
   }
@@ -350,7 +485,8 @@ __global__ void __launch_bounds__(kThreads, 8) sample_pack_kernel(const SampleAr
     const std::uint32_t pos = sh_base[dest] + local;
     if (pos < x.capacity) {
       uint2* region = x.direct ? x.dest_region[dest] : x.send + static_cast<std::size_t>(dest) * x.capacity;
-      region[pos] = make_uint2(partner, anchor);
+      if (x.direct) region[pos] = make_uint2(partner, anchor);
+      else __stcs(region + pos, make_uint2(partner, anchor));
     } else {
       const std::uint32_t at = x.spill ? atomicAdd(x.spill_count, 1u) : 0xffffffffu;
       if (at < x.spill_capacity) x.spill[at] = make_uint2(partner, anchor);
@@ -381,14 +517,14 @@ __global__ void __launch_bounds__(kThreads) count_records_kernel(const ExchangeA
 #pragma unroll
   for (int q = 0; q < kRecIlp; ++q) {
     const std::uint32_t j = j0 + q * kThreads;
-    partner[q] = j < count ? x.recv[base + j].x : 0xffffffffu;
+    partner[q] = j < count ? __ldcs(reinterpret_cast<const std::uint32_t*>(x.recv + base + j)) : 0xffffffffu;
   }
 #pragma unroll
   for (int q = 0; q < kRecIlp; ++q) rank[q] = partner[q] != 0xffffffffu ? atomicAdd(in_cnt + partner[q], 1u) : 0u;
 #pragma unroll
   for (int q = 0; q < kRecIlp; ++q) {
     const std::uint32_t j = j0 + q * kThreads;
-    if (j < count) rec_rank[base + j] = rank[q];
+    if (j < count) __stcs(rec_rank + base + j, rank[q]);
   }
 }
 
@@ -407,8 +543,8 @@ __global__ void __launch_bounds__(kThreads) scatter_records_kernel(const Exchang
     rec[q] = make_uint2(0xffffffffu, 0u);
     rank[q] = 0;
     if (j < count) {
-      rec[q] = x.recv[base + j];
-      rank[q] = rec_rank[base + j];
+      rec[q] = __ldcs(x.recv + base + j);  // streams: the window of in_anchor they scatter into is what L2 should keep
+      rank[q] = __ldcs(rec_rank + base + j);
     }
   }
 #pragma unroll
@@ -547,7 +683,7 @@ __global__ void __launch_bounds__(1024) partition_kernel(const SampleArgs a, con
 #pragma unroll
       for (int q = 0; q < kIlp; ++q) {
         if (t[q] < a.slots && is_local(a.own, partner[q])) {
-          const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t[q]) : static_cast<std::uint32_t>(t[q] / a.k);
+          const std::uint32_t anchor = a.neg_mode == 0 ? __ldg(a.csr_src + t[q]) : slot_anchor(t[q], a.k);
           const std::uint32_t pos = atomicAdd(&sh_cur[partner[q] >> p.shift], 1u);
           p.records[pos] = make_uint2(partner[q], anchor);
         }
@@ -2216,7 +2352,7 @@ int launch_csr_build(const std::uint32_t* src, const std::uint32_t* dst, std::ui
 
 int launch_sample(const SampleArgs& a, cudaStream_t stream) {
   if (a.slots == 0) return 0;
-  sample_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a);
+  sample_kernel<<<blocks_for(a.slots, kThreads * kSampleIlp), kThreads, 0, stream>>>(a);
   return 1;
 }
 
@@ -2306,7 +2442,15 @@ int launch_scan(std::uint32_t* in_cnt, std::uint32_t* in_off, std::uint32_t n, s
 
 int launch_scatter(const SampleArgs& a, const std::uint32_t* in_off, std::uint32_t* in_anchor, cudaStream_t stream) {
   if (a.slots == 0) return 0;
-  scatter_kernel<<<blocks_for(a.slots, kThreads), kThreads, 0, stream>>>(a, in_off, in_anchor);
+  // parts of at most 64 MB of in_anchor each (half of L2; every extra walk re-reads the index streams).  Measured on c4:
+  // 84 MB window (k = 20 per vertex) 264 / 236 / 250 / 248 us with 1 / 2 / 3 / 4 parts, 125 MB window (2 per edge)
+  // 716 / 376 / 425 / 494 us.  GEMPE_SCATTER_PARTS overrides (A/B hook)
+  static const int forced = [] { const char* e = std::getenv("GEMPE_SCATTER_PARTS"); return e ? std::atoi(e) : 0; }();
+  std::uint64_t parts = forced > 0 ? static_cast<std::uint64_t>(forced) : (a.slots * 4 + (64ull << 20) - 1) / (64ull << 20);
+  parts = std::min<std::uint64_t>(std::max<std::uint64_t>(parts, 1), 8);
+  const std::uint32_t part_rows = static_cast<std::uint32_t>((static_cast<std::uint64_t>(a.n) + parts - 1) / parts);
+  const dim3 grid(blocks_for(a.slots, kThreads * kScatterIlp), static_cast<unsigned>(parts));
+  scatter_kernel<<<grid, kThreads, 0, stream>>>(a, in_off, in_anchor, part_rows);
   return 1;
 }
 

@@ -24,6 +24,15 @@ ap.add_argument("--warm-iters", type=int, default=0, help="real iterations (devi
 a = ap.parse_args()
 
 import torch  # noqa: E402
+if os.environ.get("GEMPE_L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (0x05) on the primary context
+    import ctypes
+    torch.cuda.init()
+    torch.zeros(1, device="cuda")
+    rt = ctypes.CDLL("libcudart.so.12")
+    val = ctypes.c_size_t(0)
+    rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(int(os.environ["GEMPE_L2_FETCH"])))
+    rt.cudaDeviceGetLimit(ctypes.byref(val), 5)
+    print("cudaLimitMaxL2FetchGranularity: set rc", rc, "now", val.value)
 n, src, dst, dim, k, _, init, std = graphgen.make_config(a.config, device=torch.device('cuda', 0))
 torch.cuda.empty_cache()
 if a.dim:
@@ -51,3 +60,22 @@ tot, samp, gath = ctx.elapsed_ms()
 print('slot spills of the last round:', ctx.bucket_spills)
 print(f"{a.config} bucket_mode {a.bucket_mode}: {a.rounds} rounds, {tot / a.rounds:.3f} ms/round (sampling passes {samp / a.rounds:.3f}, "
       f"gather {gath / a.rounds:.3f}); tallies {int(he.sum())} edges, {int(hn.sum())} samples")
+
+if os.environ.get("GEMPE_LIVE_KERNEL_TIMES"):
+    # live per-kernel durations (CUPTI through torch.profiler): warm, back to back, at the clocks of a running job --
+    # unlike the ncu launch list, whose launches are serialised and start cold
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for it in range(10, 10 + a.rounds):
+            ctx.iterate_async(1.5, sigma, it)
+        ctx.sync()
+    rows = {}
+    for e in prof.events():
+        if e.device_type.name != "CUDA":
+            continue
+        r = rows.setdefault(e.name[:70], [0, 0.0])
+        r[0] += 1
+        r[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+    print("live kernel times (us per round):")
+    for name, (cnt, us) in sorted(rows.items(), key=lambda kv: -kv[1][1]):
+        print(f"  {us / a.rounds:12.1f}  x{cnt / a.rounds:5.1f}  {name}")
