@@ -30,6 +30,9 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", f"-I{CUDA_HOME}/i
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
+    tag = os.path.join(OUT_DIR, ".flags")  # built with other flags (GEMPE_NVCC_EXTRA A/B builds)
+    if os.path.exists(tag) and open(tag).read() != " ".join(NVCC_FLAGS + CXX_FLAGS):
+        return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in CU_SOURCES + CXX_SOURCES] + \
            [h if os.path.isabs(h) else os.path.join(CSRC, h) for h in HEADERS] + [os.path.abspath(__file__)]
