@@ -548,6 +548,7 @@ def main():
     w0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    eng.gather_events = []
     for s in range(args.steps):
         eng.round_async(mu, sigma, eng.iter + s)
     with torch.cuda.stream(stream):
@@ -556,11 +557,13 @@ def main():
     barrier()
     w1 = time.perf_counter()
     ms = ev0.elapsed_time(ev1)
+    gather_ms = sum(a.elapsed_time(b) for a, b in eng.gather_events) / args.steps  # this rank's gather launches per round
+    eng.gather_events = None
     launches = ctx.kernel_launches - launches0
     ctx.sync()
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms, gather_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms, gather_ms = float(t[0].item()), float(t[1].item())
     # the timed region is short: the same rounds continue untimed (the same number on every rank) until the clock sampler
     # has seen ~0.5 s of this load
     extra = max(0, int(500.0 / max(ms / args.steps, 1e-3)) - args.steps)
@@ -581,6 +584,21 @@ def main():
                  "pair_terms_per_iteration": int(pair_terms), "sigma": sigma,
                  "parallelism": f"vertex-sharded x{world}, samples: {samples_path}, coordinates: {exchange_path}",
                  "clocks": clocks, "gpu_launches": int(launches)})
+
+    # HBM roofline of the dominant kernel per rank: a rank gathers for the vertices it owns, 1/world of the job's
+    # algorithmic bytes (section 8d formula), in `chunks` launches per round; the slowest rank's time; no DRAM byte count
+    # (ncu runs on one GPU only), so the algorithmic figure stands in and says so
+
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    b_rank = ctx.algorithmic_bytes / world
+    alg = b_rank / (gather_ms * 1e-3) / 1e9
+    line["roofline"] = {"bound": "hbm", "peak": peak, "unit": "GB/s", "kernel": "gather_batched_kernel (per rank)",
+                        "kernel_ms": gather_ms, "launches_per_round": eng.chunks, "algorithmic_bytes": int(b_rank),
+                        "achieved": alg, "frac": alg / peak, "traffic": None,
+                        "frac_basis": "ALGORITHMIC bytes of one rank's share (counts L2-served hub rows as HBM traffic: can exceed 1) "
+                                      "/ slowest rank's live gather time per round",
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)" if peaks else "fallback 6650 GB/s",
+                        "step_frac": ctx.algorithmic_bytes / world / (ms_per_step * 1e-3) / 1e9 / peak}
 
     # end to end at N GPUs with HOST buffers: every rank uploads X_t (each needs all of it; N PCIe links in
     # parallel), the round runs, every rank returns the rows it owns (together X_{t+1}) and the job-wide tallies

@@ -156,6 +156,7 @@ class ShardedEngine:
         self.pe_trace: List[float] = []
         self._pending = []
         self._seeded = False
+        self.gather_events = None  # a list: round_async appends one CUDA event pair per gather launch (bench.py)
 
     def _wait_pending(self):
         for w in self._pending:
@@ -185,7 +186,14 @@ class ShardedEngine:
             x_next = self.ops.x_next()
             span = self.world * self.block_rows
             for c in range(self.chunks):
-                self.ops.gather_chunk(c)
+                if self.gather_events is not None:  # bench: device time of this rank's gather launches
+                    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    ev[0].record()
+                    self.ops.gather_chunk(c)
+                    ev[1].record()
+                    self.gather_events.append(ev)
+                else:
+                    self.ops.gather_chunk(c)
                 if self.collective and not self.peer_broadcast:
                     region = x_next[c * span:(c + 1) * span]
                     mine = region[self.rank * self.block_rows:(self.rank + 1) * self.block_rows]
