@@ -23,17 +23,6 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 // GEMPE_TRACE=1 prints the construction phases' wall time to stderr
-struct PhaseTimer {
-  bool on = std::getenv("GEMPE_TRACE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void lap(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[gempe] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
-    t = now;
-  }
-};
-
 thread_local std::string g_create_error;
 
 int code_of(const std::exception& e) {

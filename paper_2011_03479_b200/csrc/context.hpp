@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -14,6 +17,18 @@
 namespace gempe {
 
 void cuda_check(cudaError_t e, const char* what);
+
+// GEMPE_TRACE=1: wall-clock laps of the host-side phases (construction, run, export) on stderr
+struct PhaseTimer {
+  bool on = std::getenv("GEMPE_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gempe] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
 void set_create_error(const std::string& msg);  // read back through gempe_last_error(NULL)
 
 // Owning device allocation (cudaMalloc/cudaFree), zero-filled on request.

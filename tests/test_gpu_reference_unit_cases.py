@@ -109,3 +109,15 @@ def test_fixed_seed_reproduces_the_run(G):
     b = G.embed(G.Graph(n, src, dst), 2, cfg, 6)
     assert np.array_equal(a.embedding.view(np.uint32), b.embedding.view(np.uint32))
     assert np.array_equal(a.pe_trace, b.pe_trace)
+
+
+def test_result_download_through_the_staging_ring(G, monkeypatch):
+    """embed() exports the embedding through a ring of pinned chunks drained by host threads (large results); with a tiny
+    chunk size a small result takes the same path, ring wrap-around and ragged last chunk included."""
+    n, src, dst = er_graph(1201, 6000, 4)
+    cfg = G.IterationConfig(max_iters=6, deterministic=True)
+    plain = G.embed(G.Graph(n, src, dst), 7, cfg, 2)
+    monkeypatch.setenv("GEMPE_DOWNLOAD_CHUNK", "1000")  # 1201 * 7 * 4 bytes = 33.6 chunks, ring of 6
+    staged = G.embed(G.Graph(n, src, dst), 7, cfg, 2)
+    assert np.array_equal(plain.embedding.view(np.uint32), staged.embedding.view(np.uint32))
+    assert np.isfinite(staged.embedding).all() and np.abs(staged.embedding).sum() > 0
