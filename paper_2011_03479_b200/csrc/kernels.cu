@@ -2541,7 +2541,16 @@ int launch_gather(const GatherArgs& a, std::uint32_t lo, std::uint32_t hi, bool 
   if (ld <= 8) gather_batched_go<2, 1, 4, 2, 2, 128, 12>(a, lo, hi, precise, stream);
   else if (ld <= 16) gather_batched_go<4, 1, 4, 4, 2, 128, 8>(a, lo, hi, precise, stream);
   else if (ld <= 32) gather_batched_go<8, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);
+  // d = 64 (c3, gather ms): 16 lanes per row, 8 rows per group, 64 registers 0.269; 8 lanes per row, 4 groups x 4 rows, 80
+  // registers 0.289 (-DGEMPE_D64_ROW_LANES=8)
+#ifndef GEMPE_D64_ROW_LANES
+#define GEMPE_D64_ROW_LANES 16
+#endif
+#if GEMPE_D64_ROW_LANES == 16
   else if (ld <= 64) gather_batched_go<16, 1, 4, 8, 1, 128, 8>(a, lo, hi, precise, stream);  // 8 rows per group, 32 warps/SM
+#else
+  else if (ld <= 64) gather_batched_go<8, 2, 4, 4, 1, 128, 6>(a, lo, hi, precise, stream);
+#endif
 #ifndef GEMPE_D128_ROW_LANES
 #define GEMPE_D128_ROW_LANES 32
 #endif
