@@ -160,13 +160,21 @@ void map_back(gempe_engine* e, const float* x_dev, const std::vector<std::uint32
   if (e->n == 0) return;
   PhaseTimer timer;
   DeviceBuffer<std::uint32_t> d_map;
-  DeviceBuffer<float> packed;
+  DeviceBuffer<float> own;
   d_map.upload(to_work);
-  packed.allocate(static_cast<std::size_t>(e->n) * e->dim);
-  c->launches += launch_permute_rows(x_dev, c->ld, packed.get(), e->dim, e->dim, e->n, d_map.get(), false, c->stream);
+  // the rows are packed (un-relabelled, pitch dim) into the round's OUTPUT buffer, which holds nothing once the round is
+  // over and is rewritten by the next one -- no half-gigabyte allocation per export.  A group's buffers are written by
+  // peers, and the snapshot may itself live there: those cases get a buffer of their own.
+  const std::size_t floats = static_cast<std::size_t>(e->n) * e->dim;
+  float* packed = c->x[c->cur ^ 1].get();
+  if (e->group || x_dev == packed || c->x[c->cur ^ 1].size() < floats) {
+    own.allocate(floats);
+    packed = own.get();
+  }
+  c->launches += launch_permute_rows(x_dev, c->ld, packed, e->dim, e->dim, e->n, d_map.get(), false, c->stream);
   cuda_check(cudaStreamSynchronize(c->stream), "map_back");
   timer.lap("export: un-relabel (device)");
-  download_to_pageable(out, packed.get(), packed.size() * sizeof(float), c->stream);
+  download_to_pageable(out, packed, floats * sizeof(float), c->stream);
   timer.lap("export: download");
 }
 
