@@ -1,8 +1,12 @@
+"""Phases of one embed() call on a BASELINE configuration (GEMPE_TRACE=1 prints the laps of construction, run and export):
+
+    GEMPE_TRACE=1 python tools/embed_trace.py [c4]
+"""
 import sys, time, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2011_03479_b200 as P
 from paper_2011_03479_b200 import graphgen
-n, src, dst, dim, k, _, init, std = graphgen.make_config('c4', device=torch.device('cuda', 0))
+n, src, dst, dim, k, _, init, std = graphgen.make_config(sys.argv[1] if len(sys.argv) > 1 else 'c4', device=torch.device('cuda', 0))
 s, d = np.ascontiguousarray(src, np.uint32), np.ascontiguousarray(dst, np.uint32)
 cfg = P.IterationConfig(max_iters=20, convergence_window=21)
 for rep in range(3):
