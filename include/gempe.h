@@ -282,6 +282,12 @@ uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels la
  * indexed spill list (waits for the stream); -1 when the context does not use slotted buckets.  Diagnostics / tests. */
 int64_t gempe_bucket_spills(gempe_ctx* ctx);
 
+/* Device memory of destroyed contexts / engines is kept in a per-device cache and reused by the
+ * next ones: a process that calls embed() repeatedly does not pay cudaMalloc / cudaFree for gigabytes per call.  The cache
+ * holds at most GEMPE_DEVICE_CACHE_MB megabytes (environment, default 16384; 0 disables it); this call returns all of it
+ * to the driver.  No reference analogue (the reference allocates host vectors). */
+void gempe_trim_device_cache(void);
+
 /* ---- Several GPUs in ONE process: the C++ multi-GPU host (`devices[], n_devices` of the proposed
  * constructor).  A group is one context per listed device (a device may be listed more than once: several ranks on one
  * GPU, used by the tests), vertices sharded contiguously over the ranks, every rank holding the full X_t, CSR and edge

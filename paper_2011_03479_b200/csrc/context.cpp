@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <map>
+#include <mutex>
 
 namespace gempe {
 
@@ -20,9 +22,92 @@ void cuda_check(cudaError_t e, const char* what) {
   }
 }
 
+// ---- device memory cache (context.hpp) ------------------------------------------------------------------------------
+namespace {
+constexpr std::size_t kLarge = 1u << 20, kGranule = 2u << 20, kSmallGranule = 512;
+struct DeviceCache {
+  std::mutex mutex;
+  std::map<int, std::multimap<std::size_t, void*>> blocks;  // device -> capacity -> block
+  std::size_t bytes = 0;
+  std::size_t limit = [] {
+    const char* e = std::getenv("GEMPE_DEVICE_CACHE_MB");
+    return static_cast<std::size_t>(e ? std::max(0ll, std::atoll(e)) : 16384ll) << 20;
+  }();
+};
+DeviceCache& device_cache() {
+  static DeviceCache* cache = new DeviceCache;  // never destroyed: buffers may be released during process teardown
+  return *cache;
+}
+}  // namespace
+
+void trim_device_cache() noexcept {
+  DeviceCache& c = device_cache();
+  std::lock_guard<std::mutex> lock(c.mutex);
+  int before = 0;
+  cudaGetDevice(&before);
+  for (auto& dev : c.blocks) {
+    cudaSetDevice(dev.first);
+    for (auto& b : dev.second) cudaFree(b.second);
+    dev.second.clear();
+  }
+  c.bytes = 0;
+  cudaSetDevice(before);
+}
+
+void* device_alloc(std::size_t bytes, std::size_t* capacity, int* device) {
+  cuda_check(cudaGetDevice(device), "cudaGetDevice");
+  void* p = nullptr;
+  std::size_t want = bytes;
+  DeviceCache& c = device_cache();
+  if (c.limit) {
+    const std::size_t granule = bytes >= kLarge ? kGranule : kSmallGranule;
+    want = (bytes + granule - 1) / granule * granule;
+    std::lock_guard<std::mutex> lock(c.mutex);
+    auto& blocks = c.blocks[*device];
+    auto it = blocks.lower_bound(want);
+    if (it != blocks.end() && it->first <= want + want / 4) {  // close enough in size: at most a quarter wasted
+      p = it->second;
+      *capacity = it->first;
+      c.bytes -= it->first;
+      blocks.erase(it);
+      return p;
+    }
+  }
+  cudaError_t err = cudaMalloc(&p, want);
+  if (err == cudaErrorMemoryAllocation) {  // what the cache holds may be what is missing
+    cudaGetLastError();
+    trim_device_cache();
+    err = cudaMalloc(&p, want);
+  }
+  cuda_check(err, "cudaMalloc");
+  *capacity = want;
+  return p;
+}
+
+void device_free(void* p, std::size_t capacity, int device) noexcept {
+  if (!p) return;
+  DeviceCache& c = device_cache();
+  int before = 0;
+  cudaGetDevice(&before);
+  if (before != device) cudaSetDevice(device);
+  bool kept = false;
+  if (c.limit) {
+    // cudaFree waits for work that still uses the block; a block that is handed to the next owner must be idle too
+    if (cudaDeviceSynchronize() == cudaSuccess) {
+      std::lock_guard<std::mutex> lock(c.mutex);
+      if (c.bytes + capacity <= c.limit) {
+        c.blocks[device].emplace(capacity, p);
+        c.bytes += capacity;
+        kept = true;
+      }
+    }
+  }
+  if (!kept) cudaFree(p);
+  if (before != device) cudaSetDevice(before);
+}
+
 namespace {
 
-// GEMPE_TRACE=1 prints the construction phases' wall time to stderr
 thread_local std::string g_create_error;
 
 int code_of(const std::exception& e) {
@@ -776,7 +861,9 @@ int gempe_create(gempe_ctx** out, std::uint32_t n, std::uint64_t m, const std::u
 void gempe_destroy(gempe_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->opt.device);
+  PhaseTimer timer;
   delete c;
+  timer.lap("destroy: whole context");
 }
 
 const char* gempe_last_error(const gempe_ctx* c) { return c ? c->error.c_str() : g_create_error.c_str(); }
@@ -1462,6 +1549,8 @@ int gempe_elapsed_ms(gempe_ctx* c, float out3[3]) {
 }
 
 std::uint64_t gempe_kernel_launches(const gempe_ctx* c) { return c->launches; }
+
+void gempe_trim_device_cache(void) { trim_device_cache(); }
 
 std::int64_t gempe_bucket_spills(gempe_ctx* c) {
   if (!c->in_stride) return -1;

@@ -31,7 +31,17 @@ struct PhaseTimer {
 };
 void set_create_error(const std::string& msg);  // read back through gempe_last_error(NULL)
 
-// Owning device allocation (cudaMalloc/cudaFree), zero-filled on request.
+// Device memory behind DeviceBuffer.  Released blocks go to a per-device cache instead of cudaFree and are handed out again
+// to requests of (nearly) the same size: an engine is a few dozen allocations from bytes to gigabytes, and a process that
+// calls embed() repeatedly otherwise pays cudaMalloc / cudaFree for all of them every call.  On the bench host it is the
+// cudaFree of the SMALL blocks that hurts: destroying a c4 engine took 1 ms or, every second time, 0.1-0.55 s; with the
+// cache a call is 0.19 s every time (was 0.20-1.2 s).  The cache holds at most GEMPE_DEVICE_CACHE_MB (default 16384; 0
+// turns it off); gempe_trim_device_cache() empties it.  `capacity` is what device_free must be given back.
+void* device_alloc(std::size_t bytes, std::size_t* capacity, int* device);
+void device_free(void* p, std::size_t capacity, int device) noexcept;
+void trim_device_cache() noexcept;
+
+// Owning device allocation, zero-filled on request.
 template <typename T>
 class DeviceBuffer {
  public:
@@ -41,9 +51,9 @@ class DeviceBuffer {
   ~DeviceBuffer() { release(); }
   void allocate(std::size_t count, bool zero = false) {
     release();
-    count_ = count;
     if (count == 0) return;
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ptr_), count * sizeof(T)), "cudaMalloc");
+    ptr_ = static_cast<T*>(device_alloc(count * sizeof(T), &capacity_, &device_));
+    count_ = count;
     if (zero) {
       // the legacy-stream memset is not ordered against the context's non-blocking stream: wait for it
       cuda_check(cudaMemset(ptr_, 0, count * sizeof(T)), "cudaMemset");
@@ -59,20 +69,24 @@ class DeviceBuffer {
     }
   }
   void release() {
-    if (ptr_) cudaFree(ptr_);
+    if (ptr_) device_free(ptr_, capacity_, device_);
     ptr_ = nullptr;
     count_ = 0;
+    capacity_ = 0;
   }
   T* get() const { return ptr_; }
   std::size_t size() const { return count_; }
   void swap(DeviceBuffer& o) {
     std::swap(ptr_, o.ptr_);
     std::swap(count_, o.count_);
+    std::swap(capacity_, o.capacity_);
+    std::swap(device_, o.device_);
   }
 
  private:
   T* ptr_ = nullptr;
-  std::size_t count_ = 0;
+  std::size_t count_ = 0, capacity_ = 0;
+  int device_ = 0;
 };
 
 }  // namespace gempe

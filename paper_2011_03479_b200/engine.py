@@ -620,6 +620,11 @@ def embed(g: Graph, dim: int, cfg: Optional[IterationConfig] = None, seed: int =
         engine.close()
 
 
+def trim_device_cache():
+    """Returns the device memory cached from destroyed contexts / engines to the driver (gempe_trim_device_cache)."""
+    _capi.load().gempe_trim_device_cache()
+
+
 # ---- host numerics (no GPU) ----------------------------------------------------------------------------
 def fastmath_table(which: int):
     out = np.zeros(67, np.float64)

@@ -225,3 +225,22 @@ def test_device_sigma_search_on_special_tallies(G):
     s_dev, _, _ = device_search(sym_e, sym_n, 16.0)  # previous sigma at the ceiling: the growth cap does not bind
     assert abs(s_dev - s2) <= 1e-9 * s2
     ctx.close()
+
+
+def test_device_memory_cache_reuses_blocks_without_changing_results(G):
+    """Device memory of a destroyed engine is kept and handed to the next one (context.hpp: device_alloc): same results,
+    no growth of the process's device memory on the second call, everything back at the driver after a trim."""
+    import torch
+    n, src, dst = er_graph(20000, 200000, 3)
+    g = G.Graph(n, src, dst)
+    cfg = G.IterationConfig(max_iters=4, deterministic=True)
+    G.trim_device_cache()
+    a = G.embed(g, 32, cfg, 5)
+    free_after_first = torch.cuda.mem_get_info()[0]
+    b = G.embed(g, 32, cfg, 5)
+    assert np.array_equal(a.embedding.view(np.uint32), b.embedding.view(np.uint32)) and np.array_equal(a.pe_trace, b.pe_trace)
+    assert torch.cuda.mem_get_info()[0] >= free_after_first - (8 << 20)
+    G.trim_device_cache()
+    assert torch.cuda.mem_get_info()[0] >= free_after_first + (16 << 20)
+    c = G.embed(g, 32, cfg, 5)  # and from a cold cache again
+    assert np.array_equal(a.embedding.view(np.uint32), c.embedding.view(np.uint32))

@@ -9,7 +9,7 @@ from paper_2011_03479_b200 import graphgen
 n, src, dst, dim, k, _, init, std = graphgen.make_config(sys.argv[1] if len(sys.argv) > 1 else 'c4', device=torch.device('cuda', 0))
 s, d = np.ascontiguousarray(src, np.uint32), np.ascontiguousarray(dst, np.uint32)
 cfg = P.IterationConfig(max_iters=20, convergence_window=21)
-for rep in range(3):
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     t0 = time.perf_counter()
     g = P.Graph(n, s, d)
     t1 = time.perf_counter()
