@@ -848,3 +848,51 @@ def test_slotted_buckets_overflow_into_the_spill_list(G, oracle, golden_fastmath
     assert np.array_equal(he, want["hist_edge"]) and np.array_equal(hn, want["hist_nonedge"])
     assert rel_l2(y, want["y"]) <= TOL and rel_l2(z, want["z"]) <= TOL and rel_l2(ctx.get_coords(), want["x_next"]) <= TOL
     ctx.close()
+
+
+# ------------------------------------------------------------------------------------- randomized sweep
+
+def _random_graph(rng, n, m):
+    """m distinct undirected edges without self-loops (fewer when the graph is too small), ids in random order."""
+    pairs = set()
+    limit = n * (n - 1) // 2
+    while len(pairs) < min(m, limit):
+        a, b = (int(v) for v in rng.integers(0, n, 2))
+        if a != b and (b, a) not in pairs:
+            pairs.add((a, b))
+    e = np.array(sorted(pairs), dtype=np.uint32).reshape(-1, 2)
+    rng.shuffle(e)
+    return n, e[:, 0].copy(), e[:, 1].copy()
+
+
+@pytest.mark.parametrize("case", range(64))
+def test_randomized_shapes_modes_and_switches(G, oracle, golden_fastmath, case):
+    """Seeded random draws over what the fixed cases hold constant: vertex counts from 3 up, sparse to near-dense graphs
+    (isolated vertices, hubs), odd dimensions, both sampling schemes with odd k, every bucketing mode, hub splitting,
+    exact / table math, literal / fp32 distances, relabelling on and off -- two rounds each against the C oracle."""
+    rng = np.random.default_rng(1000 + case)
+    n = int(rng.choice([3, 4, 5, 17, 64, 257, 1000, 4099]))
+    density = float(rng.choice([0.002, 0.02, 0.2, 0.6]))
+    m = min(60000, max(1, int(density * n * (n - 1) / 2)))
+    if n * (n - 1) // 2 - m < n:  # keep non-edge sampling feasible (the sampler gives up after 10^4 draws)
+        m = max(1, n * (n - 1) // 2 - n)
+    g = _random_graph(rng, n, m)
+    dim = int(rng.choice([1, 2, 3, 7, 13, 33, 64, 65, 127, 128, 129, 200]))
+    neg_mode = int(rng.integers(0, 2))
+    k = int(rng.choice([1, 2, 3, 9])) if neg_mode else 0
+    kw = dict(bucket_mode=int(rng.choice([0, 1, 2, 3, 4])), relabel=bool(rng.integers(0, 2)),
+              precise_distance=bool(rng.integers(0, 2)))
+    if rng.integers(0, 2):
+        kw["chunk_entries"] = int(rng.choice([4, 16, 64]))
+    seed, exact, sigma0 = int(rng.integers(1, 1 << 30)), bool(rng.integers(0, 2)), float(rng.choice([0.3, 1.0, 2.5]))
+    try:
+        check_round(G, oracle, golden_fastmath, g, dim, seed=seed, neg_mode=neg_mode, k=k, exact=exact, iters=2,
+                    sigma0=sigma0, **kw)
+    except G.NearCompleteGraphError:
+        # a vertex adjacent (or hash-aliased) to every other one: the reference gives up after 10^4 draws
+        # (sampler.cpp:18-21), and so must the oracle on the same work graph
+        ctx = G.Context(G.Graph(*g), dim, seed, neg_mode=neg_mode, negatives=k, **kw)
+        want = oracle_round(oracle, ctx, ctx.get_coords(), neg_mode, k, seed, 0, 1.5, sigma0,
+                            None if exact else golden_fastmath)
+        ctx.close()
+        assert want["rc"] != 0
