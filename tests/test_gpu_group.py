@@ -104,3 +104,31 @@ def test_engine_sharded_over_a_device_list_equals_the_single_gpu_engine(G):
     assert np.array_equal(many.pe_trace, one.pe_trace) and many.final_sigma == one.final_sigma
     assert np.array_equal(many.embedding.view(np.uint32), one.embedding.view(np.uint32))
     assert np.array_equal(many.last_hist_nonedge, one.last_hist_nonedge)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_randomized_groups_are_bit_identical_to_one_context(G, case):
+    """Seeded random draws over world size (1-7 ranks), exchange path, graph shape, dimension, sampling scheme and hub
+    split: three rounds of the group equal three rounds of one context bit for bit (deterministic mode)."""
+    rng = np.random.default_rng(7000 + case)
+    n = int(rng.choice([40, 300, 1500, 5000]))
+    n, src, dst = er_graph(n, int(n * rng.choice([2, 6, 15])), int(rng.integers(1, 1000)))
+    if rng.integers(0, 3) == 0:
+        n, src, dst = star_plus_ring(max(n // 4, 30), hubs=int(rng.integers(1, 4)))
+    dim = int(rng.choice([2, 3, 16, 64, 100, 128]))
+    mode = int(rng.integers(0, 2))
+    kw = dict(neg_mode=mode, negatives=int(rng.choice([1, 4, 11])) if mode else 0)
+    if rng.integers(0, 2):
+        kw["chunk_entries"] = int(rng.choice([8, 32]))
+    world, copy_engines, seed = int(rng.integers(1, 8)), bool(rng.integers(0, 2)), int(rng.integers(1, 1 << 20))
+    g = G.Graph(n, src, dst)
+    want, x_want = _single_rounds(G, g, dim, seed, 3, **kw)
+    grp = G.Group(g, dim, seed, devices=[0] * world, copy_engines=copy_engines, deterministic=True, **kw)
+    sigma = 1.0
+    for it in range(3):
+        he, hn = grp.iterate(1.5, sigma, it)
+        assert (he.tolist(), hn.tolist()) == want[it], (case, it)
+        sigma = min(sigma * 1.4, 2.5)
+    assert grp.replicas_agree()
+    assert np.array_equal(grp.get_coords().view(np.uint32), x_want.view(np.uint32))
+    grp.close()
