@@ -896,3 +896,29 @@ def test_randomized_shapes_modes_and_switches(G, oracle, golden_fastmath, case):
                             None if exact else golden_fastmath)
         ctx.close()
         assert want["rc"] != 0
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_randomized_queued_runs_equal_the_stepwise_loop(G, case):
+    """Seeded random run-level settings (iteration budget, convergence window and tolerance, re-relabel period, rounds per
+    host round trip, sampling scheme): the loop on the device equals the host loop bit for bit."""
+    from dataclasses import replace
+    rng = np.random.default_rng(9000 + case)
+    n = int(rng.choice([60, 250, 900]))
+    g3 = er_graph(n, int(n * rng.choice([3, 8])), int(rng.integers(1, 1000)))
+    mode = int(rng.integers(0, 2))
+    cfg = G.IterationConfig(deterministic=True, max_iters=int(rng.integers(3, 70)),
+                            convergence_window=int(rng.choice([2, 5, 9])),
+                            convergence_tol=float(rng.choice([0.0, 1e-4, 1e-2])),
+                            relabel_period=int(rng.choice([0, 0, 4, 7])), neg_mode=mode,
+                            negatives=int(rng.choice([2, 5])) if mode else 0)
+    dim, seed = int(rng.choice([2, 5, 32, 128])), int(rng.integers(1, 1 << 20))
+    g = G.Graph(*g3)
+    want = _stepwise_run(G, g, dim, cfg, seed)
+    got = G.embed(g, dim, replace(cfg, batch_rounds=int(rng.choice([0, 1, 2, 5, 16]))), seed)
+    assert got.iterations == want.iterations and got.converged == want.converged
+    assert np.array_equal(got.pe_trace, want.pe_trace) and got.final_sigma == want.final_sigma
+    assert np.array_equal(got.last_hist_edge, want.last_hist_edge)
+    assert np.array_equal(got.last_hist_nonedge, want.last_hist_nonedge)
+    assert np.array_equal(got.relabel_forward, want.relabel_forward)
+    assert np.array_equal(got.embedding.view(np.uint32), want.embedding.view(np.uint32))
