@@ -922,3 +922,36 @@ def test_randomized_queued_runs_equal_the_stepwise_loop(G, case):
     assert np.array_equal(got.last_hist_nonedge, want.last_hist_nonedge)
     assert np.array_equal(got.relabel_forward, want.relabel_forward)
     assert np.array_equal(got.embedding.view(np.uint32), want.embedding.view(np.uint32))
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_randomized_engines_next_to_the_unmodified_reference(G, ref, case):
+    """Seeded random graphs, dimensions, worker / lane counts and math policies: the UNMODIFIED reference engine
+    (oracle/_ref) and the GPU engine start from the same work graph and layout bit for bit; over four free-running
+    rounds the consolidated (y, z) and the layout stay within 1e-4, sigma and the PE estimate within 1e-3."""
+    import oracle as O
+    rng = np.random.default_rng(11000 + case)
+    n = int(rng.choice([30, 200, 1200, 5000]))
+    g3 = er_graph(n, int(n * rng.choice([2, 5, 12])), int(rng.integers(1, 1000)))
+    if rng.integers(0, 4) == 0:
+        g3 = star_plus_ring(max(n // 3, 40), hubs=int(rng.integers(1, 4)))
+    n, src, dst = g3
+    dim, seed, fast = int(rng.choice([1, 2, 3, 10, 64, 128, 130])), int(rng.integers(1, 1 << 20)), bool(rng.integers(0, 2))
+    want = O.RefEngine(ref, n, src, dst, dim, seed, lane_width=int(rng.choice([1, 4, 16])),
+                       workers=int(rng.choice([1, 2, 5])), fast_math=fast)
+    got = G.EmbeddingEngine(G.Graph(n, src, dst), dim, G.IterationConfig(fast_math=fast), seed)
+    gs, gd, _ = got.work_graph()
+    ws, wd = want.work_graph()
+    assert np.array_equal(gs, ws) and np.array_equal(gd, wd)
+    assert np.array_equal(got.work_coords().view(np.uint32), want.work_coords().view(np.uint32))
+    ctx = got.context()
+    ctx.set_capture(True)
+    for it in range(4):
+        w = want.iterate(capture=True)
+        s = got.run_single_iteration()
+        y, z = ctx.get_yz()
+        assert rel_l2(z, w["z"]) <= TOL and rel_l2(y, w["y"]) <= TOL, (case, it)
+        assert rel_l2(got.work_coords(), want.work_coords()) <= TOL, (case, it)
+        assert abs(s.sigma - w["sigma"]) <= 1e-3 * w["sigma"]
+        assert abs(s.pe_estimate - w["pe_estimate"]) <= 1e-3 * abs(w["pe_estimate"])
+    got.close()
