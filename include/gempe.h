@@ -282,6 +282,15 @@ uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels la
  * indexed spill list (waits for the stream); -1 when the context does not use slotted buckets.  Diagnostics / tests. */
 int64_t gempe_bucket_spills(gempe_ctx* ctx);
 
+/* Page-locked host memory for a caller without CUDA headers (cudaHostAlloc / cudaFreeHost), e.g. the coordinate vectors
+ * handed to gempe_step_host or gempe_set_coords / gempe_get_coords every round.  Copies from and to ordinary pageable memory
+ * are staged by the driver at a fraction of the PCIe rate: BASELINE config 4, gempe_step_host, 89 ms per step on pageable
+ * vectors against 20 ms on these.  (Registering the caller's own pages with cudaHostRegister is NOT offered: on the bench
+ * host the step then takes 139 ms -- DMA over scattered 4 KB pages.)  gempe_alloc_host returns NULL on failure (message
+ * through gempe_last_error(NULL)).  No reference analogue. */
+void* gempe_alloc_host(uint64_t bytes);
+void gempe_free_host(void* ptr);
+
 /* Device memory of destroyed contexts / engines is kept in a per-device cache and reused by the
  * next ones: a process that calls embed() repeatedly does not pay cudaMalloc / cudaFree for gigabytes per call.  The cache
  * holds at most GEMPE_DEVICE_CACHE_MB megabytes (environment, default 16384; 0 disables it); this call returns all of it

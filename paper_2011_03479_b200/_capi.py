@@ -31,7 +31,7 @@ SYMBOLS = [
     "gempe_block_rows", "gempe_begin_round", "gempe_begin_round_auto", "gempe_exchange_layout", "gempe_bucket_received", "gempe_gather_chunk", "gempe_coords_ipc_handles", "gempe_open_peer",
     "gempe_add_peer_pointers", "gempe_clear_peers", "gempe_exchange_ipc_handle", "gempe_open_peer_exchange",
     "gempe_add_peer_exchange_pointer", "gempe_exchange_recv_area", "gempe_device_coords_parity", "gempe_coords_parity", "gempe_end_round", "gempe_elapsed_ms",
-    "gempe_kernel_launches", "gempe_bucket_spills", "gempe_trim_device_cache", "gempe_host_fastmath_table", "gempe_host_optimize_sigma",
+    "gempe_kernel_launches", "gempe_bucket_spills", "gempe_trim_device_cache", "gempe_alloc_host", "gempe_free_host", "gempe_host_fastmath_table", "gempe_host_optimize_sigma",
     "gempe_host_histogram_objective", "gempe_host_histogram_objective_dsigma", "gempe_host_random_relabel",
     "gempe_host_mix_seed", "gempe_default_iteration_config", "gempe_engine_create", "gempe_engine_create_multi", "gempe_engine_destroy",
     "gempe_engine_last_error", "gempe_engine_context", "gempe_engine_degenerate", "gempe_engine_iteration",
@@ -153,6 +153,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "gempe_group_replicas_agree": (i32, [vp]),
         "gempe_bucket_spills": (C.c_int64, [vp]),
         "gempe_trim_device_cache": (None, []),
+        "gempe_alloc_host": (vp, [u64]),
+        "gempe_free_host": (None, [vp]),
         "gempe_set_capture": (i32, [vp, i32]),
         "gempe_get_yz": (i32, [vp, vp, vp]),
         "gempe_get_yz_rows": (i32, [vp, vp, u64, vp, vp]),

@@ -1552,6 +1552,21 @@ std::uint64_t gempe_kernel_launches(const gempe_ctx* c) { return c->launches; }
 
 void gempe_trim_device_cache(void) { trim_device_cache(); }
 
+void* gempe_alloc_host(std::uint64_t bytes) {
+  void* p = nullptr;
+  const cudaError_t err = cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    set_create_error(std::string("cudaHostAlloc: ") + cudaGetErrorString(err));
+    return nullptr;
+  }
+  return p;
+}
+
+void gempe_free_host(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
 std::int64_t gempe_bucket_spills(gempe_ctx* c) {
   if (!c->in_stride) return -1;
   std::uint32_t count = 0;

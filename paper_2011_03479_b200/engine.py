@@ -625,6 +625,23 @@ def trim_device_cache():
     _capi.load().gempe_trim_device_cache()
 
 
+def alloc_host(shape, dtype=np.float32) -> np.ndarray:
+    """A numpy array on page-locked host memory (gempe_alloc_host): step_host / set_coords / get_coords on it run at the
+    PCIe rate.  Release it with free_host(array) -- not by dropping the last reference."""
+    L = _capi.load()
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape))
+    p = L.gempe_alloc_host(max(1, count * dt.itemsize))
+    if not p:
+        raise CudaError((L.gempe_last_error(None) or b"").decode())
+    buf = (C.c_char * (count * dt.itemsize)).from_address(p)
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
+def free_host(a: np.ndarray):
+    _capi.load().gempe_free_host(C.c_void_p(a.ctypes.data))
+
+
 # ---- host numerics (no GPU) ----------------------------------------------------------------------------
 def fastmath_table(which: int):
     out = np.zeros(67, np.float64)

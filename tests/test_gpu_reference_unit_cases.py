@@ -244,3 +244,24 @@ def test_device_memory_cache_reuses_blocks_without_changing_results(G):
     assert torch.cuda.mem_get_info()[0] >= free_after_first + (16 << 20)
     c = G.embed(g, 32, cfg, 5)  # and from a cold cache again
     assert np.array_equal(a.embedding.view(np.uint32), c.embedding.view(np.uint32))
+
+
+def test_page_locked_buffers_through_the_abi(G):
+    """gempe_alloc_host / gempe_free_host: a caller without CUDA headers gets page-locked coordinate vectors; the round on
+    them gives the same bits as on pageable memory."""
+    n, src, dst = er_graph(3000, 20000, 6)
+    ctx = G.Context(G.Graph(n, src, dst), 32, 3, deterministic=True)
+    x0 = ctx.get_coords()
+    plain_in, plain_out = x0.copy(), np.zeros_like(x0)
+    he0, hn0 = ctx.step_host(plain_in, plain_out, 1.5, 1.0, 0)
+    pin_in, pin_out = G.alloc_host(x0.shape), G.alloc_host(x0.shape)
+    try:
+        pin_in[:] = x0
+        pin_out[:] = 0
+        he1, hn1 = ctx.step_host(pin_in, pin_out, 1.5, 1.0, 0)
+        assert np.array_equal(he0, he1) and np.array_equal(hn0, hn1)
+        assert np.array_equal(plain_out.view(np.uint32), pin_out.view(np.uint32))
+    finally:
+        G.free_host(pin_in)
+        G.free_host(pin_out)
+    ctx.close()
