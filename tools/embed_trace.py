@@ -2,8 +2,8 @@
 
     GEMPE_TRACE=1 python tools/embed_trace.py [c4]
 """
-import sys, time, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+import os, sys, time, numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2011_03479_b200 as P
 from paper_2011_03479_b200 import graphgen
 n, src, dst, dim, k, _, init, std = graphgen.make_config(sys.argv[1] if len(sys.argv) > 1 else 'c4', device=torch.device('cuda', 0))
