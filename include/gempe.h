@@ -125,7 +125,8 @@ int gempe_iterate(gempe_ctx* ctx, double mu, double sigma, uint64_t iter_index,
                   uint64_t* hist_edge, uint64_t* hist_nonedge);
 
 /* The round as a pure function on HOST buffers (what a caller that keeps the coordinates on the host pays):
- * x_in (X_t, n*dim, WORK indexing, ideally pinned) is copied in while the sampling passes run, the gradient/update
+ * x_in (X_t, n*dim, WORK indexing; page-locked memory is fastest, pageable memory takes the library's staged path) is
+ * copied in while the sampling passes run, the gradient/update
  * kernel runs in slices, and each finished slice of X_{t+1} is copied to x_out while the next slice is computed.
  * Equivalent to gempe_set_coords + gempe_iterate + gempe_get_coords.  Unsharded contexts only. */
 int gempe_step_host(gempe_ctx* ctx, const float* x_in, float* x_out, double mu, double sigma, uint64_t iter_index,
@@ -283,11 +284,11 @@ uint64_t gempe_kernel_launches(const gempe_ctx* ctx);              /* kernels la
 int64_t gempe_bucket_spills(gempe_ctx* ctx);
 
 /* Page-locked host memory for a caller without CUDA headers (cudaHostAlloc / cudaFreeHost), e.g. the coordinate vectors
- * handed to gempe_step_host or gempe_set_coords / gempe_get_coords every round.  Copies from and to ordinary pageable memory
- * are staged by the driver at a fraction of the PCIe rate: BASELINE config 4, gempe_step_host, 89 ms per step on pageable
- * vectors against 20 ms on these.  (Registering the caller's own pages with cudaHostRegister is NOT offered: on the bench
- * host the step then takes 139 ms -- DMA over scattered 4 KB pages.)  gempe_alloc_host returns NULL on failure (message
- * through gempe_last_error(NULL)).  No reference analogue. */
+ * handed to gempe_step_host every round.  BASELINE config 4, gempe_step_host: 20 ms per step on these; 35-45 ms on ordinary
+ * pageable vectors, which the library moves through its own ring of pinned chunks and host threads (89 ms with the driver's
+ * staging); registering the caller's own pages with cudaHostRegister is NOT offered: on the bench host the step then takes
+ * 139 ms -- DMA over scattered 4 KB pages.  gempe_alloc_host returns NULL on failure (message through
+ * gempe_last_error(NULL)).  No reference analogue. */
 void* gempe_alloc_host(uint64_t bytes);
 void gempe_free_host(void* ptr);
 

@@ -19,7 +19,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 CU_SOURCES = ["kernels.cu"]
-CXX_SOURCES = ["hostmath.cpp", "context.cpp", "engine.cpp", "group.cpp", "formats.cpp"]
+CXX_SOURCES = ["hostmath.cpp", "context.cpp", "engine.cpp", "group.cpp", "formats.cpp", "hostcopy.cpp"]
 HEADERS = ["kernels.hpp", "context.hpp", "hostmath.hpp", "device_fns.cuh", os.path.join(ROOT, "include", "gempe.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -41,6 +41,12 @@ void* device_alloc(std::size_t bytes, std::size_t* capacity, int* device);
 void device_free(void* p, std::size_t capacity, int device) noexcept;
 void trim_device_cache() noexcept;
 
+// Transfers between the device and pageable host memory through a ring of pinned chunks and several host threads
+// (hostcopy.cpp); both return when the transfer is complete.  is_pageable_host: neither page-locked nor device memory.
+void download_to_pageable(void* dst, const void* src_dev, std::size_t bytes, cudaStream_t stream);
+void upload_from_pageable(void* dst_dev, const void* src, std::size_t bytes, cudaStream_t stream);
+bool is_pageable_host(const void* p);
+
 // Owning device allocation, zero-filled on request.
 template <typename T>
 class DeviceBuffer {

@@ -82,79 +82,6 @@ void rethrow_message(int rc, const std::string& msg) {
 
 // original-indexed export of a work-indexed device layout (engine.cpp:327-337, 376-381): rows gathered on the
 // device, one transfer into the caller's buffer
-// Device -> pageable host memory, fast: the driver's own path for a pageable destination stages through one pinned
-// buffer and copies out of it with one thread (5-10 GB/s, and a freshly allocated destination takes its page faults in
-// that thread).  Here chunks go to a ring of pinned buffers over the copy engine while several host threads move
-// finished chunks to the destination (and take the page faults) in parallel.
-void download_to_pageable(void* dst, const void* src_dev, std::size_t bytes, cudaStream_t stream) {
-  static const int kWorkers = [] {  // host threads draining the ring (bench host, 537 MB: 2 -> 67 ms, 4 -> 36 ms, 8 -> 26 ms)
-    const char* e = std::getenv("GEMPE_DOWNLOAD_THREADS");
-    const int hw = static_cast<int>(std::thread::hardware_concurrency());
-    return e ? std::max(1, std::atoi(e)) : std::min(8, std::max(2, hw / 2));
-  }();
-  const int kRing = 2 * kWorkers;
-  std::size_t kChunk = 4u << 20;
-  if (const char* env = std::getenv("GEMPE_DOWNLOAD_CHUNK")) kChunk = std::max<std::size_t>(256, std::strtoull(env, nullptr, 10));  // tests
-  if (bytes < 4 * kChunk) {
-    cuda_check(cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDeviceToHost, stream), "download");
-    cuda_check(cudaStreamSynchronize(stream), "download");
-    return;
-  }
-  // the ring is allocated once per process and kept (up to 64 MB of pinned memory: allocating it costs 20-60 ms and freeing it
-  // up to 0.4 s on the bench host -- more than the copy); one download at a time uses it
-  static std::mutex ring_mutex;
-  static char* ring = nullptr;
-  static std::size_t ring_bytes = 0;
-  std::lock_guard<std::mutex> ring_lock(ring_mutex);
-  PhaseTimer timer;
-  if (ring_bytes < kRing * kChunk) {
-    if (ring) cudaFreeHost(ring);
-    ring = nullptr;
-    ring_bytes = 0;
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ring), kRing * kChunk, cudaHostAllocPortable), "pinned staging ring");
-    ring_bytes = kRing * kChunk;
-    timer.lap("  download: pinned ring");
-  }
-  std::vector<cudaEvent_t> filled(kRing);
-  for (auto& ev : filled) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-  const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
-  std::vector<std::atomic<int>> drained(chunks);
-  for (auto& d : drained) d.store(0);
-  std::atomic<std::size_t> issued{0};
-  std::atomic<bool> failed{false};
-  int device = 0;
-  cuda_check(cudaGetDevice(&device), "cudaGetDevice");
-  auto worker = [&](int w) {
-    cudaSetDevice(device);
-    for (std::size_t i = w; i < chunks; i += kWorkers) {
-      while (issued.load(std::memory_order_acquire) <= i && !failed.load()) std::this_thread::yield();
-      if (failed.load()) return;
-      if (cudaEventSynchronize(filled[i % kRing]) != cudaSuccess) { failed.store(true); return; }
-      const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-      std::memcpy(static_cast<char*>(dst) + off, ring + (i % kRing) * kChunk, len);
-      drained[i].store(1, std::memory_order_release);
-    }
-  };
-  std::vector<std::thread> pool;
-  for (int w = 0; w < kWorkers; ++w) pool.emplace_back(worker, w);
-  cudaError_t err = cudaSuccess;
-  for (std::size_t i = 0; i < chunks && err == cudaSuccess; ++i) {
-    if (i >= static_cast<std::size_t>(kRing)) {  // the ring slot is free once its previous chunk has been moved out
-      while (!drained[i - kRing].load(std::memory_order_acquire) && !failed.load()) std::this_thread::yield();
-    }
-    const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    err = cudaMemcpyAsync(ring + (i % kRing) * kChunk, static_cast<const char*>(src_dev) + off, len, cudaMemcpyDeviceToHost, stream);
-    if (err == cudaSuccess) err = cudaEventRecord(filled[i % kRing], stream);
-    if (err != cudaSuccess) failed.store(true);
-    issued.store(i + 1, std::memory_order_release);
-  }
-  for (auto& t : pool) t.join();
-  timer.lap("  download: copy + drain");
-  for (auto& ev : filled) cudaEventDestroy(ev);
-  cuda_check(err, "download (staged)");
-  if (failed.load()) throw cuda_error("download (staged): a copy failed");
-}
-
 void map_back(gempe_engine* e, const float* x_dev, const std::vector<std::uint32_t>& to_work, float* out) {
   gempe_ctx* c = e->ctx;
   if (e->n == 0) return;

@@ -265,3 +265,24 @@ def test_page_locked_buffers_through_the_abi(G):
         G.free_host(pin_in)
         G.free_host(pin_out)
     ctx.close()
+
+
+@pytest.mark.parametrize("dim", [2, 32, 128])
+def test_step_host_on_pageable_vectors_through_the_staging_ring(G, monkeypatch, dim):
+    """gempe_step_host with ordinary (pageable) numpy arrays and a tiny ring chunk: upload and slice-by-slice download both
+    go through the pinned ring and its host threads; same bits as set_coords + iterate + get_coords."""
+    n, src, dst = er_graph(2500, 15000, 12)
+    g = G.Graph(n, src, dst)
+    ref_ctx = G.Context(g, dim, 4, deterministic=True)
+    x0 = ref_ctx.get_coords()
+    he0, hn0 = ref_ctx.iterate(1.5, 1.0, 0)
+    x1 = ref_ctx.get_coords()
+    ref_ctx.close()
+    monkeypatch.setenv("GEMPE_DOWNLOAD_CHUNK", "4096")
+    ctx = G.Context(g, dim, 4, deterministic=True)
+    x_in, x_out = x0.copy(), np.full_like(x0, np.nan)
+    he1, hn1 = ctx.step_host(x_in, x_out, 1.5, 1.0, 0)
+    assert np.array_equal(he0, he1) and np.array_equal(hn0, hn1)
+    assert np.array_equal(x_out.view(np.uint32), x1.view(np.uint32))
+    assert np.array_equal(ctx.get_coords().view(np.uint32), x1.view(np.uint32))
+    ctx.close()
