@@ -892,6 +892,11 @@ int gempe_set_coords(gempe_ctx* c, const float* x_work) {
   return guarded(c, [&] {
     if (!x_work) throw config_error("null coordinates");
     if (c->n == 0) return;
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    if (c->dim == c->ld && is_pageable_host(x_work)) {  // ordinary vectors, rows without padding: staged (hostcopy.cpp)
+      upload_from_pageable(c->x[c->cur].get(), x_work, static_cast<std::size_t>(c->n) * c->dim * sizeof(float), c->stream);
+      return;
+    }
     cuda_check(cudaMemcpy2DAsync(c->x[c->cur].get(), c->ld * sizeof(float), x_work, c->dim * sizeof(float),
                                  c->dim * sizeof(float), c->n, cudaMemcpyHostToDevice, c->stream), "set_coords");
     cuda_check(cudaStreamSynchronize(c->stream), "set_coords");
@@ -902,6 +907,11 @@ int gempe_get_coords(gempe_ctx* c, float* x_work) {
   return guarded(c, [&] {
     if (!x_work) throw config_error("null coordinates");
     if (c->n == 0) return;
+    cuda_check(cudaSetDevice(c->opt.device), "cudaSetDevice");
+    if (c->dim == c->ld && is_pageable_host(x_work)) {
+      download_to_pageable(x_work, c->x[c->cur].get(), static_cast<std::size_t>(c->n) * c->dim * sizeof(float), c->stream);
+      return;
+    }
     cuda_check(cudaMemcpy2DAsync(x_work, c->dim * sizeof(float), c->x[c->cur].get(), c->ld * sizeof(float),
                                  c->dim * sizeof(float), c->n, cudaMemcpyDeviceToHost, c->stream), "get_coords");
     cuda_check(cudaStreamSynchronize(c->stream), "get_coords");

@@ -69,7 +69,9 @@ class DeviceBuffer {
   void upload(const std::vector<T>& host) { upload(host.data(), host.size()); }
   void upload(const T* host, std::size_t count) {
     allocate(count);
-    if (count) {
+    if (count * sizeof(T) >= (16u << 20) && is_pageable_host(host)) {  // e.g. the edge arrays of the caller
+      upload_from_pageable(ptr_, host, count * sizeof(T), nullptr);
+    } else if (count) {
       cuda_check(cudaMemcpy(ptr_, host, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
       cuda_check(cudaDeviceSynchronize(), "upload");  // pageable H2D may still be in flight on return
     }
