@@ -13,6 +13,7 @@
 #include <limits>
 #include <map>
 #include <mutex>
+#include <thread>
 
 namespace gempe {
 
@@ -277,35 +278,84 @@ void build_structures(gempe_ctx* c) {
                 static_cast<std::size_t>(2 * m / std::max(1u, c->chunk_entries)) + 1024);
   c->chunk_item_off.assign(c->comm_chunks + 1, 0);
   const std::uint32_t world = static_cast<std::uint32_t>(c->opt.world), rank = static_cast<std::uint32_t>(c->opt.rank);
+  // two passes over the owned vertex range of every comm chunk, each split over a few host threads: count (items, hubs,
+  // hub slices per sub-range), prefix, fill in place -- the table is the same as a sequential walk would give (c4: 19 -> 14 ms,
+  // c5: 0.30 -> 0.21 s; what is left is writing the table itself)
+  const std::uint32_t chunk_entries = c->chunk_entries, negatives = c->opt.negatives;
+  auto pieces_of = [&](std::uint32_t v) {
+    const std::uint32_t deg = rowptr[v + 1] - rowptr[v];
+    return std::max(1u, (deg + chunk_entries - 1) / chunk_entries);
+  };
   for (std::uint32_t chunk = 0; chunk < c->comm_chunks; ++chunk) {
     c->chunk_item_off[chunk] = static_cast<std::uint32_t>(items.size());
     const std::uint64_t block = static_cast<std::uint64_t>(chunk) * world + rank;
     const std::uint64_t lo = std::min<std::uint64_t>(n, block * c->block_rows);
     const std::uint64_t hi = std::min<std::uint64_t>(n, (block + 1) * c->block_rows);
-    for (std::uint32_t v = static_cast<std::uint32_t>(lo); v < hi; ++v) {
-      const std::uint32_t deg = rowptr[v + 1] - rowptr[v];
-      const std::uint32_t pieces = std::max(1u, (deg + c->chunk_entries - 1) / c->chunk_entries);
-      std::uint32_t hub = kNoHub;
-      if (pieces > 1) {
-        hub = static_cast<std::uint32_t>(hub_first.size());
-        hub_first.push_back(parts);
-        hub_items.push_back(pieces);
-        parts += pieces;
-      }
-      for (std::uint32_t p = 0; p < pieces; ++p) {
-        ItemDesc it{};
-        it.u = v;
-        it.off_a = rowptr[v] + p * c->chunk_entries;
-        it.len_a = std::min(it.off_a + c->chunk_entries, rowptr[v + 1]) - it.off_a;
-        // own samples: one slot per adjacency position (PER_EDGE_2), or the vertex's k slots on its first item
-        it.off_b = per_edge ? it.off_a : v * c->opt.negatives;
-        it.len_b = per_edge ? it.len_a : (p == 0 ? c->opt.negatives : 0u);
-        it.first = p == 0;
-        it.hub = hub;
-        it.sub = p;
-        items.push_back(it);
-      }
+    const unsigned threads = hi - lo < (1u << 16) ? 1u : std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
+    struct Part { std::uint64_t lo, hi; std::size_t items, hubs; std::uint32_t slices; };
+    std::vector<Part> part(threads);
+    for (unsigned t = 0; t < threads; ++t) {
+      part[t] = Part{lo + (hi - lo) * t / threads, lo + (hi - lo) * (t + 1) / threads, 0, 0, 0};
     }
+    auto run = [&](auto&& fn) {
+      std::vector<std::thread> pool;
+      for (unsigned t = 1; t < threads; ++t) pool.emplace_back(fn, t);
+      fn(0u);
+      for (auto& th : pool) th.join();
+    };
+    run([&](unsigned t) {
+      Part& p = part[t];
+      for (std::uint64_t v = p.lo; v < p.hi; ++v) {
+        const std::uint32_t pieces = pieces_of(static_cast<std::uint32_t>(v));
+        p.items += pieces;
+        if (pieces > 1) {
+          ++p.hubs;
+          p.slices += pieces;
+        }
+      }
+    });
+    std::vector<std::size_t> item_at(threads), hub_at(threads);
+    std::vector<std::uint32_t> slice_at(threads);
+    std::size_t item_total = items.size(), hub_total = hub_first.size();
+    for (unsigned t = 0; t < threads; ++t) {
+      item_at[t] = item_total;
+      hub_at[t] = hub_total;
+      slice_at[t] = parts;
+      item_total += part[t].items;
+      hub_total += part[t].hubs;
+      parts += part[t].slices;
+    }
+    items.resize(item_total);
+    hub_first.resize(hub_total);
+    hub_items.resize(hub_total);
+    run([&](unsigned t) {
+      std::size_t at = item_at[t], hub_next = hub_at[t];
+      std::uint32_t slice_next = slice_at[t];
+      for (std::uint64_t vv = part[t].lo; vv < part[t].hi; ++vv) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv), pieces = pieces_of(v);
+        std::uint32_t hub = kNoHub;
+        if (pieces > 1) {
+          hub = static_cast<std::uint32_t>(hub_next);
+          hub_first[hub_next] = slice_next;
+          hub_items[hub_next] = pieces;
+          ++hub_next;
+          slice_next += pieces;
+        }
+        for (std::uint32_t p = 0; p < pieces; ++p) {
+          ItemDesc it{};
+          it.u = v;
+          it.off_a = rowptr[v] + p * chunk_entries;
+          it.len_a = std::min(it.off_a + chunk_entries, rowptr[v + 1]) - it.off_a;
+          // own samples: one slot per adjacency position (PER_EDGE_2), or the vertex's k slots on its first item
+          it.off_b = per_edge ? it.off_a : v * negatives;
+          it.len_b = per_edge ? it.len_a : (p == 0 ? negatives : 0u);
+          it.first = p == 0;
+          it.hub = hub;
+          it.sub = p;
+          items[at++] = it;
+        }
+      }
+    });
   }
   c->chunk_item_off[c->comm_chunks] = static_cast<std::uint32_t>(items.size());
   // d <= 4 runs one THREAD per item: items of similar length are put next to each other (longest first) inside every
